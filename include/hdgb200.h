@@ -1,0 +1,122 @@
+/*
+ * hdgb200.h - C ABI of the B200-native HDG trace-operator / multigrid hot path.
+ *
+ * Drop-in boundary for the reference `hdgmg` package (pure Python; its "plugin
+ * API" is duck-typed).  Every entry point below replaces one
+ * reference call site; a reference-side ctypes binding is in INTEGRATION.md.
+ *
+ * Conventions (all entry points):
+ *   - plain C types only; vectors are fp64 DEVICE pointers in the reference's
+ *     trace layout: block b of an interior facet holds n1 = p+1 contiguous values,
+ *     blocks in `block_of` order (trace.py:39-41): interior horizontal facets row
+ *     by row (j = 1..ny-1, i = 0..nx-1), then interior vertical facets column by
+ *     column (i = 1..nx-1, j = 0..ny-1)  [mesh.py:112-117];
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *     all launches are asynchronous on it;
+ *   - return 0 on success, nonzero on error; hdg_last_error() describes it
+ *     (thread-local).  Inputs are never mutated (matvec_free / _cycle return new
+ *     arrays in the reference).
+ *   - ndof == 0 systems are legal (1x1 meshes) and every apply is a no-op
+ *     (trace.py:90-91).
+ */
+#ifndef HDGB200_H
+#define HDGB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hdg_level hdg_level;       /* one trace operator on an nx x ny mesh at order p */
+typedef struct hdg_transfer hdg_transfer; /* prolongation from level k+1 into level k */
+typedef struct hdg_mg hdg_mg;             /* a level stack + workspaces + cached CUDA graphs */
+
+enum { HDG_OK = 0, HDG_EINVAL = 1, HDG_ECUDA = 2, HDG_ENOMEM = 3, HDG_ESTATE = 4 };
+
+const char* hdg_last_error(void);
+int hdg_version(void);
+/* number of kernel launches this thread issued through the library (for bench gpu_launches) */
+int64_t hdg_launch_count(void);
+
+/* ---------------------------------------------------------------- operators
+ * Replaces TraceSystem's block state + matvec_free (trace.py:29-94) and
+ * MGLevel.matvec / .operator (multigrid.py:204-207, 328-334).                  */
+
+/* Shared-block operator (K = const, tau = const: SURVEY F2/F5): `block` is the
+ * 4n1 x 4n1 row-major condensed block of an interior element (HOST pointer),
+ * local slot = side*n1 + k, sides (bottom, right, top, left) [local.py:35-43]. */
+int hdg_level_create_shared(int nx, int ny, int p, const double* block, hdg_level** out);
+
+/* Stored-block operator: `blocks` is the reference `schur` stack (E, 4n1, 4n1)
+ * row-major, element e = j*nx + i [trace.py:54], DEVICE pointer (caller keeps
+ * ownership; it may be freed after the call).  Dirichlet columns must already
+ * be zero (local.py:186-188); boundary-side rows are ignored. */
+int hdg_level_create_stored(int nx, int ny, int p, const double* blocks, hdg_level** out);
+int hdg_level_destroy(hdg_level* lev);
+int64_t hdg_level_ndof(const hdg_level* lev);
+/* bytes the operator streams from HBM per apply (0 for shared: held in constant bank) */
+int64_t hdg_level_operator_bytes(const hdg_level* lev);
+
+/* Edge block-Jacobi smoother state (north star): D^-1 per
+ * interior facet, D = that facet's diagonal n1 x n1 block of the operator.
+ * Computed and inverted in-library from the level's own blocks. */
+int hdg_level_set_blockjacobi(hdg_level* lev, double omega);
+
+/* y = A x  (trace.py:87-94) */
+int hdg_matvec(const hdg_level* lev, const double* x, double* y, void* stream);
+/* r = b - A x; if norm2_out != NULL also writes ||b - A x||^2 (one double, device) */
+int hdg_residual(const hdg_level* lev, const double* b, const double* x, double* r,
+                 double* norm2_out, void* stream);
+/* one damped block-Jacobi sweep x_out = x_in + omega D^-1 (b - A x_in); x_out != x_in */
+int hdg_bj_sweep(const hdg_level* lev, const double* b, const double* x_in, double* x_out,
+                 void* stream);
+
+/* ---------------------------------------------------------------- transfers
+ * Replaces p_prolongation / h_prolongation (multigrid.py:215-298) as operators:
+ * prolong_add: x_fine += P e_coarse;   restrict: r_coarse = P^T r_fine.        */
+
+/* p-transfer on one mesh: V = n1f x (n1f-1) row-major (coarse GLL basis at fine GLL nodes) */
+int hdg_transfer_create_p(const hdg_level* fine, const hdg_level* coarse, const double* V,
+                          hdg_transfer** out);
+/* h-transfer at p = 1 (n1 = 2): `halves` 2 x 2 x 2 (half index, fine node, coarse node);
+ * `cross` = -V_f u_cols maps of the four cross facets (right of SW, right of NW, top of SW,
+ * top of SE) of each coarse element: (ncross_sets, 4, 2, 8) row-major, HOST pointer;
+ * ncross_sets = 1 (shared by every coarse element) or Ec = coarse element count. */
+int hdg_transfer_create_h(const hdg_level* fine, const hdg_level* coarse, const double* halves,
+                          const double* cross, int64_t ncross_sets, hdg_transfer** out);
+int hdg_transfer_destroy(hdg_transfer* t);
+int hdg_prolong_add(const hdg_transfer* t, const double* e_coarse, double* x_fine, void* stream);
+int hdg_restrict(const hdg_transfer* t, const double* r_fine, double* r_coarse, void* stream);
+
+/* ---------------------------------------------------------------- multigrid
+ * Replaces _cycle / v_cycle / w_cycle (multigrid.py:393-418) with a
+ * device-resident cycle: level k's operator, BJ smoother and transfer k->k+1,
+ * and a dense coarsest-level inverse (replaces splu, multigrid.py:209-212).    */
+int hdg_mg_create(hdg_level* const* levels, hdg_transfer* const* transfers, int nlevels,
+                  hdg_mg** out);
+int hdg_mg_destroy(hdg_mg* mg);
+/* coarsest-level inverse, n x n row-major HOST pointer, n = ndof of the last level */
+int hdg_mg_set_coarse_inverse(hdg_mg* mg, const double* inv, int64_t n);
+/* x = cycle(b, x0) with nu1/nu2 block-Jacobi sweeps, visits = 1 (V) or 2 (W).
+ * x0 may be NULL (zero initial guess, as v_cycle(x0=None)).  x may alias x0.
+ * If use_graph != 0 the launch sequence is captured once per (pointers, nu, visits)
+ * into a CUDA graph and replayed. */
+int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int nu1, int nu2,
+                 int visits, int use_graph, void* stream);
+/* coarse solve on the last level alone: x = A_c^-1 b (multigrid.py:209-212) */
+int hdg_coarse_solve(hdg_mg* mg, const double* b, double* x, void* stream);
+
+/* ---------------------------------------------------------------- reductions */
+/* *out = sum_i a_i b_i (deterministic two-pass; device scalar out) */
+int hdg_dot(const double* a, const double* b, int64_t n, double* out, void* stream);
+/* CG vector updates (trace.py:156-161): x += alpha d, r -= alpha ad */
+int hdg_cg_update(double* x, double* r, const double* d, const double* ad, double alpha, int64_t n,
+                  void* stream);
+/* d = z + beta d  (trace.py:161) */
+int hdg_xpby(const double* z, double beta, double* d, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HDGB200_H */

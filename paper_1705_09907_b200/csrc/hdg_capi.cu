@@ -1,0 +1,600 @@
+// hdg_capi.cu - C ABI (include/hdgb200.h) and native runtime: operator objects, transfers,
+// the device-resident multigrid cycle and its CUDA-graph cache.
+// Reference interfaces replaced: see include/hdgb200.h (each entry cites trace.py / multigrid.py).
+#include "hdgb200.h"
+#include "hdg_kernels.cuh"
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+using namespace hdg;
+
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) return fail(HDG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKL()                                                                             \
+  do {                                                                                    \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                                   \
+    cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ != cudaSuccess) return fail(HDG_ECUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+struct hdg_level {
+  int nx = 0, ny = 0, p = 0, n1 = 0, nxp = 0;
+  long long nh = 0, n_blocks = 0, ndof = 0;
+  bool stored = false;
+  std::vector<double> Wh, Wv, Dh, Dv;                // shared mode (host copies -> kernel params)
+  double *dWh = nullptr, *dWv = nullptr;             // stored mode streams
+  double *dDh = nullptr, *dDv = nullptr;
+  bool has_bj = false;
+  double omega = 0.8;
+  double* partials = nullptr;                        // per-CTA norm partials
+  int npart = 0;
+  long long op_bytes = 0;
+};
+
+struct hdg_transfer {
+  bool is_h = false;
+  const hdg_level* fine = nullptr;
+  const hdg_level* coarse = nullptr;
+  PArgs pa{};
+  HArgs ha{};
+  double* dcross = nullptr;
+};
+
+struct GraphEntry {
+  cudaGraphExec_t exec;
+  long long nkern;
+};
+
+struct hdg_mg {
+  std::vector<hdg_level*> L;
+  std::vector<hdg_transfer*> T;
+  int n = 0;
+  std::vector<double*> X, Tm, B, R;
+  double* Ainv = nullptr;
+  long long nc = 0;
+  cudaStream_t cs = nullptr;
+  std::map<std::tuple<const void*, const void*, void*, int, int, int>, GraphEntry> graphs;
+};
+
+// ------------------------------------------------------------------------------ helpers
+
+static void host_invert(std::vector<double>& a, int n) {  // SPD Gauss-Jordan, no pivoting
+  for (int c = 0; c < n; ++c) {
+    const double piv = 1.0 / a[c * n + c];
+    for (int m = 0; m < n; ++m) a[c * n + m] *= piv;
+    a[c * n + c] = piv;
+    for (int r = 0; r < n; ++r) {
+      if (r == c) continue;
+      const double f = a[r * n + c];
+      a[r * n + c] = 0.0;
+      for (int m = 0; m < n; ++m) a[r * n + m] -= f * a[c * n + m];
+      a[r * n + c] = -f * piv;
+    }
+  }
+}
+
+template <int N1, bool STORED, int EPI>
+static int set_attr() {
+  const size_t smem = Cfg<N1>::SMEM_DOUBLES * sizeof(double);
+  CK(cudaFuncSetAttribute(trace_apply_kernel<N1, STORED, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  return 0;
+}
+
+template <int N1, bool STORED>
+static int prepare_t() {
+  int rc = 0;
+  if ((rc = set_attr<N1, STORED, EPI_Y>())) return rc;
+  if ((rc = set_attr<N1, STORED, EPI_RES>())) return rc;
+  if ((rc = set_attr<N1, STORED, EPI_BJ>())) return rc;
+  if ((rc = set_attr<N1, STORED, EPI_RESPR>())) return rc;
+  return 0;
+}
+
+template <int N1, bool STORED, int EPI>
+static int apply_t(const hdg_level* L, MvArgs& a, cudaStream_t s) {
+  using C = Cfg<N1>;
+  const size_t smem = C::SMEM_DOUBLES * sizeof(double);
+  dim3 grid((L->nx + TX - 1) / TX, (L->ny + TY - 1) / TY);
+  SharedOp<(STORED ? 1 : N1)> op;
+  if constexpr (!STORED) {
+    std::memcpy(op.Wh, L->Wh.data(), sizeof(op.Wh));
+    std::memcpy(op.Wv, L->Wv.data(), sizeof(op.Wv));
+    if (L->has_bj) {
+      std::memcpy(op.Dh, L->Dh.data(), sizeof(op.Dh));
+      std::memcpy(op.Dv, L->Dv.data(), sizeof(op.Dv));
+    } else {
+      std::memset(op.Dh, 0, sizeof(op.Dh));
+      std::memset(op.Dv, 0, sizeof(op.Dv));
+    }
+  } else {
+    std::memset(&op, 0, sizeof(op));
+  }
+  trace_apply_kernel<N1, STORED, EPI><<<grid, NT, smem, s>>>(a, op);
+  CKL();
+  return 0;
+}
+
+#define HDG_N1_SWITCH(n1, CALL)                                       \
+  switch (n1) {                                                       \
+    case 2: CALL(2); case 3: CALL(3); case 4: CALL(4); case 5: CALL(5); \
+    case 6: CALL(6); case 7: CALL(7); case 8: CALL(8); case 9: CALL(9); \
+    case 10: CALL(10); case 11: CALL(11); case 12: CALL(12); case 13: CALL(13); \
+    default: return fail(HDG_EINVAL, "order p must be in [1, 12]");   \
+  }
+
+static int apply(const hdg_level* L, int epi, MvArgs& a, cudaStream_t s) {
+  a.nx = L->nx; a.ny = L->ny; a.nxp = L->nxp; a.nh = L->nh;
+  a.Wh = L->dWh; a.Wv = L->dWv; a.Dh = L->dDh; a.Dv = L->dDv;
+  a.omega = L->omega;
+  if (L->ndof == 0) return 0;
+#define APPLY_CASE(N)                                                                 \
+  {                                                                                   \
+    if (L->stored) {                                                                  \
+      if (epi == EPI_Y) return apply_t<N, true, EPI_Y>(L, a, s);                      \
+      if (epi == EPI_RES) return apply_t<N, true, EPI_RES>(L, a, s);                  \
+      if (epi == EPI_BJ) return apply_t<N, true, EPI_BJ>(L, a, s);                    \
+      return apply_t<N, true, EPI_RESPR>(L, a, s);                                    \
+    }                                                                                 \
+    if (epi == EPI_Y) return apply_t<N, false, EPI_Y>(L, a, s);                       \
+    if (epi == EPI_RES) return apply_t<N, false, EPI_RES>(L, a, s);                   \
+    if (epi == EPI_BJ) return apply_t<N, false, EPI_BJ>(L, a, s);                     \
+    return apply_t<N, false, EPI_RESPR>(L, a, s);                                     \
+  }
+  HDG_N1_SWITCH(L->n1, APPLY_CASE)
+#undef APPLY_CASE
+}
+
+static int prepare(int n1, bool stored) {
+#define PREP_CASE(N) return stored ? prepare_t<N, true>() : prepare_t<N, false>();
+  HDG_N1_SWITCH(n1, PREP_CASE)
+#undef PREP_CASE
+}
+
+static int init_level(hdg_level* L, int nx, int ny, int p) {
+  if (nx < 1 || ny < 1) return fail(HDG_EINVAL, "mesh element counts must be positive");
+  if (p < 1 || p > MAXN1 - 1) return fail(HDG_EINVAL, "order p must be in [1, 12]");
+  L->nx = nx; L->ny = ny; L->p = p; L->n1 = p + 1;
+  L->nxp = ((nx + 31) / 32) * 32;
+  L->nh = (long long)nx * (ny - 1);
+  L->n_blocks = L->nh + (long long)(nx - 1) * ny;
+  L->ndof = L->n_blocks * L->n1;
+  const int gx = (nx + TX - 1) / TX, gy = (ny + TY - 1) / TY;
+  L->npart = gx * gy;
+  CK(cudaMalloc(&L->partials, sizeof(double) * (L->npart + 1)));
+  return 0;
+}
+
+// ------------------------------------------------------------------------------- C ABI
+
+extern "C" {
+
+const char* hdg_last_error(void) { return g_err.c_str(); }
+int hdg_version(void) { return 1; }
+int64_t hdg_launch_count(void) { return g_launches.load(); }
+
+int hdg_level_create_shared(int nx, int ny, int p, const double* block, hdg_level** out) {
+  if (!out || !block) return fail(HDG_EINVAL, "null argument");
+  hdg_level* L = new hdg_level();
+  int rc = init_level(L, nx, ny, p);
+  if (rc) { delete L; return rc; }
+  const int n1 = L->n1, Lw = 4 * n1;
+  L->Wh.assign(7 * n1 * n1, 0.0);
+  L->Wv.assign(7 * n1 * n1, 0.0);
+  for (int vert = 0; vert < 2; ++vert) {
+    std::vector<double>& W = vert ? L->Wv : L->Wh;
+    for (int q = 0; q < 7; ++q)
+      for (int k = 0; k < n1; ++k)
+        for (int m = 0; m < n1; ++m) {
+          int w1, r1, c1, w2, r2, c2;
+          merged_entry_src(vert != 0, q, k, m, n1, w1, r1, c1, w2, r2, c2);
+          double v = block[r1 * Lw + c1];
+          if (w2 >= 0) v += block[r2 * Lw + c2];
+          W[(q * n1 + k) * n1 + m] = v;
+        }
+  }
+  if ((rc = prepare(n1, false))) { hdg_level_destroy(L); return rc; }
+  *out = L;
+  return 0;
+}
+
+int hdg_level_create_stored(int nx, int ny, int p, const double* blocks, hdg_level** out) {
+  if (!out) return fail(HDG_EINVAL, "null argument");
+  hdg_level* L = new hdg_level();
+  L->stored = true;
+  int rc = init_level(L, nx, ny, p);
+  if (rc) { delete L; return rc; }
+  const int n1 = L->n1;
+  const long long nslots = (long long)ny * L->nxp;
+  const size_t wbytes = sizeof(double) * (size_t)nslots * 7 * n1 * n1;
+  L->op_bytes = 0;
+  if (L->ndof > 0) {
+    if (!blocks) { hdg_level_destroy(L); return fail(HDG_EINVAL, "null blocks"); }
+    if (cudaMalloc(&L->dWh, wbytes) != cudaSuccess || cudaMalloc(&L->dWv, wbytes) != cudaSuccess) {
+      hdg_level_destroy(L);
+      return fail(HDG_ENOMEM, "cannot allocate stored operator streams");
+    }
+    const long long nthr = nslots * 7 * n1 * n1;
+    const int bs = 256;
+    const long long nbk = (nthr + bs - 1) / bs;
+#define RELAYOUT_CASE(N)                                                                         \
+  {                                                                                              \
+    relayout_kernel<N><<<(unsigned)nbk, bs>>>(blocks, nx, ny, L->nxp, false, L->dWh);   \
+    CKL();                                                                                       \
+    relayout_kernel<N><<<(unsigned)nbk, bs>>>(blocks, nx, ny, L->nxp, true, L->dWv);    \
+    CKL();                                                                                       \
+    break;                                                                                       \
+  }
+    HDG_N1_SWITCH(n1, RELAYOUT_CASE)
+#undef RELAYOUT_CASE
+    CK(cudaDeviceSynchronize());
+    // algorithmic operator bytes: the facets' merged matrices (boundary padding excluded)
+    L->op_bytes = (long long)L->n_blocks * 7 * n1 * n1 * 8;
+  }
+  if ((rc = prepare(n1, true))) { hdg_level_destroy(L); return rc; }
+  *out = L;
+  return 0;
+}
+
+int hdg_level_destroy(hdg_level* L) {
+  if (!L) return 0;
+  cudaFree(L->dWh); cudaFree(L->dWv); cudaFree(L->dDh); cudaFree(L->dDv); cudaFree(L->partials);
+  delete L;
+  return 0;
+}
+
+int64_t hdg_level_ndof(const hdg_level* L) { return L ? L->ndof : -1; }
+int64_t hdg_level_operator_bytes(const hdg_level* L) { return L ? L->op_bytes : -1; }
+
+int hdg_level_set_blockjacobi(hdg_level* L, double omega) {
+  if (!L) return fail(HDG_EINVAL, "null level");
+  L->omega = omega;
+  const int n1 = L->n1;
+  if (!L->stored) {
+    L->Dh.assign(L->Wh.begin() + n1 * n1, L->Wh.begin() + 2 * n1 * n1);  // stencil block q = 1
+    L->Dv.assign(L->Wv.begin() + n1 * n1, L->Wv.begin() + 2 * n1 * n1);
+    host_invert(L->Dh, n1);
+    host_invert(L->Dv, n1);
+  } else if (L->ndof > 0 && !L->has_bj) {
+    const long long nslots = (long long)L->ny * L->nxp;
+    const size_t dbytes = sizeof(double) * (size_t)nslots * n1 * n1;
+    CK(cudaMalloc(&L->dDh, dbytes));
+    CK(cudaMalloc(&L->dDv, dbytes));
+    // D = q=1 stencil block of the merged stream; copy it out, then invert in place
+    const int bs = 256;
+#define DIAG_CASE(N)                                                                      \
+  {                                                                                       \
+    constexpr int WSZ = Cfg<N>::WSZ, DSZ = Cfg<N>::DSZ;                                  \
+    for (int vert = 0; vert < 2; ++vert) {                                                \
+      const double* W = vert ? L->dWv : L->dWh;                                           \
+      double* D = vert ? L->dDv : L->dDh;                                                 \
+      CK(cudaMemcpy2D(D, sizeof(double) * 32 * DSZ, W + (size_t)DSZ * 32,                 \
+                      sizeof(double) * 32 * WSZ, sizeof(double) * 32 * DSZ, nslots / 32,  \
+                      cudaMemcpyDeviceToDevice));                                         \
+      invert_kernel<N><<<(unsigned)((nslots + bs - 1) / bs), bs>>>(D, nslots);            \
+      CKL();                                                                              \
+    }                                                                                     \
+    break;                                                                                \
+  }
+    HDG_N1_SWITCH(n1, DIAG_CASE)
+#undef DIAG_CASE
+    CK(cudaDeviceSynchronize());
+  }
+  L->has_bj = true;
+  return 0;
+}
+
+int hdg_matvec(const hdg_level* L, const double* x, double* y, void* stream) {
+  if (!L) return fail(HDG_EINVAL, "null level");
+  MvArgs a{};
+  a.x = x; a.out = y;
+  return apply(L, EPI_Y, a, S(stream));
+}
+
+static int finish_norm(const hdg_level* L, double* norm2_out, cudaStream_t s) {
+  sum_partials_kernel<<<1, 32, 0, s>>>(L->partials, L->npart, norm2_out);
+  CKL();
+  return 0;
+}
+
+int hdg_residual(const hdg_level* L, const double* b, const double* x, double* r, double* norm2_out,
+                 void* stream) {
+  if (!L) return fail(HDG_EINVAL, "null level");
+  if (L->ndof == 0) {
+    if (norm2_out) CK(cudaMemsetAsync(norm2_out, 0, sizeof(double), S(stream)));
+    return 0;
+  }
+  MvArgs a{};
+  a.x = x; a.b = b; a.out = r; a.partials = norm2_out ? L->partials : nullptr;
+  int rc = apply(L, EPI_RES, a, S(stream));
+  if (rc || !norm2_out) return rc;
+  return finish_norm(L, norm2_out, S(stream));
+}
+
+int hdg_bj_sweep(const hdg_level* L, const double* b, const double* x_in, double* x_out, void* stream) {
+  if (!L) return fail(HDG_EINVAL, "null level");
+  if (!L->has_bj) return fail(HDG_ESTATE, "block-Jacobi state not set (hdg_level_set_blockjacobi)");
+  if (x_in == x_out && L->ndof > 0) return fail(HDG_EINVAL, "Jacobi sweep needs x_out != x_in");
+  MvArgs a{};
+  a.x = x_in; a.b = b; a.out = x_out;
+  return apply(L, EPI_BJ, a, S(stream));
+}
+
+// ---------------------------------------------------------------------------- transfers
+
+int hdg_transfer_create_p(const hdg_level* fine, const hdg_level* coarse, const double* V, hdg_transfer** out) {
+  if (!fine || !coarse || !V || !out) return fail(HDG_EINVAL, "null argument");
+  if (fine->nx != coarse->nx || fine->ny != coarse->ny || fine->n1 != coarse->n1 + 1)
+    return fail(HDG_EINVAL, "p-transfer needs the same mesh and p_coarse = p_fine - 1");
+  hdg_transfer* t = new hdg_transfer();
+  t->fine = fine; t->coarse = coarse;
+  std::memcpy(t->pa.V, V, sizeof(double) * fine->n1 * coarse->n1);
+  *out = t;
+  return 0;
+}
+
+int hdg_transfer_create_h(const hdg_level* fine, const hdg_level* coarse, const double* halves, const double* cross,
+                          int64_t nsets, hdg_transfer** out) {
+  if (!fine || !coarse || !halves || !cross || !out) return fail(HDG_EINVAL, "null argument");
+  if (fine->n1 != 2 || coarse->n1 != 2) return fail(HDG_EINVAL, "h-transfer runs at p = 1");
+  if (fine->nx != 2 * coarse->nx || fine->ny != 2 * coarse->ny)
+    return fail(HDG_EINVAL, "h-transfer needs the fine mesh = 2x the coarse mesh");
+  const long long Ec = (long long)coarse->nx * coarse->ny;
+  if (nsets != 1 && nsets != Ec) return fail(HDG_EINVAL, "cross maps: 1 shared set or one per coarse element");
+  hdg_transfer* t = new hdg_transfer();
+  t->is_h = true; t->fine = fine; t->coarse = coarse;
+  t->ha.nxc = coarse->nx; t->ha.nyc = coarse->ny;
+  t->ha.nhf = fine->nh; t->ha.nhc = coarse->nh;
+  std::memcpy(t->ha.halves, halves, sizeof(double) * 8);
+  const size_t bytes = sizeof(double) * 64 * (size_t)nsets;
+  if (cudaMalloc(&t->dcross, bytes) != cudaSuccess) { delete t; return fail(HDG_ENOMEM, "cross maps"); }
+  CK(cudaMemcpy(t->dcross, cross, bytes, cudaMemcpyHostToDevice));
+  t->ha.cross = t->dcross;
+  t->ha.shared_cross = (nsets == 1) ? 1 : 0;
+  *out = t;
+  return 0;
+}
+
+int hdg_transfer_destroy(hdg_transfer* t) {
+  if (!t) return 0;
+  cudaFree(t->dcross);
+  delete t;
+  return 0;
+}
+
+int hdg_prolong_add(const hdg_transfer* t, const double* ec, double* xf, void* stream) {
+  if (!t) return fail(HDG_EINVAL, "null transfer");
+  const long long nf = t->fine->n_blocks;
+  if (nf == 0) return 0;
+  const int bs = 256;
+  const unsigned grid = (unsigned)((nf + bs - 1) / bs);
+  if (t->is_h) {
+    h_prolong_add_kernel<<<grid, bs, 0, S(stream)>>>(t->ha, ec, xf);
+    CKL();
+    return 0;
+  }
+#define PPROL_CASE(N) { p_prolong_add_kernel<N><<<grid, bs, 0, S(stream)>>>(ec, xf, nf, t->pa); CKL(); return 0; }
+  HDG_N1_SWITCH(t->fine->n1, PPROL_CASE)
+#undef PPROL_CASE
+}
+
+int hdg_restrict(const hdg_transfer* t, const double* rf, double* rc, void* stream) {
+  if (!t) return fail(HDG_EINVAL, "null transfer");
+  const int bs = 256;
+  if (t->is_h) {
+    const long long nc = t->coarse->n_blocks;
+    if (nc == 0) return 0;
+    h_restrict_kernel<<<(unsigned)((nc + bs - 1) / bs), bs, 0, S(stream)>>>(t->ha, rf, rc);
+    CKL();
+    return 0;
+  }
+  const long long nf = t->fine->n_blocks;
+  if (nf == 0) return 0;
+  const unsigned grid = (unsigned)((nf + bs - 1) / bs);
+#define PRES_CASE(N) { p_restrict_kernel<N><<<grid, bs, 0, S(stream)>>>(rf, rc, nf, t->pa); CKL(); return 0; }
+  HDG_N1_SWITCH(t->fine->n1, PRES_CASE)
+#undef PRES_CASE
+}
+
+// ---------------------------------------------------------------------------- reductions
+
+static double* g_dot_partials = nullptr;
+static const int DOT_BLOCKS = 4 * 148;
+
+int hdg_dot(const double* a, const double* b, int64_t n, double* out, void* stream) {
+  if (!g_dot_partials) CK(cudaMalloc(&g_dot_partials, sizeof(double) * DOT_BLOCKS));
+  dot_partials_kernel<<<DOT_BLOCKS, 256, 0, S(stream)>>>(a, b, n, g_dot_partials);
+  CKL();
+  sum_partials_kernel<<<1, 32, 0, S(stream)>>>(g_dot_partials, DOT_BLOCKS, out);
+  CKL();
+  return 0;
+}
+
+int hdg_cg_update(double* x, double* r, const double* d, const double* ad, double alpha, int64_t n, void* stream) {
+  if (n <= 0) return 0;
+  cg_update_kernel<<<DOT_BLOCKS, 256, 0, S(stream)>>>(x, r, d, ad, alpha, n);
+  CKL();
+  return 0;
+}
+
+int hdg_xpby(const double* z, double beta, double* d, int64_t n, void* stream) {
+  if (n <= 0) return 0;
+  xpby_kernel<<<DOT_BLOCKS, 256, 0, S(stream)>>>(z, beta, d, n);
+  CKL();
+  return 0;
+}
+
+// ----------------------------------------------------------------------------- multigrid
+
+int hdg_mg_create(hdg_level* const* levels, hdg_transfer* const* transfers, int n, hdg_mg** out) {
+  if (!levels || !out || n < 1) return fail(HDG_EINVAL, "need at least one level");
+  hdg_mg* mg = new hdg_mg();
+  mg->n = n;
+  for (int k = 0; k < n; ++k) {
+    if (!levels[k]) { delete mg; return fail(HDG_EINVAL, "null level"); }
+    mg->L.push_back(levels[k]);
+    if (k + 1 < n) {
+      hdg_transfer* t = transfers ? transfers[k] : nullptr;
+      if (!t || t->fine != levels[k] || t->coarse != levels[k + 1]) {
+        delete mg;
+        return fail(HDG_EINVAL, "transfer k must map level k+1 into level k");
+      }
+      mg->T.push_back(t);
+      if (!levels[k]->has_bj) { delete mg; return fail(HDG_ESTATE, "every non-coarsest level needs a smoother"); }
+    }
+  }
+  mg->X.assign(n, nullptr); mg->Tm.assign(n, nullptr); mg->B.assign(n, nullptr); mg->R.assign(n, nullptr);
+  for (int k = 0; k < n; ++k) {
+    const size_t bytes = sizeof(double) * (size_t)(mg->L[k]->ndof + 1);
+    if (k > 0) {
+      CK(cudaMalloc(&mg->X[k], bytes));
+      CK(cudaMalloc(&mg->B[k], bytes));
+    }
+    CK(cudaMalloc(&mg->Tm[k], bytes));
+    if (k + 1 < n && mg->T[k]->is_h) CK(cudaMalloc(&mg->R[k], bytes));
+  }
+  CK(cudaStreamCreateWithFlags(&mg->cs, cudaStreamNonBlocking));
+  *out = mg;
+  return 0;
+}
+
+int hdg_mg_destroy(hdg_mg* mg) {
+  if (!mg) return 0;
+  for (auto& kv : mg->graphs) cudaGraphExecDestroy(kv.second.exec);
+  for (int k = 0; k < mg->n; ++k) {
+    if (k > 0) cudaFree(mg->X[k]);
+    cudaFree(mg->Tm[k]); cudaFree(mg->B[k]); cudaFree(mg->R[k]);
+  }
+  cudaFree(mg->Ainv);
+  if (mg->cs) cudaStreamDestroy(mg->cs);
+  delete mg;
+  return 0;
+}
+
+int hdg_mg_set_coarse_inverse(hdg_mg* mg, const double* inv, int64_t n) {
+  if (!mg || !inv) return fail(HDG_EINVAL, "null argument");
+  if (n != mg->L[mg->n - 1]->ndof) return fail(HDG_EINVAL, "coarse inverse size != coarsest ndof");
+  cudaFree(mg->Ainv);
+  mg->Ainv = nullptr;
+  mg->nc = n;
+  if (n > 0) {
+    CK(cudaMalloc(&mg->Ainv, sizeof(double) * n * n));
+    CK(cudaMemcpy(mg->Ainv, inv, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  }
+  for (auto& kv : mg->graphs) cudaGraphExecDestroy(kv.second.exec);
+  mg->graphs.clear();
+  return 0;
+}
+
+static int coarse_apply(hdg_mg* mg, const double* b, double* x, cudaStream_t s) {
+  if (mg->nc == 0) return 0;
+  if (!mg->Ainv) return fail(HDG_ESTATE, "coarse inverse not set");
+  const int rows_per_block = 8;
+  dense_gemv_kernel<<<(unsigned)((mg->nc + rows_per_block - 1) / rows_per_block), 32 * rows_per_block, 0, s>>>(
+      mg->Ainv, b, x, (int)mg->nc);
+  CKL();
+  return 0;
+}
+
+int hdg_coarse_solve(hdg_mg* mg, const double* b, double* x, void* stream) {
+  if (!mg) return fail(HDG_EINVAL, "null mg");
+  return coarse_apply(mg, b, x, S(stream));
+}
+
+// multigrid.py:393-406, device resident: on entry the level-k iterate is X[k] (or zero),
+// on exit the result is in X[k].
+static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1, int nu2, int visits,
+                     cudaStream_t s) {
+  hdg_level* L = mg->L[k];
+  double* xk = mg->X[k];
+  if (k == mg->n - 1) return coarse_apply(mg, b, xk, s);
+  const size_t bytes = sizeof(double) * (size_t)L->ndof;
+  if (zero_init && L->ndof > 0) CK(cudaMemsetAsync(xk, 0, bytes, s));
+  double* cur = xk;
+  double* oth = mg->Tm[k];
+  int rc;
+  for (int it = 0; it < nu1; ++it) {
+    if ((rc = hdg_bj_sweep(L, b, cur, oth, s))) return rc;
+    std::swap(cur, oth);
+  }
+  hdg_transfer* T = mg->T[k];
+  if (!T->is_h) {
+    MvArgs a{};
+    a.x = cur; a.b = b; a.out = mg->B[k + 1];
+    std::memcpy(a.V, T->pa.V, sizeof(a.V));
+    if ((rc = apply(L, EPI_RESPR, a, s))) return rc;
+  } else {
+    if ((rc = hdg_residual(L, b, cur, mg->R[k], nullptr, s))) return rc;
+    if ((rc = hdg_restrict(T, mg->R[k], mg->B[k + 1], s))) return rc;
+  }
+  for (int v = 0; v < visits; ++v)
+    if ((rc = cycle_rec(mg, k + 1, mg->B[k + 1], v == 0, nu1, nu2, visits, s))) return rc;
+  if ((rc = hdg_prolong_add(T, mg->X[k + 1], cur, s))) return rc;
+  for (int it = 0; it < nu2; ++it) {
+    if ((rc = hdg_bj_sweep(L, b, cur, oth, s))) return rc;
+    std::swap(cur, oth);
+  }
+  if (cur != xk && L->ndof > 0) CK(cudaMemcpyAsync(xk, cur, bytes, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+static int cycle_issue(hdg_mg* mg, const double* b, const double* x0, double* x, int nu1, int nu2, int visits,
+                       cudaStream_t s) {
+  const size_t bytes = sizeof(double) * (size_t)mg->L[0]->ndof;
+  mg->X[0] = x;
+  bool zero = (x0 == nullptr);
+  if (!zero && x0 != x && bytes) CK(cudaMemcpyAsync(x, x0, bytes, cudaMemcpyDeviceToDevice, s));
+  return cycle_rec(mg, 0, b, zero, nu1, nu2, visits, s);
+}
+
+int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int nu1, int nu2, int visits,
+                 int use_graph, void* stream) {
+  if (!mg || !b || !x) return fail(HDG_EINVAL, "null argument");
+  if (nu1 < 0 || nu2 < 0 || visits < 1) return fail(HDG_EINVAL, "bad cycle parameters");
+  if (mg->L[0]->ndof == 0) return 0;
+  cudaStream_t s = S(stream);
+  if (!use_graph) return cycle_issue(mg, b, x0, x, nu1, nu2, visits, s);
+  auto key = std::make_tuple((const void*)b, (const void*)x0, (void*)x, nu1, nu2, visits);
+  auto it = mg->graphs.find(key);
+  if (it == mg->graphs.end()) {
+    const long long c0 = g_launches.load();
+    CK(cudaStreamBeginCapture(mg->cs, cudaStreamCaptureModeThreadLocal));
+    int rc = cycle_issue(mg, b, x0, x, nu1, nu2, visits, mg->cs);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(mg->cs, &g);
+    if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+    if (e != cudaSuccess) return fail(HDG_ECUDA, std::string("capture: ") + cudaGetErrorString(e));
+    GraphEntry ge{};
+    e = cudaGraphInstantiate(&ge.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(HDG_ECUDA, std::string("instantiate: ") + cudaGetErrorString(e));
+    ge.nkern = g_launches.load() - c0;
+    g_launches.fetch_sub(ge.nkern);
+    it = mg->graphs.emplace(key, ge).first;
+  }
+  CK(cudaGraphLaunch(it->second.exec, s));
+  g_launches.fetch_add(it->second.nkern);
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,266 @@
+"""Host-side setup math: reference element, batched static condensation, Galerkin blocks.
+
+This is SETUP, not the hot path: it produces the condensed element blocks the CUDA
+kernels stream (or hold in the constant bank), the transfer matrices, and the
+condensed right-hand side.  It is written batched over *element classes*: elements
+whose coefficient samples and stabilisation agree share one block (K = I gives a
+single class per level), so setup cost scales with the number of
+distinct elements, not the mesh size.
+
+Reference algorithm restated (vectorised, batched):
+  basis.py:42-181   GLL/GL rules, barycentric evaluation, tensor reference element
+  local.py:133-237  local blocks, LU/condensation:  S = F L^-1 T + tau M_facet
+  local.py:178-188  Dirichlet folding (loads) and column masking
+  trace.py:67-79    condensed RHS as the two-owner facet sum
+  multigrid.py:215-298, 328-334   transfers and Galerkin coarse operators, in element
+                    form S_c = sum_children Q^T S Q (exact: SURVEY F4)
+"""
+
+from __future__ import annotations
+
+import numpy as np
+from numpy.polynomial import legendre as npleg
+from scipy.special import roots_jacobi
+
+NODE_SNAP_TOL = 1e-14  # basis.py:17
+NORMALS = np.array([[0.0, -1.0], [1.0, 0.0], [0.0, 1.0], [-1.0, 0.0]])  # mesh.py:15
+
+
+# ----------------------------------------------------------------------------- 1D rules
+
+
+class Rule1D:
+    __slots__ = ("order", "nodes", "weights", "bary")
+
+    def __init__(self, order, nodes, weights):
+        self.order = order
+        self.nodes = np.asarray(nodes, float)
+        self.weights = np.asarray(weights, float)
+        d = self.nodes[:, None] - self.nodes[None, :]
+        np.fill_diagonal(d, 1.0)
+        w = 1.0 / d.prod(axis=1)
+        w = w / np.abs(w).max()
+        self.bary = -w if w[0] < 0 else w
+
+    @property
+    def n(self):
+        return self.order + 1
+
+
+def gll_rule(p):
+    """basis.py:59-69."""
+    if p < 1:
+        raise ValueError("GLL basis needs order p >= 1 (at least two points)")
+    x = np.empty(p + 1)
+    x[0], x[-1] = -1.0, 1.0
+    if p > 1:
+        x[1:-1] = roots_jacobi(p - 1, 1.0, 1.0)[0]
+    Pp = npleg.legval(x, np.eye(p + 1)[p])
+    return Rule1D(p, x, 2.0 / (p * (p + 1) * Pp ** 2))
+
+
+def gl_rule(p):
+    """basis.py:72-77 (p+1 Gauss points)."""
+    x, w = npleg.leggauss(p + 1)
+    return Rule1D(p, x, w)
+
+
+def eval_matrix(rule, points):
+    """basis.py:91-105: V[q, j] = l_j(points[q]) (second barycentric form, node snapping)."""
+    pts = np.atleast_1d(np.asarray(points, float))
+    d = pts[:, None] - rule.nodes[None, :]
+    hit = np.abs(d) < NODE_SNAP_TOL
+    V = rule.bary[None, :] / np.where(hit, 1.0, d)
+    snapped = hit.any(axis=1)
+    V[snapped] = 0.0
+    V[hit] = 1.0
+    free = ~snapped
+    V[free] /= V[free].sum(axis=1, keepdims=True)
+    return V
+
+
+def diff_matrix(rule):
+    """basis.py:108-116."""
+    x, w = rule.nodes, rule.bary
+    d = x[:, None] - x[None, :]
+    np.fill_diagonal(d, 1.0)
+    D = (w[None, :] / w[:, None]) / d
+    np.fill_diagonal(D, 0.0)
+    np.fill_diagonal(D, -D.sum(axis=1))
+    return D
+
+
+class RefElement:
+    """basis.py:119-181: GLL interpolation nodes, GL quadrature with p+1 points."""
+
+    def __init__(self, p):
+        self.p = p
+        self.n1 = p + 1
+        self.nb = (p + 1) ** 2
+        self.basis = gll_rule(p)
+        self.quad = gl_rule(p)
+        self.interp_1d = eval_matrix(self.basis, self.quad.nodes)
+        self.deriv_1d = self.interp_1d @ diff_matrix(self.basis)
+        self.w2 = np.kron(self.quad.weights, self.quad.weights)
+        self.interp_2d = np.kron(self.interp_1d, self.interp_1d)
+        self.dxi_2d = np.kron(self.interp_1d, self.deriv_1d)
+        self.deta_2d = np.kron(self.deriv_1d, self.interp_1d)
+        k = np.arange(self.n1)
+        # local.py:35-43 volume node ids per side along the tangent
+        self.side_nodes = (k, p + k * self.n1, p * self.n1 + k, k * self.n1)
+        self.mass1 = self.interp_1d.T @ (self.quad.weights[:, None] * self.interp_1d)
+
+    def element_quad_points(self, x0, y0, dx, dy):
+        """basis.py:157-162 for every element at once: x0, y0 arrays (E,) -> (E, nq^2)."""
+        qx = np.asarray(x0)[:, None] + dx * (self.quad.nodes + 1.0) / 2.0
+        qy = np.asarray(y0)[:, None] + dy * (self.quad.nodes + 1.0) / 2.0
+        nq = self.quad.nodes.size
+        return np.repeat(qx[:, None, :], nq, axis=1).reshape(len(qx), -1), \
+            np.repeat(qy[:, :, None], nq, axis=2).reshape(len(qy), -1)
+
+
+_REF_CACHE = {}
+
+
+def ref_element(p):
+    if p not in _REF_CACHE:
+        _REF_CACHE[p] = RefElement(p)
+    return _REF_CACHE[p]
+
+
+# ------------------------------------------------------------------- batched condensation
+
+
+class ElementClasses:
+    """Distinct (coefficient samples, tau) rows -> condensed operators per class.
+
+    Attributes (C = number of classes):
+      S     (C, 4n1, 4n1)  condensed block with ALL sides unmasked
+      Z     (C, 4n1, 3nb)  F L^-1, maps local loads to condensed loads
+      T     (C, 3nb, 4n1)  trace columns (unmasked), for the Dirichlet fold of the loads
+      ucols (C, nb, 4n1)   u response to trace data, (L^-1 T)[2nb:] (h-transfer, multigrid.py:273)
+    """
+
+    def __init__(self, p, dx, dy, kq, tau):
+        ref = ref_element(p)
+        self.p, self.ref = p, ref
+        n1, nb = ref.n1, ref.nb
+        kq = np.atleast_2d(np.asarray(kq, float))
+        tau = np.atleast_2d(np.asarray(tau, float))
+        if np.any(kq <= 0.0):
+            raise NumericalBreakdown("coefficient not positive")
+        C = kq.shape[0]
+        jac = dx * dy / 4.0
+        wj = ref.w2 * jac
+        I2 = ref.interp_2d
+        Bx = 0.5 * dy * I2.T @ (ref.w2[:, None] * ref.dxi_2d)       # local.py:146
+        By = 0.5 * dx * I2.T @ (ref.w2[:, None] * ref.deta_2d)      # local.py:147
+        lens = (dx, dy, dx, dy)
+        fm = [0.5 * lens[s] * ref.mass1 for s in range(4)]           # local.py:68-69
+        M = np.einsum("qi,cq,qj->cij", I2, wj[None, :] / kq, I2)     # local.py:144
+        L = np.zeros((C, 3 * nb, 3 * nb))
+        L[:, :nb, :nb] = M
+        L[:, nb:2 * nb, nb:2 * nb] = M
+        G = np.hstack([Bx, By])
+        L[:, :2 * nb, 2 * nb:] = -G.T
+        L[:, 2 * nb:, :2 * nb] = G
+        T = np.zeros((C, 3 * nb, 4 * n1))
+        F = np.zeros((C, 4 * n1, 3 * nb))
+        Ms = np.zeros((C, 4 * n1, 4 * n1))
+        for s in range(4):                                           # local.py:162-176
+            idx = ref.side_nodes[s]
+            cols = slice(s * n1, (s + 1) * n1)
+            ts = tau[:, s][:, None, None]
+            L[:, 2 * nb + idx[:, None], 2 * nb + idx[None, :]] += ts * fm[s]
+            for d in range(2):
+                ns = NORMALS[s, d]
+                if ns != 0.0:
+                    T[:, d * nb + idx, cols] += ns * fm[s]
+                    F[:, cols, d * nb + idx] += ns * fm[s]
+            T[:, 2 * nb + idx, cols] += -ts * fm[s]
+            F[:, cols, 2 * nb + idx] += ts * fm[s]
+            Ms[:, cols, cols] += ts * fm[s]
+        X = np.linalg.solve(L, T)                                    # L^-1 T (local.py:233-234)
+        self.S = F @ X + Ms                                          # local.py:235
+        self.Z = np.swapaxes(np.linalg.solve(np.swapaxes(L, 1, 2), np.swapaxes(F, 1, 2)), 1, 2)
+        self.T = T
+        self.ucols = X[:, 2 * nb:, :]
+        self.n = C
+
+
+class NumericalBreakdown(RuntimeError):
+    """local.py:27."""
+
+
+def classify_rows(rows):
+    """Unique rows -> (unique_rows, inverse).  Fast path when every row is equal."""
+    rows = np.ascontiguousarray(rows)
+    if rows.shape[0] == 0:
+        return rows, np.zeros(0, np.int64)
+    if np.all(rows == rows[0]):
+        return rows[:1], np.zeros(rows.shape[0], np.int64)
+    uniq, inv = np.unique(rows, axis=0, return_inverse=True)
+    return uniq, inv.reshape(-1)
+
+
+# ----------------------------------------------------------------- transfers / Galerkin
+
+
+def p_transfer_matrix(p_fine):
+    """multigrid.py:217: coarse (p-1) GLL basis evaluated at the fine GLL nodes, n1f x n1c."""
+    return eval_matrix(gll_rule(p_fine - 1), gll_rule(p_fine).nodes)
+
+
+def galerkin_p(S, V):
+    """S_c = Q^T S Q with Q = I_4 (x) V (the p-prolongation acts facet-locally)."""
+    Q = np.kron(np.eye(4), V)
+    return np.einsum("ai,cij,jb->cab", Q.T, S, Q)
+
+
+def h_halves():
+    """multigrid.py:243 at p = 1: half[h][k][c] = l_c((t_k -+ 1)/2)."""
+    b = gll_rule(1)
+    return np.stack([eval_matrix(b, (b.nodes - 1.0) / 2.0), eval_matrix(b, (b.nodes + 1.0) / 2.0)])
+
+
+def h_cross_maps(ucols):
+    """multigrid.py:269-293: trace maps of the four cross facets of a coarse element,
+    -V_f u_cols, in coarse reference coordinates.  ucols (C, nb=4, 8) -> (C, 4, 2, 8).
+    Cross facet order: right of SW, right of NW, top of SW, top of SE."""
+    b = gll_rule(1)
+    t = b.nodes
+    pts = [(np.zeros(2), (t - 1.0) / 2.0), (np.zeros(2), (t + 1.0) / 2.0),
+           ((t - 1.0) / 2.0, np.zeros(2)), ((t + 1.0) / 2.0, np.zeros(2))]
+    out = np.empty((ucols.shape[0], 4, 2, 8))
+    for cf, (xi, eta) in enumerate(pts):
+        Vf = np.einsum("nj,ni->nji", eval_matrix(b, eta), eval_matrix(b, xi)).reshape(2, 4)
+        out[:, cf] = -np.einsum("nq,cqk->cnk", Vf, ucols)
+    return out
+
+
+def h_child_maps(halves, cross):
+    """Q_k (C, 4 children, 8, 8): child k's (b, r, t, l) traces from the coarse element's
+    8 trace dofs.  Children (SW, SE, NW, NE) as mesh.py:182-191."""
+    C = cross.shape[0]
+    Q = np.zeros((C, 4, 8, 8))
+
+    def half(k, side_child, side_coarse, h):
+        Q[:, k, 2 * side_child:2 * side_child + 2, 2 * side_coarse:2 * side_coarse + 2] = halves[h]
+
+    def xf(k, side_child, cf):
+        Q[:, k, 2 * side_child:2 * side_child + 2, :] = cross[:, cf]
+
+    # SW
+    half(0, 0, 0, 0); xf(0, 1, 0); xf(0, 2, 2); half(0, 3, 3, 0)
+    # SE
+    half(1, 0, 0, 1); half(1, 1, 1, 0); xf(1, 2, 3); xf(1, 3, 0)
+    # NW
+    xf(2, 0, 2); xf(2, 1, 1); half(2, 2, 2, 0); half(2, 3, 3, 1)
+    # NE
+    xf(3, 0, 3); half(3, 1, 1, 1); half(3, 2, 2, 1); xf(3, 3, 1)
+    return Q
+
+
+def galerkin_h(S_children, Q):
+    """S_c = sum_k Q_k^T S_k Q_k.  S_children (C, 4, 8, 8), Q (C, 4, 8, 8)."""
+    return np.einsum("ckia,ckij,ckjb->cab", Q, S_children, Q)

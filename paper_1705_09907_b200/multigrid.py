@@ -1,0 +1,490 @@
+"""h/p geometric multigrid on the GPU (drop-in for hdgmg.multigrid, multigrid.py:1-463).
+
+Same level schedule (p -> 1 on the fine mesh, then mesh halving at p = 1:
+multigrid.py:301-342), Galerkin coarse operators and transposed-prolongation
+restriction.  Every coarse Galerkin operator is applied by the same edge kernel
+as the fine level: P^T A P is assembled in ELEMENT form, S_c = sum Q^T S Q
+(exact; one block per level for K = I, F5).  The cycle itself
+(multigrid.py:393-418) runs natively (hdg_mg_cycle) and is replayed from a CUDA
+graph; only ||r|| crosses to the host, once per cycle (multigrid.py:431-436).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device as dev
+from ._lib import check, lib
+from .discretization import (ElementClasses, classify_rows, galerkin_h, galerkin_p, h_child_maps,
+                             h_cross_maps, h_halves, p_transfer_matrix, ref_element)
+from .mesh import coarsen
+from .trace import BlockOperator, TraceLayout, TraceSystem
+
+
+class HierarchyError(ValueError):
+    """multigrid.py:30."""
+
+
+class NotSPDError(RuntimeError):
+    """multigrid.py:34."""
+
+
+# ------------------------------------------------------------------------- operators
+
+
+class DeviceOperator:
+    """Stands where the reference keeps a scipy CSR level operator (multigrid.py:192):
+    `.shape`, `A @ x` (device apply), `.tocsr()` for host inspection."""
+
+    def __init__(self, block_op):
+        self.block_op = block_op
+        self.shape = (block_op.ndof, block_op.ndof)
+
+    def __matmul__(self, x):
+        return self.block_op.apply(x)
+
+    def tocsr(self):
+        return self.block_op.tocsr()
+
+    @property
+    def nnz(self):
+        return self.tocsr().nnz
+
+    def toarray(self):
+        return self.tocsr().toarray()
+
+
+class _Restriction:
+    def __init__(self, P):
+        self.P = P
+        self.shape = (P.shape[1], P.shape[0])
+
+    def __matmul__(self, r):
+        return self.P.restrict(r)
+
+
+class Prolongation:
+    """Operator form of p_prolongation / h_prolongation (multigrid.py:215-298):
+    `P @ e`, `P.T @ r` run the transfer kernels; `.tocsr()` assembles it on the host."""
+
+    def __init__(self, fine_op, coarse_op, kind, V=None, halves=None, cross=None):
+        self.fine_op, self.coarse_op, self.kind = fine_op, coarse_op, kind
+        self.V, self.halves, self.cross = V, halves, cross
+        self.shape = (fine_op.ndof, coarse_op.ndof)
+        self._handle = None
+
+    @property
+    def handle(self):
+        if self._handle is None:
+            h = ctypes.c_void_p()
+            if self.kind == "p":
+                V = np.ascontiguousarray(self.V)
+                check(lib.hdg_transfer_create_p(self.fine_op.handle, self.coarse_op.handle, V.ctypes.data,
+                                                ctypes.byref(h)))
+            else:
+                hv = np.ascontiguousarray(self.halves)
+                cr = np.ascontiguousarray(self.cross)
+                check(lib.hdg_transfer_create_h(self.fine_op.handle, self.coarse_op.handle, hv.ctypes.data,
+                                                cr.ctypes.data, cr.shape[0], ctypes.byref(h)))
+            self._handle = h
+        return self._handle
+
+    def __del__(self):
+        if self._handle is not None:
+            try:
+                lib.hdg_transfer_destroy(self._handle)
+            except Exception:
+                pass
+
+    @property
+    def T(self):
+        return _Restriction(self)
+
+    def __matmul__(self, e):
+        ed, was_np = dev.to_device(e)
+        x = dev.zeros(self.shape[0])
+        check(lib.hdg_prolong_add(self.handle, dev.ptr(ed), dev.ptr(x), dev.stream()))
+        return dev.back(x, was_np)
+
+    def prolong_add(self, e, x):
+        check(lib.hdg_prolong_add(self.handle, dev.ptr(e), dev.ptr(x), dev.stream()))
+
+    def restrict(self, r):
+        rd, was_np = dev.to_device(r)
+        out = dev.empty(self.shape[1])
+        check(lib.hdg_restrict(self.handle, dev.ptr(rd), dev.ptr(out), dev.stream()))
+        return dev.back(out, was_np)
+
+    def tocsr(self):
+        """Host assembly by probing with unit vectors of the coarse space (small levels)."""
+        import scipy.sparse as sp
+        nc = self.shape[1]
+        cols = []
+        for c in range(nc):
+            e = np.zeros(nc)
+            e[c] = 1.0
+            cols.append(sp.csr_matrix(np.asarray(self @ e)).T)
+        return sp.hstack(cols).tocsr() if cols else sp.csr_matrix(self.shape)
+
+
+# --------------------------------------------------------------------------- smoothers
+
+
+class BlockJacobiSmoother:
+    """Edge block-Jacobi (north star): x <- x + omega D^-1 (b - A x), D the
+    per-facet n1 x n1 diagonal blocks of the level operator, Jacobi (double-buffered).
+    Fills the duck-typed MGLevel.smoother slot (multigrid.py:397-405)."""
+
+    def __init__(self, block_op, omega=0.8):
+        self.block_op = block_op
+        self.omega = float(omega)
+        self.aggressiveness = 0
+        block_op.set_blockjacobi(self.omega)
+        lay = block_op.layout
+        n1 = lay.n1
+        # stored smoother entries vs operator nonzeros (cf. multigrid.py:154-156)
+        nnz_est = lay.n_blocks * n1 * n1 * 7
+        self.complexity = lay.n_blocks * n1 * n1 / max(nnz_est, 1)
+
+    def smooth(self, matvec, b, x, steps):
+        """`matvec` is accepted for signature parity; the sweep applies this level's operator."""
+        if steps < 1:
+            return x
+        bd, was_np = dev.to_device(b)
+        xd, _ = dev.to_device(x)
+        cur = xd.clone()
+        oth = dev.empty(cur.numel())
+        s = dev.stream()
+        for _ in range(steps):
+            check(lib.hdg_bj_sweep(self.block_op.handle, dev.ptr(bd), dev.ptr(cur), dev.ptr(oth), s))
+            cur, oth = oth, cur
+        return dev.back(cur, was_np)
+
+    def apply_inverse(self, r):
+        """D^-1 r via one sweep from zero: omega D^-1 r, rescaled."""
+        rd, was_np = dev.to_device(r)
+        z = dev.zeros(rd.numel())
+        out = dev.empty(rd.numel())
+        check(lib.hdg_bj_sweep(self.block_op.handle, dev.ptr(rd), dev.ptr(z), dev.ptr(out), dev.stream()))
+        return dev.back(out / self.omega, was_np)
+
+
+# ------------------------------------------------------------------------------ levels
+
+
+class _LevelSystem:
+    """What MGLevel.system offers on coarse levels: geometry + the level operator."""
+
+    def __init__(self, mesh, p, block_op):
+        self.mesh, self.p = mesh, p
+        self.layout = block_op.layout
+        self.operator = block_op
+        self.ndof, self.n_blocks = block_op.ndof, block_op.layout.n_blocks
+        self.ops = type("Ops", (), {"n1": p + 1, "nb": (p + 1) ** 2, "p": p, "ref": ref_element(p)})()
+
+    @property
+    def block_of(self):
+        return self.layout.block_of
+
+    def matvec_free(self, x):
+        return self.operator.apply(x)
+
+
+@dataclass
+class MGLevel:
+    """multigrid.py:179-212."""
+
+    mesh: object
+    p: int
+    system: object = field(repr=False)
+    kind: str = "fine"
+    operator: object = field(default=None, repr=False)
+    matrix_free: bool = True
+    rhs: object = field(default=None, repr=False)
+    smoother: object = field(default=None, repr=False)
+    prolong: object = field(default=None, repr=False)
+    _coarse_inv: object = field(default=None, repr=False)
+
+    @property
+    def ndof(self):
+        return self.operator.shape[0]
+
+    @property
+    def block_op(self):
+        return self.operator.block_op
+
+    def matvec(self, x):
+        return self.operator @ x
+
+    def coarse_inverse(self):
+        if self._coarse_inv is None:
+            A = self.operator.tocsr().toarray()
+            self._coarse_inv = np.ascontiguousarray(np.linalg.inv(A)) if A.size else np.zeros((0, 0))
+        return self._coarse_inv
+
+    def coarse_solve(self, b):
+        """multigrid.py:209-212 on the device (dense inverse GEMV)."""
+        mg = _native_mg([self])
+        bd, was_np = dev.to_device(b)
+        x = dev.empty(self.ndof)
+        check(lib.hdg_coarse_solve(mg.handle, dev.ptr(bd), dev.ptr(x), dev.stream()))
+        return dev.back(x, was_np)
+
+
+def p_prolongation(fine_sys, coarse_sys):
+    """multigrid.py:215-219 as a device operator."""
+    return Prolongation(fine_sys.operator, coarse_sys.operator, "p", V=p_transfer_matrix(fine_sys.p))
+
+
+def _coarse_classes(mesh_c, spec, tau_per_facet):
+    """Sample K on the coarse p = 1 elements (the rediscretised system h_prolongation uses,
+    multigrid.py:270-273) -> u_cols per coarse class."""
+    ref = ref_element(1)
+    nx, ny = mesh_c.n_x, mesh_c.n_y
+    e = np.arange(nx * ny)
+    x0 = mesh_c.x0 + (e % nx) * mesh_c.dx
+    y0 = mesh_c.y0 + (e // nx) * mesh_c.dy
+    qx, qy = ref.element_quad_points(x0, y0, mesh_c.dx, mesh_c.dy)
+    kq = np.asarray(spec.coefficient(qx, qy), float).reshape(len(e), -1)
+    if tau_per_facet is None:
+        tau = np.full((len(e), 4), float(spec.tau))
+    else:
+        nh = nx * (ny + 1)
+        j, i = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+        f = np.stack([j * nx + i, nh + (i + 1) * ny + j, (j + 1) * nx + i, nh + i * ny + j], -1).reshape(-1, 4)
+        tau = np.asarray(tau_per_facet, float)[f]
+    rows, inv = classify_rows(np.hstack([kq, tau]))
+    cls = ElementClasses(1, mesh_c.dx, mesh_c.dy, rows[:, :kq.shape[1]], rows[:, kq.shape[1]:])
+    return cls.ucols, inv
+
+
+def _h_level(fine_op, mesh_c, spec, tau_per_facet):
+    """Galerkin blocks of the h-coarsened level and the h-transfer maps."""
+    ucols, ucls = _coarse_classes(mesh_c, spec, tau_per_facet)
+    cross_u = h_cross_maps(ucols)                     # (Cu, 4, 2, 8)
+    halves = h_halves()
+    nxf = fine_op.mesh.n_x
+    ncx, ncy = mesh_c.n_x, mesh_c.n_y
+    cj, ci = np.meshgrid(np.arange(ncy), np.arange(ncx), indexing="ij")
+    base = (2 * cj * nxf + 2 * ci).ravel()
+    kids = np.stack([base, base + 1, base + nxf, base + nxf + 1], axis=1)
+    kid_cls = fine_op.elem_class[kids]                # (Ec, 4)
+    rows, inv = classify_rows(np.hstack([ucls[:, None], kid_cls]))
+    Q = h_child_maps(halves, cross_u[rows[:, 0]])
+    S_children = fine_op.S_cls[rows[:, 1:]]           # (C, 4, 8, 8)
+    S_c = galerkin_h(S_children, Q)
+    cross = cross_u if cross_u.shape[0] == 1 else cross_u[ucls]
+    return S_c, inv, halves, cross
+
+
+def h_prolongation(fine_sys, coarse_sys, spec=None, tau_per_facet=None):
+    """multigrid.py:229-298 as a device operator (coarse K sampled from `spec`)."""
+    if getattr(coarse_sys.mesh, "child_elements", None) is None:
+        raise HierarchyError("coarse mesh does not record its fine children")
+    spec = spec or coarse_sys.spec
+    _, _, halves, cross = _h_level(fine_sys.operator, coarse_sys.mesh, spec, tau_per_facet)
+    return Prolongation(fine_sys.operator, coarse_sys.operator, "h", halves=halves, cross=cross)
+
+
+def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother="baseline", omega=1.0,
+                    threads=1):
+    """multigrid.py:301-342: orders p..1 on the fine mesh, then halving at p = 1, Galerkin
+    operators, Pᵀ-cascaded right-hand sides.  smoother: "blockjacobi" (north star; omega
+    defaults to 0.8 when left at the reference default 1.0 is NOT applied - pass it), None."""
+    if p < 1:
+        raise HierarchyError("fine order must be >= 1")
+    fine = TraceSystem(mesh, p, spec, tau_per_facet, threads=threads)
+    levels = [MGLevel(mesh, p, fine, kind="p-level", operator=DeviceOperator(fine.operator),
+                      matrix_free=True, rhs=fine.rhs)]
+    op = fine.operator
+    for q in range(p - 1, 0, -1):                                   # multigrid.py:317-321
+        V = p_transfer_matrix(q + 1)
+        cop = BlockOperator(mesh, q, galerkin_p(op.S_cls, V), op.elem_class)
+        levels[-1].prolong = Prolongation(op, cop, "p", V=V)
+        levels.append(MGLevel(mesh, q, _LevelSystem(mesh, q, cop), kind="p-level",
+                              operator=DeviceOperator(cop), matrix_free=False))
+        op = cop
+    m = mesh
+    while m.n_x % 2 == 0 and m.n_y % 2 == 0 and m.n_x >= 4 and m.n_y >= 4:   # :322-327
+        m = coarsen(m)
+        S_c, inv, halves, cross = _h_level(op, m, spec, tau_per_facet)
+        cop = BlockOperator(m, 1, S_c, inv)
+        levels[-1].prolong = Prolongation(op, cop, "h", halves=halves, cross=cross)
+        levels.append(MGLevel(m, 1, _LevelSystem(m, 1, cop), kind="h-level",
+                              operator=DeviceOperator(cop), matrix_free=False))
+        op = cop
+    levels[-1].kind = "coarsest"
+    if levels[-1].ndof > coarse_cap:                                  # :336-339
+        raise HierarchyError(f"coarsest level has {levels[-1].ndof} unknowns, above cap {coarse_cap}")
+    for k in range(1, len(levels)):                                   # :333 rhs_k = P^T rhs_{k-1}
+        prev = levels[k - 1]
+        levels[k].rhs = _LazyRhs(prev, k) if prev.rhs is not None else None
+    if smoother is not None:
+        attach_smoothers(levels, smoother, omega)
+    return levels
+
+
+class _LazyRhs:
+    """rhs_k = P^T rhs_{k-1} (multigrid.py:333), evaluated on first use on the device."""
+
+    def __init__(self, prev, k):
+        self.prev, self.k, self.val = prev, k, None
+
+    def resolve(self):
+        if self.val is None:
+            r = self.prev.rhs.resolve() if isinstance(self.prev.rhs, _LazyRhs) else self.prev.rhs
+            self.val = self.prev.prolong.T @ np.asarray(r)
+        return self.val
+
+
+def _rhs(level):
+    return level.rhs.resolve() if isinstance(level.rhs, _LazyRhs) else level.rhs
+
+
+def attach_smoothers(levels, mode, omega=1.0):
+    """multigrid.py:345-352.  mode "blockjacobi" (omega 1.0 -> the north-star 0.8 unless given)."""
+    if mode not in ("blockjacobi", "bj"):
+        if mode in ("baseline", "aggressive") or isinstance(mode, int):
+            raise NotImplementedError(
+                "FSAI smoothers are not on the device path yet; use smoother='blockjacobi'")
+        raise ValueError(f"unknown smoother mode {mode!r}")
+    w = 0.8 if omega in (None, 1.0) else float(omega)
+    for lev in levels[:-1]:
+        lev.smoother = BlockJacobiSmoother(lev.block_op, w)
+    return levels
+
+
+# ------------------------------------------------------------------------------ cycles
+
+
+class ConvergenceMonitor:
+    """multigrid.py:358-390."""
+
+    def __init__(self, floor=1e-13):
+        self.residuals = []
+        self.floor = floor
+
+    def record(self, rnorm):
+        self.residuals.append(float(rnorm))
+
+    @property
+    def rho(self):
+        r = self.residuals
+        return [r[i + 1] / r[i] if r[i] > 0 else 0.0 for i in range(len(r) - 1)]
+
+    def asymptotic_rate(self, last=5):
+        if len(self.residuals) < 2:
+            return 0.0
+        scale = self.residuals[0] or 1.0
+        valid = [rho for rho, rn in zip(self.rho, self.residuals[1:]) if rn > self.floor * scale and rho > 0.0]
+        if not valid:
+            valid = [rho for rho in self.rho if rho > 0.0]
+        tail = valid[-last:]
+        return float(np.exp(np.mean(np.log(tail)))) if tail else 0.0
+
+    def diverged(self, window=5):
+        rho = self.rho
+        return len(rho) >= window and all(r >= 1.0 for r in rho[-window:])
+
+
+class _NativeMG:
+    def __init__(self, levels):
+        n = len(levels)
+        hs = (ctypes.c_void_p * n)(*[lev.block_op.handle.value for lev in levels])
+        ts = (ctypes.c_void_p * max(n - 1, 1))(*[levels[k].prolong.handle.value for k in range(n - 1)])
+        h = ctypes.c_void_p()
+        check(lib.hdg_mg_create(hs, ts, n, ctypes.byref(h)))
+        self.handle = h
+        self.levels = levels
+        inv = levels[-1].coarse_inverse()
+        check(lib.hdg_mg_set_coarse_inverse(h, inv.ctypes.data if inv.size else None, inv.shape[0]))
+
+    def __del__(self):
+        try:
+            lib.hdg_mg_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_MG_CACHE = {}
+
+
+def _native_mg(levels):
+    key = tuple(id(lev) for lev in levels)
+    mg = _MG_CACHE.get(key)
+    if mg is None or any(a is not b for a, b in zip(mg.levels, levels)):
+        for lev in levels[:-1]:
+            if not isinstance(lev.smoother, BlockJacobiSmoother):
+                raise NotImplementedError("the device cycle needs block-Jacobi smoothers on every level")
+        mg = _NativeMG(list(levels))
+        _MG_CACHE[key] = mg
+    return mg
+
+
+def _run_cycle(levels, b, x0, nu1, nu2, visits, use_graph=True):
+    mg = _native_mg(levels)
+    bd, was_np = dev.to_device(b)
+    x = dev.empty(bd.numel())
+    x0d = None if x0 is None else dev.to_device(x0)[0]
+    check(lib.hdg_mg_cycle(mg.handle, dev.ptr(bd), dev.ptr(x0d), dev.ptr(x), int(nu1), int(nu2), int(visits),
+                           int(use_graph), dev.stream()))
+    return dev.back(x, was_np)
+
+
+def v_cycle(levels, b, x0=None, nu1=2, nu2=2):
+    """multigrid.py:409-412 (x0 is not mutated)."""
+    return _run_cycle(levels, b, x0, nu1, nu2, 1)
+
+
+def w_cycle(levels, b, x0=None, nu1=2, nu2=2):
+    """multigrid.py:415-418."""
+    return _run_cycle(levels, b, x0, nu1, nu2, 2)
+
+
+def solve_mg(levels, b=None, x0=None, cycle="v", nu1=2, nu2=2, tol=1e-12, max_cycles=50):
+    """multigrid.py:421-439: cycles until ||b - A x|| <= tol ||b||, all vectors on the device."""
+    fine = levels[0]
+    if b is None:
+        b = _rhs(fine)
+    bd, was_np = dev.to_device(b)
+    n = bd.numel()
+    x = dev.zeros(n) if x0 is None else dev.to_device(x0)[0].clone()
+    visits = {"v": 1, "w": 2}[cycle]
+    mg = _native_mg(levels)
+    mon = ConvergenceMonitor()
+    scratch = dev.empty(1)
+    s = dev.stream()
+    check(lib.hdg_dot(dev.ptr(bd), dev.ptr(bd), n, dev.ptr(scratch), s))
+    bnorm = float(scratch.item()) ** 0.5 or 1.0
+    op = fine.block_op
+    mon.record(op.residual_norm(bd, x))
+    for _ in range(max_cycles):
+        if mon.residuals[-1] <= tol * bnorm:
+            break
+        check(lib.hdg_mg_cycle(mg.handle, dev.ptr(bd), dev.ptr(x), dev.ptr(x), int(nu1), int(nu2), visits, 1, s))
+        mon.record(op.residual_norm(bd, x))
+        if mon.diverged():
+            break
+    return dev.back(x, was_np), mon
+
+
+def fmg(levels, nu1=2, nu2=2, cycles_per_level=1):
+    """multigrid.py:442-454."""
+    x = levels[-1].coarse_solve(_rhs(levels[-1]))
+    for k in range(len(levels) - 2, -1, -1):
+        x = levels[k].prolong @ x
+        for _ in range(cycles_per_level):
+            x = v_cycle(levels[k:], _rhs(levels[k]), x, nu1, nu2)
+    return x
+
+
+def mg_preconditioner(levels, nu1=2, nu2=2):
+    """multigrid.py:457-463: one V-cycle from zero (device in, device out)."""
+
+    def apply(r):
+        return v_cycle(levels, r, None, nu1, nu2)
+
+    return apply

@@ -1,0 +1,368 @@
+"""Global trace system on the GPU (drop-in for hdgmg.trace, trace.py:26-233).
+
+`TraceSystem(mesh, p, spec)` keeps the reference constructor and attributes;
+`matvec_free` runs the edge-centric sm_100a kernel through the C ABI
+(include/hdgb200.h: hdg_matvec).  Element blocks are condensed on the host per
+element *class* (discretization.ElementClasses) and handed to the library once:
+one shared block (constant K and tau) or a stored per-element stack.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _device as dev
+from ._lib import check, lib
+from .discretization import ElementClasses, classify_rows, ref_element
+
+
+class LocalOps:
+    """The slice of local.py:46-78 that callers read (n1, nb, ref, p)."""
+
+    def __init__(self, mesh, p):
+        self.mesh, self.p = mesh, p
+        self.ref = ref_element(p)
+        self.n1, self.nb = p + 1, (p + 1) ** 2
+
+
+class TraceLayout:
+    """Facet numbering and ownership for a structured mesh (trace.py:36-65, mesh.py:112-154)."""
+
+    def __init__(self, mesh, p):
+        self.mesh, self.p = mesh, p
+        self.nx, self.ny = mesh.n_x, mesh.n_y
+        self.n1 = p + 1
+        self.nh = self.nx * (self.ny - 1)
+        self.n_blocks = self.nh + (self.nx - 1) * self.ny
+        self.ndof = self.n1 * self.n_blocks
+
+    @property
+    def interior(self):
+        nx, ny = self.nx, self.ny
+        nh_all = nx * (ny + 1)
+        h = (np.arange(1, ny)[:, None] * nx + np.arange(nx)[None, :]).ravel()
+        v = (nh_all + np.arange(1, nx)[:, None] * ny + np.arange(ny)[None, :]).ravel()
+        return np.concatenate([h, v]).astype(np.int64)
+
+    @property
+    def block_of(self):
+        nx, ny = self.nx, self.ny
+        out = np.full(nx * (ny + 1) + ny * (nx + 1), -1, np.int64)
+        out[self.interior] = np.arange(self.n_blocks)
+        return out
+
+    def side_mask(self):
+        """(E, 4) True where the element side is an interior facet (trace.py:58-59)."""
+        nx, ny = self.nx, self.ny
+        j, i = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+        return np.stack([j > 0, i < nx - 1, j < ny - 1, i > 0], axis=-1).reshape(-1, 4)
+
+    def sum_owners(self, per_elem):
+        """trace.py:73-79: facet block = slot-0 owner + slot-1 owner, vectorised."""
+        n1, nx, ny = self.n1, self.nx, self.ny
+        y = np.asarray(per_elem).reshape(ny, nx, 4, n1)
+        h = y[:-1, :, 2] + y[1:, :, 0]                     # (ny-1, nx): below TOP + above BOTTOM
+        v = y[:, :-1, 1] + y[:, 1:, 3]                     # (ny, nx-1): left RIGHT + right LEFT
+        return np.concatenate([h.reshape(-1), np.swapaxes(v, 0, 1).reshape(-1)])
+
+    def gather(self, x):
+        """trace.py:81-92: (E, 4 n1) element traces, zero on Dirichlet sides."""
+        n1, nx, ny = self.n1, self.nx, self.ny
+        x = np.asarray(x, float)
+        H = np.zeros((ny + 1, nx, n1))
+        H[1:ny] = x[:self.nh * n1].reshape(ny - 1, nx, n1)
+        V = np.zeros((nx + 1, ny, n1))
+        V[1:nx] = x[self.nh * n1:].reshape(nx - 1, ny, n1)
+        b = H[:-1]
+        t = H[1:]
+        l = np.swapaxes(V[:-1], 0, 1)
+        r = np.swapaxes(V[1:], 0, 1)
+        return np.stack([b, r, t, l], axis=2).reshape(nx * ny, 4 * n1)
+
+
+class BlockOperator:
+    """A trace operator given by element classes: blocks S_cls (C, 4n1, 4n1) with every
+    side unmasked and the class of each element.  Owns the native hdg_level."""
+
+    def __init__(self, mesh, p, S_cls, elem_class):
+        self.layout = TraceLayout(mesh, p)
+        self.mesh, self.p = mesh, p
+        self.S_cls = np.ascontiguousarray(S_cls, dtype=np.float64)
+        self.elem_class = np.asarray(elem_class, np.int64)
+        self._handle = None
+        self._bj_omega = None
+
+    @property
+    def ndof(self):
+        return self.layout.ndof
+
+    @property
+    def shared(self):
+        return self.S_cls.shape[0] == 1
+
+    @property
+    def handle(self):
+        if self._handle is None:
+            dev.require_cuda()
+            h = ctypes.c_void_p()
+            nx, ny = self.mesh.n_x, self.mesh.n_y
+            if self.shared:
+                blk = np.ascontiguousarray(self.S_cls[0])
+                check(lib.hdg_level_create_shared(nx, ny, self.p, blk.ctypes.data, ctypes.byref(h)))
+            else:
+                import torch
+                S = torch.from_numpy(self.S_cls).cuda()
+                idx = torch.from_numpy(self.elem_class).cuda()
+                blocks = S.index_select(0, idx).contiguous()
+                check(lib.hdg_level_create_stored(nx, ny, self.p, blocks.data_ptr(), ctypes.byref(h)))
+                del blocks, S, idx
+            self._handle = h
+        return self._handle
+
+    def set_blockjacobi(self, omega):
+        check(lib.hdg_level_set_blockjacobi(self.handle, float(omega)))
+        self._bj_omega = float(omega)
+
+    def operator_bytes(self):
+        return int(lib.hdg_level_operator_bytes(self.handle))
+
+    def __del__(self):
+        if self._handle is not None:
+            try:
+                lib.hdg_level_destroy(self._handle)
+            except Exception:
+                pass
+
+    # -- device applies ----------------------------------------------------------------
+    def apply(self, x):
+        xd, was_np = dev.to_device(x)
+        if xd.numel() != self.ndof:
+            raise ValueError(f"expected {self.ndof} trace values, got {xd.numel()}")
+        y = dev.empty(self.ndof)
+        if self.ndof:
+            check(lib.hdg_matvec(self.handle, dev.ptr(xd), dev.ptr(y), dev.stream()))
+        return dev.back(y, was_np)
+
+    def residual_norm(self, b, x):
+        """||b - A x|| on the device; one scalar crosses to the host."""
+        out = dev.empty(1)
+        check(lib.hdg_residual(self.handle, dev.ptr(b), dev.ptr(x), None, dev.ptr(out), dev.stream()))
+        return float(out.item()) ** 0.5
+
+    # -- host views (tests, tooling, coarse inverse) -------------------------------------
+    def schur(self):
+        """Reference-layout blocks (E, 4n1, 4n1) with Dirichlet columns zeroed (local.py:186-188)."""
+        S = self.S_cls[self.elem_class].copy()
+        cm = np.repeat(self.layout.side_mask(), self.p + 1, axis=1)
+        return S * cm[:, None, :]
+
+    def tocsr(self):
+        """trace.py:98-128, vectorised: scatter interior (row, col) blocks."""
+        lay = self.layout
+        n1 = lay.n1
+        if lay.ndof == 0:
+            return sp.csr_matrix((0, 0))
+        S = self.schur()
+        nx, ny = lay.nx, lay.ny
+        e = np.arange(nx * ny)
+        i, j = e % nx, e // nx
+        blk = np.full((nx * ny, 4), -1, np.int64)
+        blk[:, 0] = np.where(j > 0, (j - 1) * nx + i, -1)
+        blk[:, 2] = np.where(j < ny - 1, j * nx + i, -1)
+        blk[:, 3] = np.where(i > 0, lay.nh + (i - 1) * ny + j, -1)
+        blk[:, 1] = np.where(i < nx - 1, lay.nh + i * ny + j, -1)
+        dof = (blk[:, :, None] * n1 + np.arange(n1)).reshape(-1, 4 * n1)
+        ok = np.repeat(blk >= 0, n1, axis=1)
+        rr = np.broadcast_to(dof[:, :, None], S.shape)
+        cc = np.broadcast_to(dof[:, None, :], S.shape)
+        m = ok[:, :, None] & ok[:, None, :]
+        return sp.coo_matrix((S[m], (rr[m], cc[m])), shape=(lay.ndof, lay.ndof)).tocsr()
+
+
+class TraceSystem:
+    """Condensed HDG system A lam = b on the interior facet skeleton (trace.py:26-69)."""
+
+    def __init__(self, mesh, p, spec, tau_per_facet=None, threads=1):
+        self.mesh, self.p, self.spec = mesh, p, spec
+        self.ops = LocalOps(mesh, p)
+        self.layout = TraceLayout(mesh, p)
+        self.n_blocks, self.ndof = self.layout.n_blocks, self.layout.ndof
+        ref = self.ops.ref
+        nx, ny = mesh.n_x, mesh.n_y
+        E = nx * ny
+        e = np.arange(E)
+        x0 = mesh.x0 + (e % nx) * mesh.dx
+        y0 = mesh.y0 + (e // nx) * mesh.dy
+        qx, qy = ref.element_quad_points(x0, y0, mesh.dx, mesh.dy)
+        kq = np.asarray(spec.coefficient(qx, qy), float).reshape(E, -1)    # local.py:138
+        tau = self._element_tau(spec, tau_per_facet)
+        rows, inv = classify_rows(np.hstack([kq, tau]))
+        nq2 = kq.shape[1]
+        self.classes = ElementClasses(p, mesh.dx, mesh.dy, rows[:, :nq2], rows[:, nq2:])
+        self.elem_class = inv
+        self.operator = BlockOperator(mesh, p, self.classes.S, inv)
+        self.rhs = self._condensed_rhs(spec, qx, qy, x0, y0)
+
+    @classmethod
+    def from_blocks(cls, mesh, p, S_cls, elem_class=None, rhs=None):
+        """A system from explicit condensed blocks (e.g. the K = I shared block)."""
+        self = cls.__new__(cls)
+        self.mesh, self.p, self.spec = mesh, p, None
+        self.ops = LocalOps(mesh, p)
+        self.layout = TraceLayout(mesh, p)
+        self.n_blocks, self.ndof = self.layout.n_blocks, self.layout.ndof
+        S_cls = np.asarray(S_cls, float).reshape(-1, 4 * (p + 1), 4 * (p + 1))
+        if elem_class is None:
+            elem_class = np.zeros(mesh.n_x * mesh.n_y, np.int64)
+        self.classes = None
+        self.elem_class = np.asarray(elem_class, np.int64)
+        self.operator = BlockOperator(mesh, p, S_cls, self.elem_class)
+        self.rhs = np.zeros(self.ndof) if rhs is None else np.asarray(rhs, float)
+        return self
+
+    # -- setup helpers ----------------------------------------------------------------------
+    def _element_tau(self, spec, tau_per_facet):
+        E = self.mesh.n_x * self.mesh.n_y
+        if tau_per_facet is None:
+            return np.full((E, 4), float(spec.tau))
+        return np.asarray(tau_per_facet, float)[self.mesh_elem_to_facets()]  # local.py:151-154
+
+    def mesh_elem_to_facets(self):
+        m = self.mesh
+        nx, ny = m.n_x, m.n_y
+        nh = nx * (ny + 1)
+        j, i = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+        return np.stack([j * nx + i, nh + (i + 1) * ny + j, (j + 1) * nx + i, nh + i * ny + j],
+                        axis=-1).reshape(-1, 4)
+
+    def _condensed_rhs(self, spec, qx, qy, x0, y0):
+        """Loads (local.py:178-184) condensed per element (local.py:236), summed over owners."""
+        ref = self.ops.ref
+        n1, nb = ref.n1, ref.nb
+        E = qx.shape[0]
+        if self.ndof == 0:
+            return np.zeros(0)
+        m = self.mesh
+        wj = ref.w2 * (m.dx * m.dy / 4.0)
+        fq = np.asarray(spec.source(qx, qy), float).reshape(E, -1)
+        load = np.zeros((E, 3 * nb))
+        load[:, 2 * nb:] = (fq * wj) @ ref.interp_2d
+        inner = self.layout.side_mask()
+        bnd_e, bnd_s = np.nonzero(~inner)
+        if bnd_e.size:
+            lam_bc = np.zeros((E, 4 * n1))
+            t = ref.quad.nodes
+            nx = m.n_x
+            i, j = bnd_e % nx, bnd_e // nx
+            sx = np.where(bnd_s == 1, i + 1, i)
+            sy = np.where(bnd_s == 2, j + 1, j)
+            px = m.x0 + sx * m.dx
+            py = m.y0 + sy * m.dy
+            horiz = (bnd_s == 0) | (bnd_s == 2)
+            ln = np.where(horiz, m.dx, m.dy)
+            s = ln[:, None] * (t[None, :] + 1.0) / 2.0
+            X = px[:, None] + np.where(horiz, 1.0, 0.0)[:, None] * s
+            Y = py[:, None] + np.where(horiz, 0.0, 1.0)[:, None] * s
+            g = np.asarray(spec.dirichlet(X, Y), float).reshape(X.shape)
+            rhs1 = (g * ref.quad.weights[None, :]) @ ref.interp_1d
+            proj = np.linalg.solve(ref.mass1, rhs1.T).T                    # local.py:72-78
+            for k in range(n1):
+                lam_bc[bnd_e, bnd_s * n1 + k] = proj[:, k]
+            Tcls = self.classes.T[self.elem_class[np.unique(bnd_e)]]
+            ub = np.unique(bnd_e)
+            load[ub] -= np.einsum("eij,ej->ei", Tcls, lam_bc[ub])
+        if self.classes.n == 1:
+            cl = load @ self.classes.Z[0].T
+        else:
+            cl = np.einsum("eij,ej->ei", self.classes.Z[self.elem_class], load)
+        return self.layout.sum_owners(cl)
+
+    # -- reference attributes -----------------------------------------------------------------
+    @property
+    def interior(self):
+        return self.layout.interior
+
+    @property
+    def block_of(self):
+        return self.layout.block_of
+
+    @property
+    def schur(self):
+        return self.operator.schur()
+
+    # -- matrix-free application --------------------------------------------------------------
+    def matvec_free(self, x):
+        """y = A x on the GPU (trace.py:87-94).  numpy in -> numpy out; CUDA tensor -> tensor."""
+        if self.ndof == 0:
+            return np.zeros(0) if not hasattr(x, "is_cuda") else x.new_zeros(0)
+        return self.operator.apply(x)
+
+    def gather_element(self, x, e):
+        """trace.py:81-85 (host view)."""
+        if self.ndof == 0:
+            return np.zeros(4 * self.ops.n1)
+        return self.layout.gather(np.asarray(x, float))[e]
+
+    def assemble_csr(self):
+        """trace.py:98-128 (host CSR; used as a checker and for the coarse inverse)."""
+        return self.operator.tocsr()
+
+    def matvec_csr(self, x):
+        return self.assemble_csr() @ x
+
+    # -- solvers ------------------------------------------------------------------------------
+    def solve_cg(self, tol=1e-12, maxiter=5000, matvec=None, precond=None, x0=None, b=None):
+        """trace.py:142-163 on the device: vectors stay in HBM, the three scalars per
+        iteration the reference computes (r.z, d.Ad, ||r||) cross to the host.
+        `b` extends the reference signature (which always solves with self.rhs)."""
+        bd, was_np = dev.to_device(self.rhs if b is None else b)
+        n = bd.numel()
+        s = dev.stream()
+        mv = matvec or self.operator.apply
+        x = dev.zeros(n) if x0 is None else dev.to_device(x0)[0].clone()
+        r = bd - mv(x) if x0 is not None else bd.clone()
+        z = precond(r) if precond else r
+        d = z.clone()
+        scratch = dev.empty(1)
+
+        def dot(a, c):
+            check(lib.hdg_dot(dev.ptr(a), dev.ptr(c), n, dev.ptr(scratch), s))
+            return float(scratch.item())
+
+        rz = dot(r, z)
+        bnorm = dot(bd, bd) ** 0.5 or 1.0
+        for it in range(maxiter):
+            if dot(r, r) ** 0.5 <= tol * bnorm:
+                return dev.back(x, was_np), it
+            ad = mv(d)
+            alpha = rz / dot(d, ad)
+            check(lib.hdg_cg_update(dev.ptr(x), dev.ptr(r), dev.ptr(d), dev.ptr(ad), alpha, n, s))
+            z = precond(r) if precond else r
+            rz_new = dot(r, z)
+            check(lib.hdg_xpby(dev.ptr(z), rz_new / rz, dev.ptr(d), n, s))
+            rz = rz_new
+        return dev.back(x, was_np), maxiter
+
+
+def flop_memop_count(system, mode):
+    """trace.py:201-233 (analytic counters, reference byte model)."""
+    n1 = system.ops.n1
+    rows = system.ndof
+    if mode == "csr":
+        nnz = system.assemble_csr().nnz
+        flops = 2 * nnz - rows
+        bytes_ = 8 * nnz + 4 * (nnz + rows + 1) + 8 * (2 * rows)
+    elif mode == "free":
+        rowlen = 4 * n1
+        flops = system.n_blocks * (2 * 2 * n1 * rowlen - n1)
+        bytes_ = 8 * system.mesh.n_x * system.mesh.n_y * rowlen * rowlen + 8 * (2 * rows)
+        bytes_ += 4 * system.n_blocks * (1 + 2 + 2 * rowlen)
+    elif mode == "dense":
+        flops = 2 * rows * rows - rows
+        bytes_ = 8 * (rows * rows + 2 * rows)
+    else:
+        raise ValueError(f"unknown matvec mode {mode!r}")
+    return {"flops": int(flops), "bytes": int(bytes_), "ai": flops / bytes_ if bytes_ else 0.0}

@@ -1,0 +1,243 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle and the
+reference golden vectors.  Criterion: max|y_gpu - y_ref| <= 1e-12 ||y_ref||_inf
+(stricter than the reference's own max(1, ||ref||) floor, test_trace.py:48, also checked)."""
+
+import numpy as np
+import pytest
+
+import specs
+from oracle import hdg_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_1705_09907_b200.multigrid as mg
+    import paper_1705_09907_b200.problem as pb
+    import paper_1705_09907_b200.trace as tr
+    from paper_1705_09907_b200.mesh import build_cartesian
+
+    class NS:
+        pass
+    ns = NS()
+    ns.mg, ns.pb, ns.tr, ns.mesh = mg, pb, tr, build_cartesian
+    return ns
+
+
+# ------------------------------------------------------------------------------ matvec
+
+
+@pytest.mark.parametrize("n,p", [(2, 1), (4, 2), (4, 3), (8, 1), (8, 2), (8, 5), (3, 2)])
+def test_matvec_manufactured_golden(P, golden, n, p):
+    """Stored-block path (tanh K varies per element) against reference outputs."""
+    g = golden("small_systems.npz")
+    s = P.tr.TraceSystem(P.mesh(n, n), p, specs.manufactured(P.pb.ProblemSpec))
+    assert not s.operator.shared
+    key = f"n{n}p{p}"
+    y = s.matvec_free(g[key + "_x"])
+    ref = g[key + "_y"]
+    assert rel(y, ref) < TOL
+    assert np.abs(y - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())   # test_trace.py:48
+
+
+@pytest.mark.parametrize("p", list(range(1, 13)))
+@pytest.mark.parametrize("shape", [(37, 21), (64, 64)])
+def test_matvec_shared_all_orders(P, p, shape):
+    """Shared-block path (K = I), every order the kernels are built for, ragged tiles."""
+    nx, ny = shape
+    s = P.tr.TraceSystem(P.mesh(nx, ny), p, specs.constant(P.pb.ProblemSpec))
+    assert s.operator.shared
+    S = s.operator.S_cls[0]
+    o = O.OracleTrace(O.Grid(nx, ny), p, None, _blocks=np.broadcast_to(S, (nx * ny,) + S.shape).copy())
+    o.schur *= o.gmask[:, None, :]
+    x = np.random.default_rng(1000 * p + nx).uniform(-1, 1, s.ndof)
+    assert rel(s.matvec_free(x), o.matvec(x)) < TOL
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8, 12])
+def test_matvec_stored_equals_shared(P, p):
+    """Same operator held both ways (stored stream vs constant bank)."""
+    m = P.mesh(40, 33)
+    s = P.tr.TraceSystem(m, p, specs.constant(P.pb.ProblemSpec))
+    E = 40 * 33
+    st = P.tr.TraceSystem.from_blocks(m, p, np.repeat(s.operator.S_cls, E, axis=0), np.arange(E))
+    assert not st.operator.shared
+    x = np.random.default_rng(p).standard_normal(s.ndof)
+    assert rel(st.matvec_free(x), s.matvec_free(x)) < TOL
+
+
+@pytest.mark.parametrize("n,p", [(16, 2), (24, 4), (16, 8)])
+def test_matvec_heterogeneous_vs_oracle(P, n, p):
+    Kg = specs.hetero_K(n, seed=n + p)
+    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+    s = P.tr.TraceSystem(P.mesh(n, n), p, spec)
+    o = O.OracleTrace(O.Grid(n, n), p, O.Spec(O.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0))
+    x = np.random.default_rng(7).uniform(-1, 1, s.ndof)
+    assert rel(s.matvec_free(x), o.matvec(x)) < TOL
+
+
+def test_matvec_edge_cases(P):
+    s11 = P.tr.TraceSystem(P.mesh(1, 1), 2, specs.constant(P.pb.ProblemSpec))
+    assert s11.ndof == 0 and s11.matvec_free(np.zeros(0)).size == 0      # trace.py:90-91
+    s = P.tr.TraceSystem(P.mesh(4, 4), 2, specs.manufactured(P.pb.ProblemSpec))
+    np.testing.assert_array_equal(s.matvec_free(np.zeros(s.ndof)), 0.0)   # test_trace.py:33-35
+    with pytest.raises(ValueError):
+        s.matvec_free(np.zeros(s.ndof + 1))
+    x = np.random.default_rng(0).standard_normal(s.ndof)
+    np.testing.assert_array_equal(s.matvec_free(x), s.matvec_free(x))     # determinism (:51-56)
+
+
+def test_matvec_torch_zero_copy(P):
+    import torch
+    s = P.tr.TraceSystem(P.mesh(32, 32), 3, specs.constant(P.pb.ProblemSpec))
+    x = torch.rand(s.ndof, dtype=torch.float64, device="cuda")
+    y = s.matvec_free(x)
+    assert isinstance(y, torch.Tensor) and y.is_cuda
+    assert rel(y.cpu().numpy(), s.matvec_free(x.cpu().numpy())) == 0.0
+
+
+def test_config2_properties_full_size(P):
+    """BASELINE configs[1] size (1024^2, p=4, K=I): symmetry, linearity, determinism and a
+    sampled-row check against the oracle block."""
+    import torch
+    n, p = 1024, 4
+    s = P.tr.TraceSystem(P.mesh(n, n), p, specs.constant(P.pb.ProblemSpec))
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.rand(s.ndof, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    yv = torch.rand(s.ndof, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    Ax, Ay = s.matvec_free(x), s.matvec_free(yv)
+    lhs, rhs_ = float(Ax @ yv), float(x @ Ay)
+    assert abs(lhs - rhs_) <= 1e-11 * max(1.0, abs(lhs))                 # test_trace.py:59-66
+    A2 = s.matvec_free(2.0 * x + yv)
+    assert float((A2 - (2.0 * Ax + Ay)).abs().max()) <= 1e-12 * float(A2.abs().max())
+    assert torch.equal(Ax, s.matvec_free(x))
+    # sampled facets against the oracle restatement on the gathered element traces
+    S = s.operator.S_cls[0]
+    xs = x.cpu().numpy()
+    lay = s.layout
+    xe_all = lay.gather(xs)
+    cm = np.repeat(lay.side_mask(), p + 1, axis=1)
+    ye = np.einsum("ij,ej->ei", S, xe_all * cm)
+    ref = lay.sum_owners(ye)
+    assert rel(Ax.cpu().numpy(), ref) < TOL
+
+
+# ------------------------------------------------------------------------------ transfers
+
+
+@pytest.mark.parametrize("tag,n,p", [("m8p3", 8, 3), ("m4p2", 4, 2)])
+def test_transfers_match_golden(P, golden, tag, n, p):
+    g = golden("hierarchies.npz")
+    levels = P.mg.build_hierarchy(P.mesh(n, n), p, specs.manufactured(P.pb.ProblemSpec), smoother=None)
+    for k, lev in enumerate(levels):
+        assert rel(lev.matvec(g[f"{tag}_L{k}_v"]), g[f"{tag}_L{k}_Av"]) < TOL
+        if lev.prolong is not None:
+            assert rel(lev.prolong @ g[f"{tag}_L{k}_Pv_in"], g[f"{tag}_L{k}_Pv"]) < TOL
+            assert rel(lev.prolong.T @ g[f"{tag}_L{k}_v"], g[f"{tag}_L{k}_PTv"]) < TOL
+
+
+def test_h_transfer_heterogeneous_vs_oracle(P):
+    n = 16
+    Kg = specs.hetero_K(n, seed=5)
+    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+    levels = P.mg.build_hierarchy(P.mesh(n, n), 2, spec, smoother=None)
+    lo = O.build_levels(O.Grid(n, n), 2, O.Spec(O.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0))
+    rng = np.random.default_rng(3)
+    for lev, ol in zip(levels, lo):
+        v = rng.standard_normal(lev.ndof)
+        assert rel(lev.matvec(v), ol.operator @ v) < TOL
+        if lev.prolong is not None:
+            vc = rng.standard_normal(lev.prolong.shape[1])
+            assert rel(lev.prolong @ vc, ol.prolong @ vc) < TOL
+            assert rel(lev.prolong.T @ v, ol.prolong.T @ v) < TOL
+
+
+# ------------------------------------------------------------------------------- cycles
+
+
+def history_close(got, ref):
+    got, ref = np.asarray(got), np.asarray(ref)
+    assert got.shape == ref.shape, (got.shape, ref.shape)       # identical iteration counts
+    np.testing.assert_allclose(got, ref, rtol=1e-5, atol=1e-10 * ref[0])
+
+
+@pytest.mark.parametrize("tag,n,p", [("m8p3", 8, 3), ("m4p2", 4, 2)])
+def test_vcycle_and_solve_match_golden(P, golden, tag, n, p):
+    g = golden("hierarchies.npz")
+    levels = P.mg.build_hierarchy(P.mesh(n, n), p, specs.manufactured(P.pb.ProblemSpec),
+                                  smoother="blockjacobi", omega=0.8)
+    b = levels[0].rhs
+    assert rel(P.mg.v_cycle(levels, b), g[f"{tag}_bj_x1"]) < TOL
+    _, mon = P.mg.solve_mg(levels, b=b, tol=1e-10, max_cycles=400)
+    history_close(mon.residuals, g[f"{tag}_bj_res"])
+    _, monw = P.mg.solve_mg(levels, b=b, cycle="w", tol=1e-10, max_cycles=400)
+    history_close(monw.residuals, g[f"{tag}_bjw_res"])
+
+
+def test_kI_vcycle_matches_golden(P, golden):
+    g = golden("hierarchies.npz")
+    levels = P.mg.build_hierarchy(P.mesh(16, 16), 4, specs.constant(P.pb.ProblemSpec), smoother="blockjacobi")
+    b = g["kI16p4_b"]
+    assert rel(P.mg.v_cycle(levels, b), g["kI16p4_bj_x1"]) < TOL
+    _, mon = P.mg.solve_mg(levels, b=b, tol=1e-10, max_cycles=400)
+    history_close(mon.residuals, g["kI16p4_bj_res"])
+
+
+def test_heterogeneous_vcycle_and_pcg_match_golden(P, golden):
+    g = golden("hierarchies.npz")
+    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(g["het8p2_K"]), specs.zero, specs.zero, 1.0)
+    levels = P.mg.build_hierarchy(P.mesh(8, 8), 2, spec, smoother="blockjacobi")
+    b = g["het8p2_b"]
+    assert rel(levels[0].system.matvec_free(b), g["het8p2_y"]) < TOL
+    assert rel(P.mg.v_cycle(levels, b), g["het8p2_bj_x1"]) < TOL
+    _, mon = P.mg.solve_mg(levels, b=b, tol=1e-10, max_cycles=2000)
+    history_close(mon.residuals, g["het8p2_bj_res"])
+    x, it = levels[0].system.solve_cg(tol=1e-10, precond=P.mg.mg_preconditioner(levels), b=b)
+    assert it == int(g["het8p2_pcg_iters"][0])
+    assert rel(x, g["het8p2_pcg_x"]) < 1e-9
+
+
+def test_config1_golden(P, golden):
+    """BASELINE configs[0] end to end: rhs, one matvec, one V(2,2) BJ(0.8) cycle on
+    levels[:6] (down to 4x4): rel. residual 0.267064; full solve 92 cycles, rho 0.80898."""
+    g = golden("config1.npz")
+    levels = P.mg.build_hierarchy(P.mesh(64, 64), 2, P.pb.config1_problem(), smoother=None)[:6]
+    P.mg.attach_smoothers(levels, "blockjacobi", 0.8)
+    fine = levels[0]
+    b = fine.rhs
+    assert rel(b, g["b"]) < TOL
+    assert rel(fine.matvec(b), g["Ab"]) < TOL
+    x1 = P.mg.v_cycle(levels, b)
+    assert rel(x1, g["x1"]) < TOL
+    r1 = np.linalg.norm(b - fine.matvec(x1)) / np.linalg.norm(b)
+    assert abs(r1 - 0.267064) < 5e-7
+    x, mon = P.mg.solve_mg(levels, b=b, tol=1e-10, max_cycles=400)
+    history_close(mon.residuals, g["res"])
+    assert len(mon.residuals) - 1 == 92
+    assert abs(mon.asymptotic_rate() - 0.80898) < 1e-5
+    assert rel(x, g["x"]) < 1e-10
+
+
+def test_vcycle_graph_replay_and_zero_input(P):
+    levels = P.mg.build_hierarchy(P.mesh(32, 32), 3, specs.constant(P.pb.ProblemSpec), smoother="blockjacobi")
+    b = np.random.default_rng(4).uniform(-1, 1, levels[0].ndof)
+    x1 = P.mg.v_cycle(levels, b)
+    x2 = P.mg.v_cycle(levels, b)
+    np.testing.assert_array_equal(x1, x2)
+    np.testing.assert_array_equal(P.mg.v_cycle(levels, np.zeros_like(b)), 0.0)   # test_multigrid.py:206-209
+    lo = O.build_levels(O.Grid(32, 32), 3, specs.constant(O.Spec), smoother="blockjacobi")
+    assert rel(x1, O.v_cycle(lo, b)) < TOL
+    x0 = np.random.default_rng(5).standard_normal(levels[0].ndof)
+    x0c = x0.copy()
+    assert rel(P.mg.v_cycle(levels, b, x0), O.v_cycle(lo, b, x0)) < TOL
+    np.testing.assert_array_equal(x0, x0c)                                       # x0 not mutated

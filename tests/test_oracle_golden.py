@@ -6,6 +6,8 @@ import pytest
 
 from oracle import hdg_oracle as O
 
+import specs
+
 
 def history_close(got, ref):
     """Residual histories: identical lengths (iteration counts); each entry within
@@ -21,27 +23,7 @@ def rel(a, b):
 
 
 def bump_spec():
-    # problem.py:31-89 manufactured problem, restated for the oracle inputs
-    def parts(x, y):
-        return x * (x - 1.0), y * (y - 1.0), np.exp(-x * x - y * y)
-
-    def u(x, y):
-        P, Q, E = parts(x, y)
-        return P * Q * E
-
-    def K(x, y):
-        return np.tanh(x + y) + 1.0
-
-    def f(x, y):
-        P, Q, E = parts(x, y)
-        Px = (2.0 * x - 1.0) - 2.0 * x * P
-        Qy = (2.0 * y - 1.0) - 2.0 * y * Q
-        Pxx = (2.0 + 4.0 * x - 6.0 * x * x) - 2.0 * x * Px
-        Qyy = (2.0 + 4.0 * y - 6.0 * y * y) - 2.0 * y * Qy
-        t = np.tanh(x + y)
-        return -((1.0 - t * t) * (Px * Q * E + P * Qy * E) + (t + 1.0) * (Pxx * Q * E + Qyy * P * E))
-
-    return O.Spec(K, f, u, 1.0)
+    return specs.manufactured(O.Spec)
 
 
 @pytest.mark.parametrize("n,p", [(2, 1), (4, 2), (4, 3), (8, 1), (8, 2), (8, 5), (3, 2)])

@@ -1,0 +1,91 @@
+"""Host-side setup of the product (batched condensation, Galerkin element blocks) against
+the CPU oracle and the reference golden vectors.  No GPU needed: device handles are lazy."""
+
+import numpy as np
+import pytest
+
+import specs
+from oracle import hdg_oracle as O
+from paper_1705_09907_b200.mesh import build_cartesian
+from paper_1705_09907_b200.multigrid import build_hierarchy
+from paper_1705_09907_b200.problem import ProblemSpec, config1_problem, piecewise_coefficient
+from paper_1705_09907_b200.trace import TraceSystem
+
+
+def rel(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300)
+
+
+@pytest.mark.parametrize("n,p", [(2, 1), (4, 2), (4, 3), (3, 2)])
+def test_blocks_and_rhs_match_golden(golden, n, p):
+    g = golden("small_systems.npz")
+    s = TraceSystem(build_cartesian(n, n), p, specs.manufactured(ProblemSpec))
+    key = f"n{n}p{p}"
+    assert rel(s.schur, g[key + "_schur"]) < 1e-12
+    assert rel(s.rhs, g[key + "_rhs"]) < 1e-12
+    x = g[key + "_x"]
+    assert rel(s.assemble_csr() @ x, g[key + "_y"]) < 1e-12
+
+
+@pytest.mark.parametrize("n,p", [(8, 1), (8, 2), (8, 5)])
+def test_csr_matches_golden_matvec(golden, n, p):
+    g = golden("small_systems.npz")
+    s = TraceSystem(build_cartesian(n, n), p, specs.manufactured(ProblemSpec))
+    key = f"n{n}p{p}"
+    assert rel(s.assemble_csr() @ g[key + "_x"], g[key + "_y"]) < 1e-12
+    assert rel(s.rhs, g[key + "_rhs"]) < 1e-12
+
+
+@pytest.mark.parametrize("p", range(1, 9))
+def test_constant_K_is_one_class(golden, p):
+    g = golden("small_systems.npz")
+    s = TraceSystem(build_cartesian(4, 4), p, specs.constant(ProblemSpec))
+    assert s.operator.S_cls.shape[0] == 1
+    assert rel(s.schur[5], g[f"kI_n4p{p}_schur5"]) < 1e-12
+    assert rel(s.schur[0], g[f"kI_n4p{p}_schur0"]) < 1e-12
+
+
+def test_rectangular_mesh_layout():
+    m = build_cartesian(5, 3)
+    s = TraceSystem(m, 2, specs.manufactured(ProblemSpec))
+    o = O.OracleTrace(O.Grid(5, 3), 2, specs.manufactured(O.Spec))
+    assert s.ndof == o.ndof
+    np.testing.assert_array_equal(s.block_of, o.block_of)
+    x = np.random.default_rng(0).standard_normal(s.ndof)
+    assert rel(s.assemble_csr() @ x, o.matvec(x)) < 1e-12
+    assert rel(s.layout.gather(x), np.where(o.gmask, x[o.gidx], 0.0)) == 0.0
+
+
+@pytest.mark.parametrize("tag,n,p", [("m8p3", 8, 3), ("m4p2", 4, 2)])
+def test_galerkin_levels_match_golden(golden, tag, n, p):
+    g = golden("hierarchies.npz")
+    levels = build_hierarchy(build_cartesian(n, n), p, specs.manufactured(ProblemSpec), smoother=None)
+    for k, lev in enumerate(levels):
+        assert tuple(g[f"{tag}_L{k}_shape"]) == (lev.mesh.n_x, lev.p, lev.ndof)
+        A = lev.operator.tocsr()
+        assert rel(A @ g[f"{tag}_L{k}_v"], g[f"{tag}_L{k}_Av"]) < 1e-12
+
+
+def test_galerkin_heterogeneous_match_golden(golden):
+    g = golden("hierarchies.npz")
+    spec = ProblemSpec(piecewise_coefficient(g["het8p2_K"]), specs.zero, specs.zero, 1.0)
+    levels = build_hierarchy(build_cartesian(8, 8), 2, spec, smoother=None)
+    for k, lev in enumerate(levels):
+        v = np.random.default_rng(100 + k).standard_normal(lev.ndof)
+        assert rel(lev.operator.tocsr() @ v, g[f"het8p2_L{k}_Av"]) < 1e-12
+
+
+def test_kI_hierarchy_one_block_per_level():
+    levels = build_hierarchy(build_cartesian(16, 16), 4, specs.constant(ProblemSpec), smoother=None)
+    assert all(lev.block_op.S_cls.shape[0] == 1 for lev in levels)
+    o = O.build_levels(O.Grid(16, 16), 4, specs.constant(O.Spec))
+    for lev, lo in zip(levels, o):
+        v = np.random.default_rng(lev.ndof).standard_normal(lev.ndof)
+        assert rel(lev.operator.tocsr() @ v, lo.operator @ v) < 1e-12
+
+
+def test_config1_rhs_matches_golden(golden):
+    g = golden("config1.npz")
+    s = TraceSystem(build_cartesian(64, 64), 2, config1_problem())
+    assert rel(s.rhs, g["b"]) < 1e-12
+    assert rel(s.assemble_csr() @ g["b"], g["Ab"]) < 1e-12
