@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhdgb200.so")
+LIB_PATH = os.environ.get("HDGB200_LIB") or os.path.join(_HERE, "libhdgb200.so")
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 c_void_p = ctypes.c_void_p

@@ -111,11 +111,38 @@ static int prepare_t() {
   return 0;
 }
 
+static int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+// persistent grid: every SM gets as many CTAs as fit (<= MAX_CTAS_PER_SM), never more than tiles
+template <int N1, bool STORED, int EPI>
+static int grid_for(const hdg_level* L) {
+  using C = Cfg<N1>;
+  static int occ = -1;
+  if (occ < 0) {
+    const size_t smem = C::SMEM_DOUBLES * sizeof(double);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trace_apply_kernel<N1, STORED, EPI>, NT, smem) !=
+            cudaSuccess || occ < 1)
+      occ = 1;
+    if (occ > MAX_CTAS_PER_SM) occ = MAX_CTAS_PER_SM;
+  }
+  const long long tiles = (long long)((L->nx + TX - 1) / TX) * ((L->ny + C::TY - 1) / C::TY);
+  const long long g = (long long)sm_count() * occ;
+  return (int)(tiles < g ? tiles : g);
+}
+
 template <int N1, bool STORED, int EPI>
 static int apply_t(const hdg_level* L, MvArgs& a, cudaStream_t s) {
   using C = Cfg<N1>;
   const size_t smem = C::SMEM_DOUBLES * sizeof(double);
-  dim3 grid((L->nx + TX - 1) / TX, (L->ny + TY - 1) / TY);
+  const int grid = grid_for<N1, STORED, EPI>(L);
   SharedOp<(STORED ? 1 : N1)> op;
   if constexpr (!STORED) {
     std::memcpy(op.Wh, L->Wh.data(), sizeof(op.Wh));
@@ -144,7 +171,7 @@ static int apply_t(const hdg_level* L, MvArgs& a, cudaStream_t s) {
   }
 
 static int apply(const hdg_level* L, int epi, MvArgs& a, cudaStream_t s) {
-  a.nx = L->nx; a.ny = L->ny; a.nxp = L->nxp; a.nh = L->nh;
+  a.nx = L->nx; a.ny = L->ny; a.nxp = L->nxp; a.nh = (int)L->nh;
   a.Wh = L->dWh; a.Wv = L->dWv; a.Dh = L->dDh; a.Dv = L->dDv;
   a.omega = L->omega;
   if (L->ndof == 0) return 0;
@@ -179,8 +206,8 @@ static int init_level(hdg_level* L, int nx, int ny, int p) {
   L->nh = (long long)nx * (ny - 1);
   L->n_blocks = L->nh + (long long)(nx - 1) * ny;
   L->ndof = L->n_blocks * L->n1;
-  const int gx = (nx + TX - 1) / TX, gy = (ny + TY - 1) / TY;
-  L->npart = gx * gy;
+  if (L->ndof >= (1LL << 31) - 64) return fail(HDG_EINVAL, "one level must hold < 2^31 trace dofs per GPU");
+  L->npart = sm_count() * MAX_CTAS_PER_SM;
   CK(cudaMalloc(&L->partials, sizeof(double) * (L->npart + 1)));
   return 0;
 }
@@ -311,8 +338,16 @@ int hdg_matvec(const hdg_level* L, const double* x, double* y, void* stream) {
   return apply(L, EPI_Y, a, S(stream));
 }
 
+static int res_grid(const hdg_level* L) {
+#define RESG_CASE(N) return L->stored ? grid_for<N, true, EPI_RES>(L) : grid_for<N, false, EPI_RES>(L);
+  HDG_N1_SWITCH(L->n1, RESG_CASE)
+#undef RESG_CASE
+}
+
 static int finish_norm(const hdg_level* L, double* norm2_out, cudaStream_t s) {
-  sum_partials_kernel<<<1, 32, 0, s>>>(L->partials, L->npart, norm2_out);
+  const int g = res_grid(L);
+  if (g < 0 || g > L->npart) return fail(HDG_ESTATE, "norm partial buffer too small");
+  sum_partials_kernel<<<1, 32, 0, s>>>(L->partials, g, norm2_out);
   CKL();
   return 0;
 }

@@ -32,25 +32,56 @@
 
 namespace hdg {
 
-constexpr int TX = 32;   // tile width in elements (= warp width: lanes walk i)
-constexpr int TY = 8;    // tile height in elements (= warps per CTA)
-constexpr int NT = TX * TY;
+#ifndef HDG_NBUF
+#define HDG_NBUF 2         // stage buffers per CTA (2 = prefetch next tile while computing)
+#endif
+#ifndef HDG_F_MAXN1
+#define HDG_F_MAXN1 5      // two facets per thread per orientation up to this n1
+#endif
+#ifndef HDG_MINB
+#define HDG_MINB 2         // __launch_bounds__ min blocks per SM for the trace kernel
+#endif
+#ifndef HDG_NWARP
+#define HDG_NWARP 8
+#endif
+
+constexpr int TX = 32;     // tile width in elements (= warp width: lanes walk i)
+constexpr int NWARP = HDG_NWARP;   // warps per CTA
+constexpr int NT = TX * NWARP;
 constexpr int MAXN1 = 13;  // p <= 12
+constexpr int MAX_CTAS_PER_SM = 8;
 
 enum Epi { EPI_Y = 0, EPI_RES = 1, EPI_BJ = 2, EPI_RESPR = 3 };
 
 template <int N1> struct Cfg {
-  static constexpr int S = (N1 & 1) ? N1 : N1 + 1;  // odd smem stride per facet block
+  static constexpr int S = N1;                      // facet blocks contiguous in a staged run
+  static constexpr int F = (N1 <= HDG_F_MAXN1) ? 2 : 1;  // facets per thread per orientation
+  static constexpr int TY = NWARP * F;              // tile height in elements
   static constexpr int WSZ = 7 * N1 * N1;           // merged facet operator entries
   static constexpr int DSZ = N1 * N1;               // block-Jacobi inverse entries
   static constexpr int QUNROLL = (N1 <= 8) ? 7 : 1; // keep registers bounded at high order
   static constexpr int HROWS = TY + 2, HCOLS = TX + 1;
   static constexpr int VCOLS = TX + 2, VROWS = TY + 1;
-  static constexpr int SMEM_DOUBLES = (HROWS * HCOLS + VCOLS * VROWS) * S;
+  // H rows are exact copies of contiguous global runs (TMA bulk copies); each run has one
+  // slack double so its start can be shifted to the global 16-byte parity.  V columns are
+  // contiguous along j in HBM but lanes walk i, so they are TRANSPOSED while staging (8-byte
+  // LDGSTS scatter) into [row][column] with an odd block stride: conflict-free 64-bit LDS.
+  static constexpr bool CONTIG = true;
+  static constexpr int RS = (HCOLS * S + 2) & ~1;                         // H row stride (even)
+  static constexpr int HSZ = HROWS * RS;                                  // even
+  static constexpr int SV = (N1 & 1) ? N1 : N1 + 1;                       // V block stride (odd)
+  static constexpr int BUF_X = HSZ + VROWS * VCOLS * SV;
+  // output staging (reuses the consumed x buffer): h rows of TX facets, v columns of TY facets
+  static constexpr int NOUT = N1;                                         // max outputs per facet
+  static constexpr int YCS = (TY * NOUT) | 1;                             // odd column stride
+  static constexpr int BUF_Y = TY * TX * NOUT + TX * YCS;
+  static constexpr int BUF = ((BUF_X > BUF_Y ? BUF_X : BUF_Y) + 1) & ~1;  // doubles per stage buffer
+  static constexpr int NBUF = HDG_NBUF;
+  static constexpr int SMEM_DOUBLES = NBUF * BUF;
 };
 
-// Shared-mode operator: both merged facet matrices + block-Jacobi inverses.
-// Passed by value => constant bank; fully unrolled indices become c[0x0][imm] operands.
+// Shared-mode operator: both merged facet matrices + block-Jacobi inverses, passed by value
+// (kernel-parameter constant bank -> LDCU.128 into uniform registers, shared by all lanes).
 template <int N1> struct SharedOp {
   double Wh[7 * N1 * N1];
   double Wv[7 * N1 * N1];
@@ -60,7 +91,7 @@ template <int N1> struct SharedOp {
 
 struct MvArgs {
   int nx, ny, nxp;          // mesh and padded interleave row length (multiple of 32)
-  long long nh;             // interior horizontal facet blocks = nx * (ny - 1)
+  int nh;                   // interior horizontal facet blocks = nx * (ny - 1)
   const double* x;          // input trace vector
   const double* b;          // right-hand side (RES / BJ / RESPR)
   double* out;              // y | r | x_out | r_coarse
@@ -73,10 +104,9 @@ struct MvArgs {
   double V[MAXN1 * (MAXN1 - 1)];  // RESPR: fine x coarse p-transfer matrix, row-major
 };
 
-__device__ __forceinline__ long long hblk(int nx, int i, int j) { return (long long)(j - 1) * nx + i; }
-__device__ __forceinline__ long long vblk(long long nh, int ny, int i, int j) {
-  return nh + (long long)(i - 1) * ny + j;
-}
+// reference block numbering (trace.py:39-41, mesh.py:112-117); ndof < 2^31 per level
+__device__ __forceinline__ int hblk(int nx, int i, int j) { return (j - 1) * nx + i; }
+__device__ __forceinline__ int vblk(int nh, int ny, int i, int j) { return nh + (i - 1) * ny + j; }
 
 // streaming load of operator data: read once per apply, so keep it out of L1 and mark it
 // evict-first in L2 (x, which IS re-read by neighbouring tiles, keeps the L2)
@@ -91,80 +121,231 @@ __device__ __forceinline__ double ld_stream(const double* p, uint64_t pol) {
   return v;
 }
 
-template <int N1>
-__device__ __forceinline__ void stage_tile(const MvArgs& a, double* Hs, double* Vs, int i0, int j0) {
-  using C = Cfg<N1>;
-  constexpr int HROW = C::HCOLS * N1;
-  for (int t = threadIdx.x; t < C::HROWS * HROW; t += NT) {
-    const int jj = t / HROW, r = t - jj * HROW;
-    const int ii = r / N1, m = r - ii * N1;
-    const int i = i0 - 1 + ii, j = j0 - 1 + jj;
-    double v = 0.0;
-    if (j >= 1 && j <= a.ny - 1 && i >= 0 && i < a.nx) v = __ldg(a.x + hblk(a.nx, i, j) * N1 + m);
-    Hs[(jj * C::HCOLS + ii) * C::S + m] = v;
+// async global->shared copy of one double; src_size 0 zero-fills (boundary / outside the mesh)
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NPEND> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND));
+}
+
+// global start (element index) of H row r / V column c of the tile staged at (i0, j0)
+template <int N1> __device__ __forceinline__ int h_run_start(const MvArgs& a, int i0, int j0, int r) {
+  return ((j0 - 2 + r) * a.nx + i0 - 1) * N1;
+}
+template <int N1> __device__ __forceinline__ int v_run_start(const MvArgs& a, int i0, int j0, int c) {
+  return (a.nh + (i0 - 2 + c) * a.ny + j0 - 1) * N1;
+}
+
+// ------------------------------------------------------------------- mbarrier / TMA (bulk)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// arrive on `bar` once this thread's prior cp.async (LDGSTS) complete; counts as one arrival
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// bounded wait: a lost arrival must surface as an error (trap), never as a hung GPU
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  for (int spin = 0; spin < (1 << 20); ++spin) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (done) return;
   }
-  constexpr int VCOL = C::VROWS * N1;
-  for (int t = threadIdx.x; t < C::VCOLS * VCOL; t += NT) {
-    const int ii = t / VCOL, r = t - ii * VCOL;
-    const int jj = r / N1, m = r - jj * N1;
-    const int i = i0 - 1 + ii, j = j0 - 1 + jj;
-    double v = 0.0;
-    if (i >= 1 && i <= a.nx - 1 && j >= 0 && j < a.ny) v = __ldg(a.x + vblk(a.nh, a.ny, i, j) * N1 + m);
-    Vs[(ii * C::VROWS + jj) * C::S + m] = v;
+  __trap();
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// smem index of element e of a staged run = base + o + e, with o = parity shift so that the
+// smem index has the parity of the global index (16-byte alignment of the bulk copy)
+__device__ __forceinline__ int run_shift(int g0, int base) { return (g0 - base) & 1; }
+
+// A run: global elements [g0, g0 + len) of x; elements [elo, ehi) are real facets, the rest
+// (Dirichlet facets / outside the mesh) must read as 0.  Returns the TMA bytes it will load.
+struct Run {
+  int g0, base, elo, ehi, len;
+  bool valid;
+};
+
+__device__ __forceinline__ unsigned run_bytes(const Run& r) {
+  if (!r.valid || r.ehi <= r.elo) return 0u;
+  int gs = r.g0 + r.elo, ge = r.g0 + r.ehi;
+  gs += gs & 1;
+  if (gs < ge) ge -= ge & 1;
+  return ge > gs ? (unsigned)(ge - gs) * 8u : 0u;
+}
+
+// issued by one lane: head/tail doubles by LDGSTS, the aligned body by one bulk copy
+__device__ __forceinline__ void run_issue(const double* __restrict__ x, double* buf, const Run& r, uint64_t* bar) {
+  if (!r.valid || r.ehi <= r.elo) return;
+  double* d = buf + r.base + run_shift(r.g0, r.base) - r.g0;  // d[g] = smem slot of global element g
+  int gs = r.g0 + r.elo, ge = r.g0 + r.ehi;
+  if (gs & 1) { cp_async8(d + gs, x + gs, true); ++gs; }
+  if (gs < ge && (ge & 1)) { cp_async8(d + ge - 1, x + ge - 1, true); --ge; }
+  if (ge > gs) tma_load_1d(d + gs, x + gs, (unsigned)(ge - gs) * 8u, bar);
+}
+
+// zero the non-facet part of a run (all lanes of the owning warp)
+__device__ __forceinline__ void run_zero(double* buf, const Run& r, int lane) {
+  double* d = buf + r.base + run_shift(r.g0, r.base);
+  if (!r.valid || r.ehi <= r.elo) {
+    for (int e = lane; e < r.len; e += 32) d[e] = 0.0;
+    return;
+  }
+  for (int e = lane; e < r.elo; e += 32) d[e] = 0.0;
+  for (int e = r.ehi + lane; e < r.len; e += 32) d[e] = 0.0;
+}
+
+template <int N1> __device__ __forceinline__ Run h_run(const MvArgs& a, int i0, int j0, int r) {
+  using C = Cfg<N1>;
+  const int j = j0 - 1 + r;
+  Run q;
+  q.g0 = h_run_start<N1>(a, i0, j0, r);
+  q.base = r * C::RS;
+  q.len = C::HCOLS * N1;
+  q.elo = (i0 == 0) ? N1 : 0;                        // column i = -1
+  q.ehi = min(C::HCOLS, a.nx - (i0 - 1)) * N1;       // columns i < nx
+  q.valid = (j >= 1 && j <= a.ny - 1);
+  return q;
+}
+// Stage the x blocks of one tile's facet stencils into shared memory.  H rows
+// h(i0-1 .. i0+TX-1, j) and V columns v(i, j0-1 .. j0+TY-1) are contiguous runs of the
+// reference layout, so each is ONE bulk (TMA) copy issued by the owning warp's lane 0, plus at
+// most two 8-byte LDGSTS for a misaligned head/tail.  Completion: `bar` (2 arrivals per warp).
+//   H region: h(i, j), i in [i0-1, i0+TX), j in [j0-1, j0+TY]      ((TY+2) x (TX+1) blocks)
+//   V region: v(i, j), i in [i0-1, i0+TX], j in [j0-1, j0+TY)      ((TX+2) x (TY+1) blocks)
+template <int N1>
+__device__ __forceinline__ void stage_tile(const MvArgs& a, double* buf, int i0, int j0, uint64_t* bar) {
+  using C = Cfg<N1>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool edge = (i0 == 0) || (j0 == 0) || (i0 + TX >= a.nx) || (j0 + C::TY >= a.ny);
+#ifdef HDG_EXP_NOSTAGE
+  if (lane == 0) mbar_arrive_expect_tx(bar, 0);
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)));
+  return;
+#endif
+  if (lane == 0) {
+    unsigned bytes = 0;
+    for (int r = warp; r < C::HROWS; r += NWARP) bytes += run_bytes(h_run<N1>(a, i0, j0, r));
+    fence_proxy_async();               // prior generic reads/writes of this buffer -> async proxy
+    mbar_arrive_expect_tx(bar, bytes);
+    for (int r = warp; r < C::HROWS; r += NWARP) run_issue(a.x, buf, h_run<N1>(a, i0, j0, r), bar);
+  }
+  if (edge) {  // zero Dirichlet / out-of-mesh parts of H rows (interior tiles skip this)
+    for (int r = warp; r < C::HROWS; r += NWARP) run_zero(buf, h_run<N1>(a, i0, j0, r), lane);
+  }
+  // V columns: coalesced 8-byte LDGSTS from the contiguous run, transposed into [row][col];
+  // src-size 0 zero-fills Dirichlet / out-of-mesh blocks
+  {
+    double* Vs = buf + C::HSZ;
+    const int elo = (j0 == 0) ? N1 : 0;                          // row j = -1
+    const int ehi = min(C::VROWS, a.ny - (j0 - 1)) * N1;         // rows j < ny
+    for (int c = warp; c < C::VCOLS; c += NWARP) {
+      const int i = i0 - 1 + c;
+      const bool colok = (i >= 1 && i <= a.nx - 1);
+      const double* src = a.x + (colok ? v_run_start<N1>(a, i0, j0, c) : 0);
+#pragma unroll
+      for (int q = 0; q < (C::VROWS * N1 + 31) / 32; ++q) {
+        const int e = lane + 32 * q;
+        if (e < C::VROWS * N1) {
+          const int r = e / N1, m = e - r * N1;
+          const bool ok = colok && e >= elo && e < ehi;
+          cp_async8(Vs + (r * C::VCOLS + c) * C::SV + m, ok ? src + e : a.x, ok);
+        }
+      }
+    }
+  }
+  cp_async_mbar_arrive(bar);           // every thread: one arrival when its LDGSTS land
+}
+
+// acc_f = W . [x of facet f's 7 stencil blocks] for FF facets of one orientation.
+// Shared mode: W is uniform (constant bank), each W value feeds FF facets.
+template <int N1, int FF>
+__device__ __forceinline__ void apply_shared(const double* const (&nb)[FF][7], const double* W,
+                                             double (&acc)[FF][N1]) {
+#pragma unroll
+  for (int f = 0; f < FF; ++f)
+#pragma unroll
+    for (int k = 0; k < N1; ++k) acc[f][k] = 0.0;
+#ifdef HDG_EXP_NOCOMPUTE
+#pragma unroll
+  for (int f = 0; f < FF; ++f)
+#pragma unroll
+    for (int k = 0; k < N1; ++k) acc[f][k] = nb[f][1][k] + nb[f][4][k];
+  return;
+#endif
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    double xv[FF][N1];
+#pragma unroll
+    for (int f = 0; f < FF; ++f)
+#pragma unroll
+      for (int m = 0; m < N1; ++m) xv[f][m] = nb[f][q][m];
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        const double w = W[(q * N1 + k) * N1 + m];
+#pragma unroll
+        for (int f = 0; f < FF; ++f) acc[f][k] = fma(w, xv[f][m], acc[f][k]);
+      }
   }
 }
 
-// acc = W_f . [x of the 7 stencil blocks];  W from constant bank (shared) or streamed (stored)
-template <int N1, bool STORED>
-__device__ __forceinline__ void facet_apply(const double* const* nb, const double* Wc, const double* Ws,
-                                            double (&acc)[N1]) {
+// Stored mode: this facet's merged matrix streams from HBM (coalesced across the warp).
+template <int N1>
+__device__ __forceinline__ void apply_stored(const double* const (&nb)[7], const double* Ws, double (&acc)[N1]) {
   using C = Cfg<N1>;
+  const uint64_t pol = evict_first_policy();
 #pragma unroll
   for (int k = 0; k < N1; ++k) acc[k] = 0.0;
-  if constexpr (!STORED) {
-#pragma unroll
-    for (int q = 0; q < 7; ++q) {
-      double xv[N1];
-#pragma unroll
-      for (int m = 0; m < N1; ++m) xv[m] = nb[q][m];
-#pragma unroll
-      for (int k = 0; k < N1; ++k)
-#pragma unroll
-        for (int m = 0; m < N1; ++m) acc[k] = fma(Wc[(q * N1 + k) * N1 + m], xv[m], acc[k]);
-    }
-  } else {
-    const uint64_t pol = evict_first_policy();
 #pragma unroll (C::QUNROLL)
-    for (int q = 0; q < 7; ++q) {
-      double xv[N1];
+  for (int q = 0; q < 7; ++q) {
+    double xv[N1];
 #pragma unroll
-      for (int m = 0; m < N1; ++m) xv[m] = nb[q][m];
-      const double* Wq = Ws + (size_t)q * N1 * N1 * 32;
+    for (int m = 0; m < N1; ++m) xv[m] = nb[q][m];
+    const double* Wq = Ws + (size_t)q * N1 * N1 * 32;
 #pragma unroll
-      for (int k = 0; k < N1; ++k)
+    for (int k = 0; k < N1; ++k)
 #pragma unroll
-        for (int m = 0; m < N1; ++m) acc[k] = fma(ld_stream(Wq + (k * N1 + m) * 32, pol), xv[m], acc[k]);
-    }
+      for (int m = 0; m < N1; ++m) acc[k] = fma(ld_stream(Wq + (k * N1 + m) * 32, pol), xv[m], acc[k]);
   }
 }
 
+template <int EPI, int N1> struct NOutOf { static constexpr int v = (EPI == EPI_RESPR) ? N1 - 1 : N1; };
+
+// Per-facet epilogue: the facet's output values (y | r | x_out | r_coarse) into `o`.
 template <int N1, bool STORED, int EPI>
-__device__ __forceinline__ void facet_epilogue(const MvArgs& a, long long blk, const double* xf,
-                                               const double* Dc, const double* Ds, const double (&acc)[N1],
+__device__ __forceinline__ void facet_epilogue(const MvArgs& a, int blk, const double* xf, const double* Dc,
+                                               const double* Ds, const double (&acc)[N1], double (&o)[N1],
                                                double& nrm) {
   if constexpr (EPI == EPI_Y) {
 #pragma unroll
-    for (int k = 0; k < N1; ++k) a.out[blk * N1 + k] = acc[k];
+    for (int k = 0; k < N1; ++k) o[k] = acc[k];
   } else {
     double r[N1];
 #pragma unroll
     for (int k = 0; k < N1; ++k) r[k] = __ldg(a.b + blk * N1 + k) - acc[k];
     if constexpr (EPI == EPI_RES) {
 #pragma unroll
-      for (int k = 0; k < N1; ++k) nrm = fma(r[k], r[k], nrm);
-      if (a.out != nullptr) {
-#pragma unroll
-        for (int k = 0; k < N1; ++k) a.out[blk * N1 + k] = r[k];
+      for (int k = 0; k < N1; ++k) {
+        nrm = fma(r[k], r[k], nrm);
+        o[k] = r[k];
       }
     } else if constexpr (EPI == EPI_BJ) {
       double dinv[N1 * N1];
@@ -172,7 +353,6 @@ __device__ __forceinline__ void facet_epilogue(const MvArgs& a, long long blk, c
 #pragma unroll
         for (int t = 0; t < N1 * N1; ++t) dinv[t] = Dc[t];
       } else {
-#pragma unroll
         const uint64_t pol = evict_first_policy();
 #pragma unroll
         for (int t = 0; t < N1 * N1; ++t) dinv[t] = ld_stream(Ds + (size_t)t * 32, pol);
@@ -182,83 +362,206 @@ __device__ __forceinline__ void facet_epilogue(const MvArgs& a, long long blk, c
         double s = 0.0;
 #pragma unroll
         for (int m = 0; m < N1; ++m) s = fma(dinv[k * N1 + m], r[m], s);
-        a.out[blk * N1 + k] = fma(a.omega, s, xf[k]);
+        o[k] = fma(a.omega, s, xf[k]);
       }
     } else {  // EPI_RESPR: r_coarse = V^T r  (multigrid.py:399, p-level)
       constexpr int NC = N1 - 1;
 #pragma unroll
-      for (int c = 0; c < (NC > 0 ? NC : 1); ++c) {
-        if (c < NC) {
-          double s = 0.0;
+      for (int c = 0; c < NC; ++c) {
+        double s = 0.0;
 #pragma unroll
-          for (int k = 0; k < N1; ++k) s = fma(a.V[k * NC + c], r[k], s);
-          a.out[blk * NC + c] = s;
-        }
+        for (int k = 0; k < N1; ++k) s = fma(a.V[k * NC + c], r[k], s);
+        o[c] = s;
       }
+      o[N1 - 1] = 0.0;
     }
   }
 }
 
+// One tile: thread (tx, w) owns, for f < F, horizontal facet h(i0+tx, j0+F w+f) (bottom of that
+// element) and vertical facet v(i0+tx, j0+F w+f) (its left side); consecutive rows share
+// stencil blocks (the compiler CSEs the repeated shared-memory loads).  Outputs are staged through
+// shared memory (the consumed x buffer) and written back as contiguous runs.
 template <int N1, bool STORED, int EPI>
-__global__ void __launch_bounds__(NT)
+__device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(STORED ? 1 : N1)>& op,
+                                             double* buf, int i0, int j0, double& nrm) {
+  using C = Cfg<N1>;
+  constexpr int F = C::F;
+  constexpr int NO = NOutOf<EPI, N1>::v;
+  const int tx = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = i0 + tx, ii = tx + 1;
+  const double* Hs = buf;
+  const double* Vs = buf + C::HSZ;
+  // run shifts: H row r starts at parity of ((j0-2+r) nx + i0-1) N1, V column c likewise
+  const int hpar0 = h_run_start<N1>(a, i0, j0, 0), hstep = a.nx * N1;
+  auto H = [&](int r, int c) { return Hs + r * C::RS + ((hpar0 + r * hstep) & 1) + c * C::S; };
+  auto V = [&](int c, int r) { return Vs + (r * C::VCOLS + c) * C::SV; };
+  double oh[F][N1], ov[F][N1];
+  // ---- horizontal facets: owners (i, j-1) [TOP rows] and (i, j) [BOTTOM rows]
+  {
+    const double* nb[F][7];
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      const int jj = F * w + f + 1;
+      nb[f][0] = H(jj - 1, ii); nb[f][1] = H(jj, ii); nb[f][2] = H(jj + 1, ii);
+      nb[f][3] = V(ii, jj - 1); nb[f][4] = V(ii + 1, jj - 1); nb[f][5] = V(ii, jj); nb[f][6] = V(ii + 1, jj);
+    }
+    if constexpr (!STORED) {
+      double acc[F][N1];
+      apply_shared<N1, F>(nb, op.Wh, acc);
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const int j = j0 + F * w + f;
+        if (i < a.nx && j >= 1 && j <= a.ny - 1)
+          facet_epilogue<N1, false, EPI>(a, hblk(a.nx, i, j), nb[f][1], op.Dh, nullptr, acc[f], oh[f], nrm);
+      }
+    } else {
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const int j = j0 + F * w + f;
+        if (j >= 1 && j <= a.ny - 1) {  // warp-uniform; lanes i >= nx read zero padding slots
+          const long long grp = ((long long)j * a.nxp + i0) >> 5;
+          double acc[N1];
+          apply_stored<N1>(nb[f], a.Wh + (size_t)grp * C::WSZ * 32 + tx, acc);
+          if (i < a.nx)
+            facet_epilogue<N1, true, EPI>(a, hblk(a.nx, i, j), nb[f][1], nullptr,
+                                          a.Dh + (size_t)grp * C::DSZ * 32 + tx, acc, oh[f], nrm);
+        }
+      }
+    }
+  }
+  // ---- vertical facets: owners (i-1, j) [RIGHT rows] and (i, j) [LEFT rows]
+  {
+    const double* nb[F][7];
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      const int jj = F * w + f + 1;
+      nb[f][0] = V(ii - 1, jj); nb[f][1] = V(ii, jj); nb[f][2] = V(ii + 1, jj);
+      nb[f][3] = H(jj, ii - 1); nb[f][4] = H(jj + 1, ii - 1); nb[f][5] = H(jj, ii); nb[f][6] = H(jj + 1, ii);
+    }
+    if constexpr (!STORED) {
+      double acc[F][N1];
+      apply_shared<N1, F>(nb, op.Wv, acc);
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const int j = j0 + F * w + f;
+        if (i >= 1 && i <= a.nx - 1 && j < a.ny)
+          facet_epilogue<N1, false, EPI>(a, vblk(a.nh, a.ny, i, j), nb[f][1], op.Dv, nullptr, acc[f], ov[f], nrm);
+      }
+    } else {
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const int j = j0 + F * w + f;
+        if (j < a.ny) {
+          const long long grp = ((long long)j * a.nxp + i0) >> 5;
+          double acc[N1];
+          apply_stored<N1>(nb[f], a.Wv + (size_t)grp * C::WSZ * 32 + tx, acc);
+          if (i >= 1 && i <= a.nx - 1)
+            facet_epilogue<N1, true, EPI>(a, vblk(a.nh, a.ny, i, j), nb[f][1], nullptr,
+                                          a.Dv + (size_t)grp * C::DSZ * 32 + tx, acc, ov[f], nrm);
+        }
+      }
+    }
+  }
+  // ---- outputs -> shared (x buffer is consumed) -> contiguous global runs
+  __syncthreads();
+  double* Yh = buf;                       // [row r][tx][NO]
+  double* Yv = buf + C::TY * TX * NO;     // [col tx][row r][NO], column stride YCS (odd)
+#pragma unroll
+  for (int f = 0; f < F; ++f) {
+    const int r = F * w + f;
+#pragma unroll
+    for (int k = 0; k < NO; ++k) {
+      Yh[(r * TX + tx) * NO + k] = oh[f][k];
+      Yv[tx * C::YCS + r * NO + k] = ov[f][k];
+    }
+  }
+  __syncthreads();
+  if (a.out == nullptr) return;  // norm-only residual
+#ifdef HDG_EXP_NOOUT
+  if (a.nx > 0) return;
+#endif
+  const int lane = tx;
+  // h rows: facets h(i0 .. i0+TX-1, j) -> blocks (j-1)*nx + i, contiguous
+  const int hcount = min(TX, a.nx - i0) * NO;
+#pragma unroll
+  for (int rr = 0; rr < C::TY / NWARP; ++rr) {
+    const int r = w + rr * NWARP;
+    const int j = j0 + r;
+    if (j >= 1 && j <= a.ny - 1) {
+      double* dst = a.out + hblk(a.nx, i0, j) * NO + lane;
+      const double* src = Yh + r * TX * NO + lane;
+#pragma unroll
+      for (int q = 0; q < (TX * NO + 31) / 32; ++q)
+        if (lane + 32 * q < hcount) dst[32 * q] = src[32 * q];
+    }
+  }
+  // v columns: facets v(i, j0 .. j0+TY-1) -> blocks nh + (i-1)*ny + j, contiguous
+  const int vcount = min(C::TY, a.ny - j0) * NO;
+#pragma unroll
+  for (int cc = 0; cc < TX / NWARP; ++cc) {
+    const int c = w + cc * NWARP;
+    const int iv = i0 + c;
+    if (iv >= 1 && iv <= a.nx - 1) {
+      double* dst = a.out + vblk(a.nh, a.ny, iv, j0) * NO + lane;
+      const double* src = Yv + c * C::YCS + lane;
+#pragma unroll
+      for (int q = 0; q < (C::TY * NO + 31) / 32; ++q)
+        if (lane + 32 * q < vcount) dst[32 * q] = src[32 * q];
+    }
+  }
+}
+
+// Persistent, double-buffered: CTA c walks tiles c, c + grid, ...; the next tile's stencil
+// values stream into the other shared buffer (cp.async group) while this tile computes.
+template <int N1, bool STORED, int EPI>
+__global__ void __launch_bounds__(NT, STORED ? 2 : HDG_MINB)
 trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 : N1)> op) {
   using C = Cfg<N1>;
-  extern __shared__ double smem[];
-  double* Hs = smem;
-  double* Vs = smem + C::HROWS * C::HCOLS * C::S;
-  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
-  stage_tile<N1>(a, Hs, Vs, i0, j0);
-  __syncthreads();
-
-  const int tx = threadIdx.x & (TX - 1), ty = threadIdx.x / TX;
-  const int i = i0 + tx, j = j0 + ty;
-  const int ii = tx + 1, jj = ty + 1;
-  auto H = [&](int r, int c) { return Hs + (r * C::HCOLS + c) * C::S; };
-  auto V = [&](int c, int r) { return Vs + (c * C::VROWS + r) * C::S; };
+  extern __shared__ __align__(16) double smem[];
+  const int tiles_x = (a.nx + TX - 1) / TX;
+  const int ntiles = tiles_x * ((a.ny + C::TY - 1) / C::TY);
+  __shared__ __align__(8) uint64_t bars[2];
   double nrm = 0.0;
-  const double* Wc_h = nullptr; const double* Wc_v = nullptr;
-  const double* Dc_h = nullptr; const double* Dc_v = nullptr;
-  if constexpr (!STORED) { Wc_h = op.Wh; Wc_v = op.Wv; Dc_h = op.Dh; Dc_v = op.Dv; }
-  const long long grp_off = (((long long)j * a.nxp + i0) >> 5);  // warp group of this row segment
-
-  // horizontal facet h(i, j): owners (i, j-1) [TOP rows] and (i, j) [BOTTOM rows]
-  if (i < a.nx && j >= 1 && j <= a.ny - 1) {
-    const double* nb[7] = {H(jj - 1, ii), H(jj, ii), H(jj + 1, ii),
-                           V(ii, jj - 1), V(ii + 1, jj - 1), V(ii, jj), V(ii + 1, jj)};
-    double acc[N1];
-    const double* Ws = nullptr; const double* Ds = nullptr;
-    if constexpr (STORED) {
-      Ws = a.Wh + (size_t)grp_off * C::WSZ * 32 + tx;
-      if constexpr (EPI == EPI_BJ) Ds = a.Dh + (size_t)grp_off * C::DSZ * 32 + tx;
-    }
-    facet_apply<N1, STORED>(nb, Wc_h, Ws, acc);
-    facet_epilogue<N1, STORED, EPI>(a, hblk(a.nx, i, j), H(jj, ii), Dc_h, Ds, acc, nrm);
+  int tile = blockIdx.x;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], NWARP + NT);   // lane-0 expect_tx arrivals + per-thread LDGSTS arrivals
+    mbar_init(&bars[1], NWARP + NT);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  // vertical facet v(i, j): owners (i-1, j) [RIGHT rows] and (i, j) [LEFT rows]
-  if (i >= 1 && i <= a.nx - 1 && j < a.ny) {
-    const double* nb[7] = {V(ii - 1, jj), V(ii, jj), V(ii + 1, jj),
-                           H(jj, ii - 1), H(jj + 1, ii - 1), H(jj, ii), H(jj + 1, ii)};
-    double acc[N1];
-    const double* Ws = nullptr; const double* Ds = nullptr;
-    if constexpr (STORED) {
-      Ws = a.Wv + (size_t)grp_off * C::WSZ * 32 + tx;
-      if constexpr (EPI == EPI_BJ) Ds = a.Dv + (size_t)grp_off * C::DSZ * 32 + tx;
+  __syncthreads();
+  if constexpr (C::NBUF == 2) {
+    if (tile < ntiles) stage_tile<N1>(a, smem, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, &bars[0]);
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+      const int next = tile + gridDim.x;
+      double* cur = smem + (it & 1) * C::BUF;
+      if (next < ntiles) stage_tile<N1>(a, smem + ((it + 1) & 1) * C::BUF, (next % tiles_x) * TX,
+                                        (next / tiles_x) * C::TY, &bars[(it + 1) & 1]);
+      mbar_wait(&bars[it & 1], (it >> 1) & 1);
+      __syncthreads();
+      compute_tile<N1, STORED, EPI>(a, op, cur, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
+      __syncthreads();
     }
-    facet_apply<N1, STORED>(nb, Wc_v, Ws, acc);
-    facet_epilogue<N1, STORED, EPI>(a, vblk(a.nh, a.ny, i, j), V(ii, jj), Dc_v, Ds, acc, nrm);
+  } else {
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+      stage_tile<N1>(a, smem, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, &bars[0]);
+      mbar_wait(&bars[0], it & 1);
+      __syncthreads();
+      compute_tile<N1, STORED, EPI>(a, op, smem, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
+      __syncthreads();
+    }
   }
-
   if constexpr (EPI == EPI_RES) {
     if (a.partials != nullptr) {
-      __shared__ double red[NT / 32];
+      __shared__ double red[NWARP];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
       if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
       __syncthreads();
       if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < NT / 32; ++w) s += red[w];
-        a.partials[blockIdx.y * gridDim.x + blockIdx.x] = s;
+        double t = 0.0;
+        for (int q = 0; q < NWARP; ++q) t += red[q];
+        a.partials[blockIdx.x] = t;
       }
     }
   }
