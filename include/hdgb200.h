@@ -72,6 +72,20 @@ int hdg_residual(const hdg_level* lev, const double* b, const double* x, double*
 int hdg_bj_sweep(const hdg_level* lev, const double* b, const double* x_in, double* x_out,
                  void* stream);
 
+/* FSAI smoother (the reference default, multigrid.py:47-173): lower-triangular G and its
+ * transpose in CSR (HOST arrays, int32 indices, sorted), lambda_max of G'GA, Chebyshev lower
+ * fraction and omega.  Built on the host by the caller (fsai_build, multigrid.py:123-159). */
+int hdg_level_set_fsai(hdg_level* lev, int64_t n, const int32_t* g_rowptr, const int32_t* g_cols,
+                       const double* g_vals, int64_t nnz, const int32_t* gt_rowptr,
+                       const int32_t* gt_cols, const double* gt_vals, double lam_max,
+                       double cheb_fraction, double omega);
+/* z = G'(G r)  (multigrid.py:72-74) */
+int hdg_fsai_apply(const hdg_level* lev, const double* r, double* z, void* stream);
+/* `steps` Chebyshev-weighted sweeps x <- x + w_k G'G(b - A x) in place (multigrid.py:83-88);
+ * work_r, work_t: ndof scratch vectors */
+int hdg_fsai_sweeps(const hdg_level* lev, const double* b, double* x, double* work_r,
+                    double* work_t, int steps, void* stream);
+
 /* ---------------------------------------------------------------- transfers
  * Replaces p_prolongation / h_prolongation (multigrid.py:215-298) as operators:
  * prolong_add: x_fine += P e_coarse;   restrict: r_coarse = P^T r_fine.        */
@@ -98,7 +112,8 @@ int hdg_mg_create(hdg_level* const* levels, hdg_transfer* const* transfers, int 
 int hdg_mg_destroy(hdg_mg* mg);
 /* coarsest-level inverse, n x n row-major HOST pointer, n = ndof of the last level */
 int hdg_mg_set_coarse_inverse(hdg_mg* mg, const double* inv, int64_t n);
-/* x = cycle(b, x0) with nu1/nu2 block-Jacobi sweeps, visits = 1 (V) or 2 (W).
+/* x = cycle(b, x0) with nu1/nu2 smoothing sweeps (FSAI if attached to the level, else
+ * block-Jacobi), visits = 1 (V) or 2 (W).
  * x0 may be NULL (zero initial guess, as v_cycle(x0=None)).  x may alias x0.
  * If use_graph != 0 the launch sequence is captured once per (pointers, nu, visits)
  * into a CUDA graph and replayed. */

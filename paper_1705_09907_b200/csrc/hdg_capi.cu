@@ -5,6 +5,7 @@
 #include "hdg_kernels.cuh"
 
 #include <atomic>
+#define _USE_MATH_DEFINES
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -49,6 +50,12 @@ struct hdg_level {
   double* partials = nullptr;                        // per-CTA norm partials
   int npart = 0;
   long long op_bytes = 0;
+  // FSAI smoother (multigrid.py:47-88): G and G' in CSR on the device
+  bool has_fsai = false;
+  bool use_fsai = false;   // active smoother of the cycle: the one attached last
+  int *g_ptr = nullptr, *g_col = nullptr, *gt_ptr = nullptr, *gt_col = nullptr;
+  double *g_val = nullptr, *gt_val = nullptr;
+  double lam_max = 1.0, cheb_frac = 0.15, fsai_omega = 1.0;
 };
 
 struct hdg_transfer {
@@ -286,6 +293,8 @@ int hdg_level_create_stored(int nx, int ny, int p, const double* blocks, hdg_lev
 int hdg_level_destroy(hdg_level* L) {
   if (!L) return 0;
   cudaFree(L->dWh); cudaFree(L->dWv); cudaFree(L->dDh); cudaFree(L->dDv); cudaFree(L->partials);
+  cudaFree(L->g_ptr); cudaFree(L->g_col); cudaFree(L->g_val);
+  cudaFree(L->gt_ptr); cudaFree(L->gt_col); cudaFree(L->gt_val);
   delete L;
   return 0;
 }
@@ -328,6 +337,7 @@ int hdg_level_set_blockjacobi(hdg_level* L, double omega) {
     CK(cudaDeviceSynchronize());
   }
   L->has_bj = true;
+  L->use_fsai = false;
   return 0;
 }
 
@@ -373,6 +383,87 @@ int hdg_bj_sweep(const hdg_level* L, const double* b, const double* x_in, double
   MvArgs a{};
   a.x = x_in; a.b = b; a.out = x_out;
   return apply(L, EPI_BJ, a, S(stream));
+}
+
+// -------------------------------------------------------------------------------- FSAI
+
+}  // extern "C"
+template <typename T>
+static int upload(T** dst, const T* src, size_t n) {
+  cudaFree(*dst);
+  *dst = nullptr;
+  CK(cudaMalloc(dst, sizeof(T) * (n ? n : 1)));
+  if (n) CK(cudaMemcpy(*dst, src, sizeof(T) * n, cudaMemcpyHostToDevice));
+  return 0;
+}
+extern "C" {
+
+int hdg_level_set_fsai(hdg_level* L, int64_t n, const int32_t* g_ptr, const int32_t* g_col, const double* g_val,
+                       int64_t nnz, const int32_t* gt_ptr, const int32_t* gt_col, const double* gt_val,
+                       double lam_max, double cheb_fraction, double omega) {
+  if (!L) return fail(HDG_EINVAL, "null level");
+  if (n != L->ndof) return fail(HDG_EINVAL, "FSAI factor size != level ndof");
+  int rc;
+  if ((rc = upload(&L->g_ptr, g_ptr, n + 1)) || (rc = upload(&L->g_col, g_col, nnz)) ||
+      (rc = upload(&L->g_val, g_val, nnz)) || (rc = upload(&L->gt_ptr, gt_ptr, n + 1)) ||
+      (rc = upload(&L->gt_col, gt_col, nnz)) || (rc = upload(&L->gt_val, gt_val, nnz)))
+    return rc;
+  L->lam_max = lam_max; L->cheb_frac = cheb_fraction; L->fsai_omega = omega;
+  L->has_fsai = true;
+  L->use_fsai = true;
+  return 0;
+}
+
+static int spmv(const hdg_level* L, bool transposed, const double* x, double* y, const double* xin, double w,
+                cudaStream_t s) {
+  const int n = (int)L->ndof;
+  if (n == 0) return 0;
+  const int bs = 256;
+  const unsigned grid = (unsigned)(((long long)n * 4 + bs - 1) / bs);
+  const int* rp = transposed ? L->gt_ptr : L->g_ptr;
+  const int* ci = transposed ? L->gt_col : L->g_col;
+  const double* v = transposed ? L->gt_val : L->g_val;
+  if (xin) csr_spmv_kernel<true><<<grid, bs, 0, s>>>(n, rp, ci, v, x, y, xin, w);
+  else csr_spmv_kernel<false><<<grid, bs, 0, s>>>(n, rp, ci, v, x, y, nullptr, 0.0);
+  CKL();
+  return 0;
+}
+
+// Chebyshev-weighted steps (multigrid.py:76-81)
+static double fsai_weight(const hdg_level* L, int k, int steps) {
+  const double lo = L->cheb_frac * L->lam_max, hi = L->lam_max;
+  const double mid = 0.5 * (hi + lo), half = 0.5 * (hi - lo);
+  const double theta = mid + half * std::cos(M_PI * (2.0 * k - 1.0) / (2.0 * steps));
+  return L->fsai_omega / theta;
+}
+
+int hdg_fsai_apply(const hdg_level* L, const double* r, double* z, void* stream) {
+  if (!L || !L->has_fsai) return fail(HDG_ESTATE, "FSAI state not set");
+  if (L->ndof == 0) return 0;
+  double* t = nullptr;
+  CK(cudaMallocAsync(&t, sizeof(double) * L->ndof, S(stream)));
+  int rc = spmv(L, false, r, t, nullptr, 0.0, S(stream));
+  if (!rc) rc = spmv(L, true, t, z, nullptr, 0.0, S(stream));
+  cudaFreeAsync(t, S(stream));
+  return rc;
+}
+
+static int fsai_sweeps(const hdg_level* L, const double* b, double* x, double* r, double* t, int steps,
+                       cudaStream_t s) {
+  for (int k = 1; k <= steps; ++k) {
+    int rc;
+    if ((rc = hdg_residual(L, b, x, r, nullptr, s))) return rc;               // r = b - A x
+    if ((rc = spmv(L, false, r, t, nullptr, 0.0, s))) return rc;             // t = G r
+    if ((rc = spmv(L, true, t, x, x, fsai_weight(L, k, steps), s))) return rc;  // x += w G't
+  }
+  return 0;
+}
+
+int hdg_fsai_sweeps(const hdg_level* L, const double* b, double* x, double* work_r, double* work_t, int steps,
+                    void* stream) {
+  if (!L || !L->has_fsai) return fail(HDG_ESTATE, "FSAI state not set");
+  if (L->ndof == 0 || steps < 1) return 0;
+  return fsai_sweeps(L, b, x, work_r, work_t, steps, S(stream));
 }
 
 // ---------------------------------------------------------------------------- transfers
@@ -495,7 +586,10 @@ int hdg_mg_create(hdg_level* const* levels, hdg_transfer* const* transfers, int 
         return fail(HDG_EINVAL, "transfer k must map level k+1 into level k");
       }
       mg->T.push_back(t);
-      if (!levels[k]->has_bj) { delete mg; return fail(HDG_ESTATE, "every non-coarsest level needs a smoother"); }
+      if (!levels[k]->has_bj && !levels[k]->has_fsai) {
+        delete mg;
+        return fail(HDG_ESTATE, "every non-coarsest level needs a smoother");
+      }
     }
   }
   mg->X.assign(n, nullptr); mg->Tm.assign(n, nullptr); mg->B.assign(n, nullptr); mg->R.assign(n, nullptr);
@@ -506,7 +600,7 @@ int hdg_mg_create(hdg_level* const* levels, hdg_transfer* const* transfers, int 
       CK(cudaMalloc(&mg->B[k], bytes));
     }
     CK(cudaMalloc(&mg->Tm[k], bytes));
-    if (k + 1 < n && mg->T[k]->is_h) CK(cudaMalloc(&mg->R[k], bytes));
+    if (k + 1 < n) CK(cudaMalloc(&mg->R[k], bytes));
   }
   CK(cudaStreamCreateWithFlags(&mg->cs, cudaStreamNonBlocking));
   *out = mg;
@@ -568,9 +662,14 @@ static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1
   double* cur = xk;
   double* oth = mg->Tm[k];
   int rc;
-  for (int it = 0; it < nu1; ++it) {
-    if ((rc = hdg_bj_sweep(L, b, cur, oth, s))) return rc;
-    std::swap(cur, oth);
+  const bool fsai = L->use_fsai;   // the smoother attached last (FSAI or block-Jacobi)
+  if (fsai) {
+    if ((rc = fsai_sweeps(L, b, cur, mg->R[k], oth, nu1, s))) return rc;
+  } else {
+    for (int it = 0; it < nu1; ++it) {
+      if ((rc = hdg_bj_sweep(L, b, cur, oth, s))) return rc;
+      std::swap(cur, oth);
+    }
   }
   hdg_transfer* T = mg->T[k];
   if (!T->is_h) {
@@ -585,9 +684,13 @@ static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1
   for (int v = 0; v < visits; ++v)
     if ((rc = cycle_rec(mg, k + 1, mg->B[k + 1], v == 0, nu1, nu2, visits, s))) return rc;
   if ((rc = hdg_prolong_add(T, mg->X[k + 1], cur, s))) return rc;
-  for (int it = 0; it < nu2; ++it) {
-    if ((rc = hdg_bj_sweep(L, b, cur, oth, s))) return rc;
-    std::swap(cur, oth);
+  if (fsai) {
+    if ((rc = fsai_sweeps(L, b, cur, mg->R[k], oth, nu2, s))) return rc;
+  } else {
+    for (int it = 0; it < nu2; ++it) {
+      if ((rc = hdg_bj_sweep(L, b, cur, oth, s))) return rc;
+      std::swap(cur, oth);
+    }
   }
   if (cur != xk && L->ndof > 0) CK(cudaMemcpyAsync(xk, cur, bytes, cudaMemcpyDeviceToDevice, s));
   return 0;

@@ -521,35 +521,34 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
   extern __shared__ __align__(16) double smem[];
   const int tiles_x = (a.nx + TX - 1) / TX;
   const int ntiles = tiles_x * ((a.ny + C::TY - 1) / C::TY);
-  __shared__ __align__(8) uint64_t bars[2];
+  constexpr int NB = C::NBUF;
+  __shared__ __align__(8) uint64_t bars[NB];
   double nrm = 0.0;
-  int tile = blockIdx.x;
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], NWARP + NT);   // lane-0 expect_tx arrivals + per-thread LDGSTS arrivals
-    mbar_init(&bars[1], NWARP + NT);
+#pragma unroll
+    for (int q = 0; q < NB; ++q) mbar_init(&bars[q], NWARP + NT);  // lane-0 expect_tx + per-thread LDGSTS arrivals
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if constexpr (C::NBUF == 2) {
-    if (tile < ntiles) stage_tile<N1>(a, smem, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, &bars[0]);
-    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-      const int next = tile + gridDim.x;
-      double* cur = smem + (it & 1) * C::BUF;
-      if (next < ntiles) stage_tile<N1>(a, smem + ((it + 1) & 1) * C::BUF, (next % tiles_x) * TX,
-                                        (next / tiles_x) * C::TY, &bars[(it + 1) & 1]);
-      mbar_wait(&bars[it & 1], (it >> 1) & 1);
-      __syncthreads();
-      compute_tile<N1, STORED, EPI>(a, op, cur, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
-      __syncthreads();
+  // ring of NB stage buffers: tiles blockIdx.x + it*grid; prefetch distance NB-1
+#pragma unroll
+  for (int q = 0; q < NB - 1; ++q) {
+    const int t = blockIdx.x + q * gridDim.x;
+    if (t < ntiles) stage_tile<N1>(a, smem + q * C::BUF, (t % tiles_x) * TX, (t / tiles_x) * C::TY, &bars[q]);
+  }
+  int slot = 0;
+  unsigned phase = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int pre = tile + (NB - 1) * gridDim.x;
+    if (pre < ntiles) {
+      const int ps = (slot + NB - 1) % NB;
+      stage_tile<N1>(a, smem + ps * C::BUF, (pre % tiles_x) * TX, (pre / tiles_x) * C::TY, &bars[ps]);
     }
-  } else {
-    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-      stage_tile<N1>(a, smem, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, &bars[0]);
-      mbar_wait(&bars[0], it & 1);
-      __syncthreads();
-      compute_tile<N1, STORED, EPI>(a, op, smem, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
-      __syncthreads();
-    }
+    mbar_wait(&bars[slot], phase);
+    __syncthreads();
+    compute_tile<N1, STORED, EPI>(a, op, smem + slot * C::BUF, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
+    __syncthreads();
+    if (++slot == NB) { slot = 0; phase ^= 1u; }
   }
   if constexpr (EPI == EPI_RES) {
     if (a.partials != nullptr) {
@@ -860,6 +859,26 @@ __global__ void sum_partials_kernel(const double* __restrict__ partials, int n, 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (threadIdx.x == 0) *out = s;
+}
+
+// ------------------------------------------------------------------------------ FSAI (CSR)
+// y = M x  or  x_out = x_in + w (M x)   (multigrid.py:72-74, 83-88); 4 lanes per row
+template <bool AXPY>
+__global__ void csr_spmv_kernel(int n, const int* __restrict__ rowptr, const int* __restrict__ cols,
+                                const double* __restrict__ vals, const double* __restrict__ x, double* __restrict__ y,
+                                const double* __restrict__ xin, double w) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 2;
+  const int sub = threadIdx.x & 3;
+  double s = 0.0;
+  if (row < n) {
+    const int e = __ldg(rowptr + row + 1);
+    for (int k = __ldg(rowptr + row) + sub; k < e; k += 4) s = fma(__ldg(vals + k), __ldg(x + __ldg(cols + k)), s);
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  if (row < n && sub == 0) {
+    if constexpr (AXPY) y[row] = fma(w, s, xin[row]); else y[row] = s;
+  }
 }
 
 // CG vector updates (trace.py:156-161): x += a d, r -= a ad ;  d = z + beta d

@@ -1,0 +1,174 @@
+"""FSAI smoother: host setup, device application (reference: multigrid.py:38-173).
+
+Setup (host, once per level) restates `fsai_build`: for every row i of the lower-triangular
+pattern, solve the dense SPD principal system A[P_i, P_i] g = e_last and scale g by
+1/sqrt(g_last) (multigrid.py:133-152) - here batched over all rows at once (rows padded to a
+common length with identity blocks).  lambda_max of G'G A by the same 20-step power
+iteration with seed 1234 (multigrid.py:162-173), Chebyshev sweep weights on
+[frac lambda_max, lambda_max] (multigrid.py:76-81).
+
+Application runs on the device: x <- x + w_k G'(G(b - A x)) is one residual kernel + two CSR
+SpMV kernels (the second fused with the update) per sweep (hdg_fsai_sweeps).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _device as dev
+from ._lib import check, lib
+
+CHEB_LOWER_FRACTION = 0.15             # multigrid.py:43
+CHEB_LOWER_FRACTION_AGGRESSIVE = 0.30  # multigrid.py:44
+
+
+class NotSPDError(RuntimeError):
+    """multigrid.py:34."""
+
+
+def _aggressive_pattern(A, power, max_complexity):
+    """multigrid.py:91-120: lower(|A|^power), the strongest extra couplings filling the budget."""
+    absA = sp.csr_matrix((np.abs(A.data), A.indices, A.indptr), shape=A.shape)
+    W = absA
+    for _ in range(power - 1):
+        W = (W @ absA).tocsr()
+    lower = sp.tril(W, format="coo")
+    base = sp.tril(A, format="coo")
+    budget = int((max_complexity * A.nnz + A.shape[0]) // 2)
+    if lower.nnz <= budget:
+        return lower.tocsr()
+    n = A.shape[0]
+    key_low = lower.row.astype(np.int64) * n + lower.col
+    in_base = np.isin(key_low, base.row.astype(np.int64) * n + base.col)
+    extras = np.flatnonzero(~in_base)
+    room = max(budget - int(in_base.sum()), 0)
+    order = extras[np.argsort(-lower.data[extras], kind="stable")][:room]
+    keep = np.concatenate([np.flatnonzero(in_base), order])
+    return sp.coo_matrix((np.ones(keep.size), (lower.row[keep], lower.col[keep])), shape=A.shape).tocsr()
+
+
+def _rows_solve(A, pattern):
+    """All FSAI rows at once: (n, L, L) principal blocks, real entries at the end of each row."""
+    n = A.shape[0]
+    counts = np.diff(pattern.indptr)
+    L = int(counts.max()) if n else 0
+    cols = np.zeros((n, L), np.int64)
+    valid = np.zeros((n, L), bool)
+    rr = np.repeat(np.arange(n), counts)
+    pos = np.arange(pattern.nnz) - np.repeat(pattern.indptr[:-1], counts) + np.repeat(L - counts, counts)
+    cols[rr, pos] = pattern.indices
+    valid[rr, pos] = True
+    out = np.empty(pattern.nnz)
+    chunk = max(1, (1 << 24) // max(L * L, 1))
+    Acsr = A.tocsr()
+    for s in range(0, n, chunk):
+        c = cols[s:s + chunk]
+        v = valid[s:s + chunk]
+        m = c.shape[0]
+        sub = np.asarray(Acsr[np.repeat(c, L, axis=1).ravel(), np.tile(c, (1, L)).ravel()]).reshape(m, L, L)
+        mask2 = v[:, :, None] & v[:, None, :]
+        sub = np.where(mask2, sub, 0.0)
+        eye = np.broadcast_to(np.eye(L), sub.shape)
+        sub = np.where((~v)[:, :, None] & (~v)[:, None, :], eye, sub)
+        rhs = np.zeros((m, L))
+        rhs[:, -1] = 1.0
+        try:
+            g = np.linalg.solve(sub, rhs[:, :, None])[:, :, 0]
+        except np.linalg.LinAlgError as exc:
+            raise NotSPDError("singular principal submatrix in FSAI") from exc
+        if np.any(g[:, -1] <= 0.0):
+            bad = s + int(np.flatnonzero(g[:, -1] <= 0.0)[0])
+            raise NotSPDError(f"non-SPD principal submatrix in FSAI row {bad}")
+        g = g / np.sqrt(g[:, -1:])
+        out[pattern.indptr[s]:pattern.indptr[min(s + chunk, n)]] = g[v]
+    return out
+
+
+class FSAISmoother:
+    """multigrid.py:47-88 with device application.  Host attributes match the reference
+    (G, Gt scipy CSR; omega, aggressiveness, complexity, lam_max, cheb_fraction)."""
+
+    def __init__(self, G, omega, aggressiveness, complexity, lam_max, cheb_fraction):
+        self.G = G
+        self.Gt = G.T.tocsr()
+        self.omega = omega
+        self.aggressiveness = aggressiveness
+        self.complexity = complexity
+        self.lam_max = lam_max
+        self.cheb_fraction = cheb_fraction
+        self.block_op = None
+
+    def sweep_weights(self, steps):
+        lo, hi = self.cheb_fraction * self.lam_max, self.lam_max
+        mid, half = 0.5 * (hi + lo), 0.5 * (hi - lo)
+        k = np.arange(1, steps + 1)
+        return self.omega / (mid + half * np.cos(np.pi * (2 * k - 1) / (2 * steps)))
+
+    # -- device ------------------------------------------------------------------------------
+    def bind(self, block_op):
+        """Upload G and G' to the level's native handle (hdg_level_set_fsai)."""
+        G, Gt = self.G.tocsr(), self.Gt
+        G.sort_indices()
+        Gt.sort_indices()
+        arrs = [np.ascontiguousarray(a) for a in (G.indptr.astype(np.int32), G.indices.astype(np.int32), G.data,
+                                                  Gt.indptr.astype(np.int32), Gt.indices.astype(np.int32), Gt.data)]
+        check(lib.hdg_level_set_fsai(block_op.handle, G.shape[0], arrs[0].ctypes.data, arrs[1].ctypes.data,
+                                     arrs[2].ctypes.data, G.nnz, arrs[3].ctypes.data, arrs[4].ctypes.data,
+                                     arrs[5].ctypes.data, float(self.lam_max), float(self.cheb_fraction),
+                                     float(self.omega)))
+        self.block_op = block_op
+        return self
+
+    def apply_inverse(self, r):
+        """G'(G r) on the device (multigrid.py:72-74)."""
+        rd, was_np = dev.to_device(r)
+        out = dev.empty(rd.numel())
+        check(lib.hdg_fsai_apply(self.block_op.handle, dev.ptr(rd), dev.ptr(out), dev.stream()))
+        return dev.back(out, was_np)
+
+    def smooth(self, matvec, b, x, steps):
+        """multigrid.py:83-88 on the device (the level's own operator is applied)."""
+        if steps < 1:
+            return x
+        bd, was_np = dev.to_device(b)
+        xd = dev.to_device(x)[0].clone()
+        n = xd.numel()
+        r, t = dev.empty(n), dev.empty(n)
+        check(lib.hdg_fsai_sweeps(self.block_op.handle, dev.ptr(bd), dev.ptr(xd), dev.ptr(r), dev.ptr(t),
+                                  int(steps), dev.stream()))
+        return dev.back(xd, was_np)
+
+
+def _estimate_lam_max(A, G, iters=20, seed=1234):
+    """multigrid.py:162-173 (host, deterministic)."""
+    Gt = G.T.tocsr()
+    v = np.random.default_rng(seed).standard_normal(A.shape[0])
+    lam = 1.0
+    for _ in range(iters):
+        w = Gt @ (G @ (A @ v))
+        lam = np.linalg.norm(w)
+        if lam == 0.0:
+            return 1.0
+        v = w / lam
+    return lam
+
+
+def fsai_build(A, aggressiveness=1, omega=1.0, max_complexity=2.85):
+    """multigrid.py:123-159."""
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    n = A.shape[0]
+    if aggressiveness == 1:
+        pattern = sp.tril(A, format="csr")
+    else:
+        pattern = _aggressive_pattern(A, aggressiveness, max_complexity)
+    pattern.sort_indices()
+    data = _rows_solve(A, pattern) if n else np.zeros(0)
+    G = sp.csr_matrix((data, pattern.indices.astype(np.int64), pattern.indptr.astype(np.int64)), shape=(n, n))
+    complexity = (2 * G.nnz - n) / A.nnz if A.nnz else 1.0
+    lam_max = _estimate_lam_max(A, G) if n else 1.0
+    frac = CHEB_LOWER_FRACTION if aggressiveness == 1 else CHEB_LOWER_FRACTION_AGGRESSIVE
+    return FSAISmoother(G, omega, aggressiveness, complexity, lam_max, frac)

@@ -20,16 +20,13 @@ from . import _device as dev
 from ._lib import check, lib
 from .discretization import (ElementClasses, classify_rows, galerkin_h, galerkin_p, h_child_maps,
                              h_cross_maps, h_halves, p_transfer_matrix, ref_element)
+from .fsai import FSAISmoother, NotSPDError, fsai_build  # noqa: F401  (re-exported like the reference)
 from .mesh import coarsen
 from .trace import BlockOperator, TraceLayout, TraceSystem
 
 
 class HierarchyError(ValueError):
     """multigrid.py:30."""
-
-
-class NotSPDError(RuntimeError):
-    """multigrid.py:34."""
 
 
 # ------------------------------------------------------------------------- operators
@@ -289,11 +286,11 @@ def h_prolongation(fine_sys, coarse_sys, spec=None, tau_per_facet=None):
     return Prolongation(fine_sys.operator, coarse_sys.operator, "h", halves=halves, cross=cross)
 
 
-def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother="baseline", omega=1.0,
+def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother="baseline", omega=None,
                     threads=1):
     """multigrid.py:301-342: orders p..1 on the fine mesh, then halving at p = 1, Galerkin
-    operators, Pᵀ-cascaded right-hand sides.  smoother: "blockjacobi" (north star; omega
-    defaults to 0.8 when left at the reference default 1.0 is NOT applied - pass it), None."""
+    operators, P^T-cascaded right-hand sides.  smoother: "baseline" | "aggressive" (FSAI, the
+    reference default, omega 1.0) | "blockjacobi" (north star, omega 0.8) | None."""
     if p < 1:
         raise HierarchyError("fine order must be >= 1")
     fine = TraceSystem(mesh, p, spec, tau_per_facet, threads=threads)
@@ -344,16 +341,21 @@ def _rhs(level):
     return level.rhs.resolve() if isinstance(level.rhs, _LazyRhs) else level.rhs
 
 
-def attach_smoothers(levels, mode, omega=1.0):
-    """multigrid.py:345-352.  mode "blockjacobi" (omega 1.0 -> the north-star 0.8 unless given)."""
-    if mode not in ("blockjacobi", "bj"):
-        if mode in ("baseline", "aggressive") or isinstance(mode, int):
-            raise NotImplementedError(
-                "FSAI smoothers are not on the device path yet; use smoother='blockjacobi'")
+def attach_smoothers(levels, mode, omega=None):
+    """multigrid.py:345-352 on every level but the coarsest.  mode: "baseline" (FSAI on the
+    pattern of A), "aggressive" (pattern of A^2), an int power, or "blockjacobi".  omega
+    defaults: FSAI 1.0 (reference), block-Jacobi 0.8 (north star)."""
+    if mode in ("blockjacobi", "bj"):
+        w = 0.8 if omega is None else float(omega)
+        for lev in levels[:-1]:
+            lev.smoother = BlockJacobiSmoother(lev.block_op, w)
+        return levels
+    power = {"baseline": 1, "aggressive": 2}.get(mode, mode)
+    if not isinstance(power, int) or isinstance(power, bool) or power < 1:
         raise ValueError(f"unknown smoother mode {mode!r}")
-    w = 0.8 if omega in (None, 1.0) else float(omega)
+    w = 1.0 if omega is None else float(omega)
     for lev in levels[:-1]:
-        lev.smoother = BlockJacobiSmoother(lev.block_op, w)
+        lev.smoother = fsai_build(lev.operator.tocsr(), power, w).bind(lev.block_op)
     return levels
 
 
@@ -417,8 +419,8 @@ def _native_mg(levels):
     mg = _MG_CACHE.get(key)
     if mg is None or any(a is not b for a, b in zip(mg.levels, levels)):
         for lev in levels[:-1]:
-            if not isinstance(lev.smoother, BlockJacobiSmoother):
-                raise NotImplementedError("the device cycle needs block-Jacobi smoothers on every level")
+            if not isinstance(lev.smoother, (BlockJacobiSmoother, FSAISmoother)):
+                raise NotImplementedError("the device cycle needs a block-Jacobi or FSAI smoother on every level")
         mg = _NativeMG(list(levels))
         _MG_CACHE[key] = mg
     return mg

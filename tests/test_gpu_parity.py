@@ -241,3 +241,45 @@ def test_vcycle_graph_replay_and_zero_input(P):
     x0c = x0.copy()
     assert rel(P.mg.v_cycle(levels, b, x0), O.v_cycle(lo, b, x0)) < TOL
     np.testing.assert_array_equal(x0, x0c)                                       # x0 not mutated
+
+
+# ------------------------------------------------------------------------------- FSAI
+
+
+@pytest.mark.parametrize("tag,n,p", [("m8p3", 8, 3), ("m4p2", 4, 2)])
+def test_fsai_solve_matches_golden(P, golden, tag, n, p):
+    """Reference default smoother (FSAI baseline, multigrid.py:47-173) on the device:
+    identical lambda_max, iteration count and residual history."""
+    g = golden("hierarchies.npz")
+    levels = P.mg.build_hierarchy(P.mesh(n, n), p, specs.manufactured(P.pb.ProblemSpec), smoother="baseline")
+    lam = [lev.smoother.lam_max for lev in levels[:-1]]
+    assert rel(lam, g[f"{tag}_fsai_lam"]) < 1e-10
+    x, mon = P.mg.solve_mg(levels)
+    history_close(mon.residuals, g[f"{tag}_fsai_res"])
+    assert rel(x, g[f"{tag}_fsai_x"]) < 1e-10
+
+
+def test_fsai_smoother_api(P):
+    levels = P.mg.build_hierarchy(P.mesh(8, 8), 2, specs.manufactured(P.pb.ProblemSpec), smoother="baseline")
+    lo = O.build_levels(O.Grid(8, 8), 2, specs.manufactured(O.Spec), smoother="baseline")
+    rng = np.random.default_rng(8)
+    for lev, ol in zip(levels[:-1], lo[:-1]):
+        r = rng.standard_normal(lev.ndof)
+        assert rel(lev.smoother.apply_inverse(r), ol.smoother.apply_inverse(r)) < TOL
+        b = rng.standard_normal(lev.ndof)
+        x0 = rng.standard_normal(lev.ndof)
+        got = lev.smoother.smooth(lev.matvec, b, x0, 3)
+        ref = ol.smoother.smooth(ol.matvec, b, x0, 3)
+        assert rel(got, ref) < TOL
+    b = levels[0].rhs
+    assert rel(P.mg.v_cycle(levels, b), O.v_cycle(lo, b)) < TOL
+
+
+def test_aggressive_fsai_converges_fast(P):
+    """test_multigrid.py:267-270: aggressive FSAI V-cycle rate <= 0.05."""
+    levels = P.mg.build_hierarchy(P.mesh(8, 8), 3, specs.manufactured(P.pb.ProblemSpec), smoother="aggressive")
+    _, mon = P.mg.solve_mg(levels, tol=1e-13)
+    assert mon.asymptotic_rate() <= 0.05
+    lo = O.build_levels(O.Grid(8, 8), 3, specs.manufactured(O.Spec), smoother="aggressive")
+    _, mo = O.solve_mg(lo, tol=1e-13)
+    assert len(mon.residuals) == len(mo.residuals)

@@ -89,3 +89,38 @@ def test_config1_rhs_matches_golden(golden):
     s = TraceSystem(build_cartesian(64, 64), 2, config1_problem())
     assert rel(s.rhs, g["b"]) < 1e-12
     assert rel(s.assemble_csr() @ g["b"], g["Ab"]) < 1e-12
+
+
+# ------------------------------------------------------------------------------ FSAI setup
+
+
+@pytest.mark.parametrize("power", [1, 2])
+def test_fsai_factor_matches_oracle(power):
+    from paper_1705_09907_b200.fsai import fsai_build
+    s = TraceSystem(build_cartesian(8, 8), 3, specs.manufactured(ProblemSpec))
+    A = s.assemble_csr()
+    sm = fsai_build(A, power)
+    so = O.FSAI(A, power)
+    assert (sm.G != so.G).nnz == 0 or rel(sm.G.toarray(), so.G.toarray()) < 1e-12
+    assert abs(sm.lam_max - so.lam_max) < 1e-10 * so.lam_max
+    assert abs(sm.complexity - so.complexity) < 1e-12
+    np.testing.assert_allclose(sm.sweep_weights(3), so.sweep_weights(3), rtol=1e-12)
+
+
+def test_fsai_complexity_bands():
+    # test_multigrid.py:165-174: baseline complexity 1, aggressive in [2, 3]
+    from paper_1705_09907_b200.fsai import fsai_build
+    A4 = TraceSystem(build_cartesian(4, 4), 2, specs.manufactured(ProblemSpec)).assemble_csr()
+    assert abs(fsai_build(A4, 1).complexity - 1.0) < 1e-12
+    A16 = TraceSystem(build_cartesian(16, 16), 4, specs.manufactured(ProblemSpec)).assemble_csr()
+    assert 2.0 <= fsai_build(A16, 2).complexity <= 3.0
+
+
+def test_fsai_exact_for_diagonal_and_rejects_indefinite():
+    import scipy.sparse as sp
+    from paper_1705_09907_b200.fsai import NotSPDError, fsai_build
+    d = np.array([4.0, 1.0, 9.0, 16.0])
+    sm = fsai_build(sp.diags(d).tocsr(), 1)                       # test_multigrid.py:153-162
+    np.testing.assert_allclose(sm.G.toarray(), np.diag(1.0 / np.sqrt(d)), atol=1e-14)
+    with pytest.raises(NotSPDError):                              # test_multigrid.py:183-186
+        fsai_build(sp.csr_matrix(np.array([[1.0, 2.0], [2.0, 1.0]])), 1)
