@@ -49,46 +49,52 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region (NVML in a background
+    thread every ~2 ms; the timed regions are tens of ms)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, index=0):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.stop = index, [], threading.Event()
+        self.max_mhz = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            masks = {k: getattr(N, v) for k, v in self.NAMES.items()}
+
+            def run():
+                while not self.stop.is_set():
+                    try:
+                        sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                        rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((float(sm), [k for k, m in masks.items() if rs & m]))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.t = threading.Thread(target=run, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+        except Exception:
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.t is not None:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4)
-                          if len(r) > 3 + k and r[3 + k].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({x for r in self.rows for x in r[1]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(sm), "source": "nvml"}
 
 
 def dist_init(n_gpus):
@@ -175,7 +181,19 @@ def run_ours(args, rank, ws):
     from paper_1705_09907_b200.trace import TraceSystem
     lib = P.lib
 
-    sysg = TraceSystem(build_cartesian(N_MESH, N_MESH), P_ORDER, constant_problem(0.0, 1.0))
+    strip = None
+    if ws == 1:
+        sysg = TraceSystem(build_cartesian(N_MESH, N_MESH), P_ORDER, constant_problem(0.0, 1.0))
+    else:
+        # weak scaling: rank r owns element rows [1024 r, 1024 (r+1)) of a 1024 x 1024*ws mesh
+        # of square elements (SURVEY 8(e) strips); ghost rows refreshed by NCCL before each apply
+        from paper_1705_09907_b200.distributed import StripLayout, StripOperator
+        from paper_1705_09907_b200.mesh import Mesh
+        L = StripLayout(N_MESH, N_MESH * ws, P_ORDER, ws, rank)
+        h_el = 1.0 / N_MESH
+        blk = TraceSystem(Mesh(4, 4, 0.0, 0.0, h_el, h_el), P_ORDER, constant_problem(0.0, 1.0)).operator.S_cls
+        sysg = TraceSystem.from_blocks(Mesh(N_MESH, L.nyl, 0.0, L.lo * h_el, h_el, h_el), P_ORDER, blk)
+        strip = StripOperator(L, sysg.operator.apply)
     ndof = sysg.ndof
     op = sysg.operator
     h = op.handle
@@ -191,6 +209,8 @@ def run_ours(args, rank, ws):
     def step():
         for a in range(APPLIES):
             k = a % NB
+            if strip is not None:
+                strip.exchange(xs[k])
             P._lib.check(lib.hdg_matvec(h, xs[k].data_ptr(), ys[k].data_ptr(), sp))
 
     # ---- device-resident throughput
@@ -211,7 +231,8 @@ def run_ours(args, rank, ws):
     t_ms = barrier_max(ev0.elapsed_time(ev1), ws)
     applies = APPLIES * args.steps
     kernel_us = t_ms * 1e3 / applies
-    value = ws * ndof * applies / (t_ms * 1e-3) / 1e9
+    owned = int(strip.L.owned.sum()) if strip is not None else ndof
+    value = ws * owned * applies / (t_ms * 1e-3) / 1e9
 
     # single-launch event timing of the dominant kernel (same stream)
     e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -231,7 +252,7 @@ def run_ours(args, rank, ws):
         xd = x_pin.to("cuda", non_blocking=True)
         y = None
         for _ in range(APPLIES):
-            y = sysg.matvec_free(xd)
+            y = strip.apply(xd) if strip is not None else sysg.matvec_free(xd)
         y_pin.copy_(y, non_blocking=True)
 
     for _ in range(max(args.warmup, 3)):
@@ -244,7 +265,7 @@ def run_ours(args, rank, ws):
     e1.record(stream)
     torch.cuda.synchronize()
     t_e2e = barrier_max(e0.elapsed_time(e1), ws)
-    e2e_val = ws * ndof * applies / (t_e2e * 1e-3) / 1e9
+    e2e_val = ws * owned * applies / (t_e2e * 1e-3) / 1e9
 
     # ---- parity spot check of the timed output against the host formula (cheap, sampled)
     y_chk = ys[0].cpu().numpy()
@@ -259,7 +280,8 @@ def run_ours(args, rank, ws):
             "config": {"workload": f"configs[1]: {N_MESH}x{N_MESH} quad mesh, p={P_ORDER}, K=I (shared block), "
                                    f"fp64, {APPLIES} applies/step, x~U[-1,1] seed 1",
                        "ndof": ndof, "l2": "rotating 4 (x,y) pairs = %.0f MB > 126 MB L2" % (NB * 16 * ndof / 1e6),
-                       "parallelism": "replicas" if ws > 1 else "single"},
+                       "parallelism": f"strips{ws} (1024 element rows per GPU, NCCL halo rows)" if ws > 1
+                       else "single"},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ndof, "d2h_bytes_per_step": 8 * ndof,
                     "path": "TraceSystem.matvec_free(cuda tensor) x100 after pinned H2D of x; D2H of y"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -269,10 +291,46 @@ def run_ours(args, rank, ws):
                          "fp64_tflops": flops / (kernel_us * 1e-6) / 1e12},
             "gpu_launches": int(launches),
             "clocks": clk.summary()}
+    if ws == 1 and not args.no_vcycle:
+        line["vcycle"] = vcycle_timings()
     if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(y_chk, x_host)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def vcycle_timings(steps=20):
+    """V(2,2) block-Jacobi(0.8) cycle time on the configs[1] hierarchy (1024^2, p=4, K=I, 14
+    levels) and on configs[0] (64^2, p=2, sliced to 4x4), device-resident, graph-replayed."""
+    import torch
+    from paper_1705_09907_b200 import _lib
+    from paper_1705_09907_b200.mesh import build_cartesian
+    from paper_1705_09907_b200.multigrid import _native_mg, build_hierarchy
+    from paper_1705_09907_b200.problem import config1_problem, constant_problem
+    out = {}
+    for name, (n, p, spec, cut) in {"cfg2_1024p4": (1024, 4, constant_problem(0.0, 1.0), None),
+                                    "cfg1_64p2": (64, 2, config1_problem(), 6)}.items():
+        levels = build_hierarchy(build_cartesian(n, n), p, spec, smoother=None)
+        levels = levels[:cut] if cut else levels
+        from paper_1705_09907_b200.multigrid import attach_smoothers
+        attach_smoothers(levels, "blockjacobi", 0.8)
+        mg = _native_mg(levels)
+        b = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, levels[0].ndof)).cuda()
+        x = torch.zeros_like(b)
+        st = torch.cuda.current_stream()
+        for _ in range(3):
+            _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), x.data_ptr(), x.data_ptr(), 2, 2, 1, 1,
+                                             st.cuda_stream))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), x.data_ptr(), x.data_ptr(), 2, 2, 1, 1,
+                                             st.cuda_stream))
+        e1.record(st)
+        torch.cuda.synchronize()
+        out[name] = {"ms_per_cycle": e0.elapsed_time(e1) / steps, "levels": len(levels), "ndof": levels[0].ndof}
+    return out
 
 
 def cpu_baseline(y_gpu, x_host):
@@ -297,6 +355,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-vcycle", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))

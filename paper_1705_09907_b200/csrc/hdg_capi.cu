@@ -100,11 +100,21 @@ static void host_invert(std::vector<double>& a, int n) {  // SPD Gauss-Jordan, n
   }
 }
 
+#ifndef HDG_WS
+#define HDG_WS 0
+#endif
+// warp-specialized (producer warp + compute warps) or uniform kernel
+template <int N1, bool STORED, int EPI>
+static auto kernel_ptr() {
+  if constexpr (HDG_WS) return trace_apply_ws_kernel<N1, STORED, EPI>;
+  else return trace_apply_kernel<N1, STORED, EPI>;
+}
+static constexpr int kThreads = HDG_WS ? NT + 32 : NT;
+
 template <int N1, bool STORED, int EPI>
 static int set_attr() {
   const size_t smem = Cfg<N1>::SMEM_DOUBLES * sizeof(double);
-  CK(cudaFuncSetAttribute(trace_apply_kernel<N1, STORED, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
+  CK(cudaFuncSetAttribute(kernel_ptr<N1, STORED, EPI>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   return 0;
 }
 
@@ -135,7 +145,7 @@ static int grid_for(const hdg_level* L) {
   static int occ = -1;
   if (occ < 0) {
     const size_t smem = C::SMEM_DOUBLES * sizeof(double);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, trace_apply_kernel<N1, STORED, EPI>, NT, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel_ptr<N1, STORED, EPI>(), kThreads, smem) !=
             cudaSuccess || occ < 1)
       occ = 1;
     if (occ > MAX_CTAS_PER_SM) occ = MAX_CTAS_PER_SM;
@@ -164,7 +174,7 @@ static int apply_t(const hdg_level* L, MvArgs& a, cudaStream_t s) {
   } else {
     std::memset(&op, 0, sizeof(op));
   }
-  trace_apply_kernel<N1, STORED, EPI><<<grid, NT, smem, s>>>(a, op);
+  kernel_ptr<N1, STORED, EPI>()<<<grid, kThreads, smem, s>>>(a, op);
   CKL();
   return 0;
 }

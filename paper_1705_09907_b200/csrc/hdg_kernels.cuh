@@ -41,6 +41,9 @@ namespace hdg {
 #ifndef HDG_MINB
 #define HDG_MINB 2         // __launch_bounds__ min blocks per SM for the trace kernel
 #endif
+#ifndef HDG_WS_MINB
+#define HDG_WS_MINB 2      // warp-specialized kernel: CTAs per SM the registers must allow
+#endif
 #ifndef HDG_NWARP
 #define HDG_NWARP 8
 #endif
@@ -223,6 +226,41 @@ template <int N1> __device__ __forceinline__ Run h_run(const MvArgs& a, int i0, 
   q.valid = (j >= 1 && j <= a.ny - 1);
   return q;
 }
+// V columns c = c0, c0 + cstep, ... of the tile: lane-constant element offsets hoisted out of
+// the column loop, so each copy is a pointer add, a predicate and the LDGSTS.
+template <int N1>
+__device__ __forceinline__ void stage_v_columns(const MvArgs& a, double* Vs, int i0, int j0, int c0, int cstep,
+                                                int lane) {
+  using C = Cfg<N1>;
+  constexpr int LEN = C::VROWS * N1;
+  constexpr int NQ = (LEN + 31) / 32;
+  const int elo = (j0 == 0) ? N1 : 0;                          // row j = -1
+  const int ehi = min(C::VROWS, a.ny - (j0 - 1)) * N1;         // rows j < ny
+  int soffq[NQ];
+  bool okq[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int e = lane + 32 * q;
+    const int r = e / N1, m = e - r * N1;
+    soffq[q] = (r * C::VCOLS) * C::SV + m;
+    okq[q] = (e < LEN) && e >= elo && e < ehi;
+  }
+  const long long cstride = (long long)a.ny * N1;
+  const double* src = a.x + (long long)v_run_start<N1>(a, i0, j0, c0);
+  for (int c = c0; c < C::VCOLS; c += cstep, src += cstep * cstride) {
+    const int i = i0 - 1 + c;
+    const bool colok = (i >= 1 && i <= a.nx - 1);
+    double* dst = Vs + c * C::SV;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      if (lane + 32 * q < LEN) {
+        const bool ok = colok && okq[q];
+        cp_async8(dst + soffq[q], ok ? src + lane + 32 * q : a.x, ok);
+      }
+    }
+  }
+}
+
 // Stage the x blocks of one tile's facet stencils into shared memory.  H rows
 // h(i0-1 .. i0+TX-1, j) and V columns v(i, j0-1 .. j0+TY-1) are contiguous runs of the
 // reference layout, so each is ONE bulk (TMA) copy issued by the owning warp's lane 0, plus at
@@ -251,27 +289,13 @@ __device__ __forceinline__ void stage_tile(const MvArgs& a, double* buf, int i0,
   }
   // V columns: coalesced 8-byte LDGSTS from the contiguous run, transposed into [row][col];
   // src-size 0 zero-fills Dirichlet / out-of-mesh blocks
-  {
-    double* Vs = buf + C::HSZ;
-    const int elo = (j0 == 0) ? N1 : 0;                          // row j = -1
-    const int ehi = min(C::VROWS, a.ny - (j0 - 1)) * N1;         // rows j < ny
-    for (int c = warp; c < C::VCOLS; c += NWARP) {
-      const int i = i0 - 1 + c;
-      const bool colok = (i >= 1 && i <= a.nx - 1);
-      const double* src = a.x + (colok ? v_run_start<N1>(a, i0, j0, c) : 0);
-#pragma unroll
-      for (int q = 0; q < (C::VROWS * N1 + 31) / 32; ++q) {
-        const int e = lane + 32 * q;
-        if (e < C::VROWS * N1) {
-          const int r = e / N1, m = e - r * N1;
-          const bool ok = colok && e >= elo && e < ehi;
-          cp_async8(Vs + (r * C::VCOLS + c) * C::SV + m, ok ? src + e : a.x, ok);
-        }
-      }
-    }
-  }
+  stage_v_columns<N1>(a, buf + C::HSZ, i0, j0, warp, NWARP, lane);
   cp_async_mbar_arrive(bar);           // every thread: one arrival when its LDGSTS land
 }
+
+// barrier among the NT compute threads only (named barrier 1; the warp-specialized kernel has
+// an extra producer warp that must not take part)
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory"); }
 
 // acc_f = W . [x of facet f's 7 stencil blocks] for FF facets of one orientation.
 // Shared mode: W is uniform (constant bank), each W value feeds FF facets.
@@ -464,7 +488,7 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
     }
   }
   // ---- outputs -> shared (x buffer is consumed) -> contiguous global runs
-  __syncthreads();
+  consumer_sync();
   double* Yh = buf;                       // [row r][tx][NO]
   double* Yv = buf + C::TY * TX * NO;     // [col tx][row r][NO], column stride YCS (odd)
 #pragma unroll
@@ -476,7 +500,7 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
       Yv[tx * C::YCS + r * NO + k] = ov[f][k];
     }
   }
-  __syncthreads();
+  consumer_sync();
   if (a.out == nullptr) return;  // norm-only residual
 #ifdef HDG_EXP_NOOUT
   if (a.nx > 0) return;
@@ -557,6 +581,82 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
       for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
       if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
       __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < NWARP; ++q) t += red[q];
+        a.partials[blockIdx.x] = t;
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------- warp-specialized variant
+// One producer warp (warp NWARP) streams tiles into an NB-slot ring; the NWARP compute warps
+// only compute.  full[slot]: 1 expect_tx arrival (producer lane 0) + 32 LDGSTS arrivals;
+// empty[slot]: NT consumer arrivals.
+template <int N1>
+__device__ __forceinline__ void produce_tile(const MvArgs& a, double* buf, int i0, int j0, uint64_t* full) {
+  using C = Cfg<N1>;
+  const int lane = threadIdx.x & 31;
+  const bool edge = (i0 == 0) || (j0 == 0) || (i0 + TX >= a.nx) || (j0 + C::TY >= a.ny);
+  if (edge) {
+    for (int r = 0; r < C::HROWS; ++r) run_zero(buf, h_run<N1>(a, i0, j0, r), lane);
+  }
+  stage_v_columns<N1>(a, buf + C::HSZ, i0, j0, 0, 1, lane);
+  __syncwarp();
+  if (lane == 0) {
+    unsigned bytes = 0;
+    for (int r = 0; r < C::HROWS; ++r) bytes += run_bytes(h_run<N1>(a, i0, j0, r));
+    fence_proxy_async();
+    mbar_arrive_expect_tx(full, bytes);
+    for (int r = 0; r < C::HROWS; ++r) run_issue(a.x, buf, h_run<N1>(a, i0, j0, r), full);
+  }
+  cp_async_mbar_arrive(full);
+}
+
+template <int N1, bool STORED, int EPI>
+__global__ void __launch_bounds__(NT + 32, HDG_WS_MINB)
+trace_apply_ws_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 : N1)> op) {
+  using C = Cfg<N1>;
+  constexpr int NB = C::NBUF;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t full[NB], empty[NB];
+  const int tiles_x = (a.nx + TX - 1) / TX;
+  const int ntiles = tiles_x * ((a.ny + C::TY - 1) / C::TY);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      mbar_init(&full[q], 1 + 32);
+      mbar_init(&empty[q], NT);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  int slot = 0;
+  unsigned phase = 0;
+  if (threadIdx.x >= NT) {  // ---- producer warp
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      mbar_wait(&empty[slot], phase ^ 1u);
+      produce_tile<N1>(a, smem + slot * C::BUF, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, &full[slot]);
+      if (++slot == NB) { slot = 0; phase ^= 1u; }
+    }
+    return;
+  }
+  double nrm = 0.0;             // ---- compute warps
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    mbar_wait(&full[slot], phase);
+    compute_tile<N1, STORED, EPI>(a, op, smem + slot * C::BUF, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
+    consumer_sync();
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[slot])) : "memory");
+    if (++slot == NB) { slot = 0; phase ^= 1u; }
+  }
+  if constexpr (EPI == EPI_RES) {
+    if (a.partials != nullptr) {
+      __shared__ double red[NWARP];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+      consumer_sync();
       if (threadIdx.x == 0) {
         double t = 0.0;
         for (int q = 0; q < NWARP; ++q) t += red[q];

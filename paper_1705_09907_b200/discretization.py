@@ -192,6 +192,90 @@ class NumericalBreakdown(RuntimeError):
     """local.py:27."""
 
 
+class PiecewiseCondenser:
+    """Batched condensation on the GPU for elements with an element-wise CONSTANT coefficient
+    K_e and uniform tau (configs 3/5-style heterogeneous media).
+
+    With flux mass M/K_e (local.py:144 when kq is constant on the element), eliminating the
+    flux first gives an nb x nb SPD system per element instead of the 3nb x 3nb LU
+    (local.py:208):  (Stab + K Lap) u = T_u - K G,   q = K M^-1 (T_q + B^T u), so
+        S(K) = K A0 + Ms + (K C0 + F_u) (Stab + K Lap)^-1 (T_u - K G)
+    with K-independent A0 = F_q M^-1 T_q, C0 = F_q M^-1 B^T, G = B M^-1 T_q,
+    Lap = B M^-1 B^T.  Same operator as local.py:223-237 up to rounding (checked against the
+    oracle in tests).  Returns S for all given K as a CUDA float64 tensor (E, 4n1, 4n1)."""
+
+    def __init__(self, p, dx, dy, tau):
+        ref = ref_element(p)
+        n1, nb = ref.n1, ref.nb
+        self.p, self.n1, self.nb = p, n1, nb
+        wj = ref.w2 * (dx * dy / 4.0)
+        I2 = ref.interp_2d
+        M = I2.T @ (wj[:, None] * I2)
+        Bx = 0.5 * dy * I2.T @ (ref.w2[:, None] * ref.dxi_2d)
+        By = 0.5 * dx * I2.T @ (ref.w2[:, None] * ref.deta_2d)
+        lens = (dx, dy, dx, dy)
+        fm = [0.5 * lens[s] * ref.mass1 for s in range(4)]
+        stab = np.zeros((nb, nb))
+        Tq = np.zeros((2 * nb, 4 * n1))
+        Tu = np.zeros((nb, 4 * n1))
+        Fq = np.zeros((4 * n1, 2 * nb))
+        Fu = np.zeros((4 * n1, nb))
+        Ms = np.zeros((4 * n1, 4 * n1))
+        for s in range(4):
+            idx = ref.side_nodes[s]
+            cols = slice(s * n1, (s + 1) * n1)
+            stab[np.ix_(idx, idx)] += tau * fm[s]
+            for d in range(2):
+                ns = NORMALS[s, d]
+                if ns != 0.0:
+                    Tq[d * nb + idx, cols] += ns * fm[s]
+                    Fq[cols, d * nb + idx] += ns * fm[s]
+            Tu[idx, cols] += -tau * fm[s]
+            Fu[cols, idx] += tau * fm[s]
+            Ms[cols, cols] += tau * fm[s]
+        Mi = np.linalg.inv(M)
+        B = (Bx, By)
+        self.Lap = sum(B[d] @ Mi @ B[d].T for d in range(2))
+        self.G = sum(B[d] @ Mi @ Tq[d * nb:(d + 1) * nb] for d in range(2))
+        self.A0 = sum(Fq[:, d * nb:(d + 1) * nb] @ Mi @ Tq[d * nb:(d + 1) * nb] for d in range(2))
+        self.C0 = sum(Fq[:, d * nb:(d + 1) * nb] @ Mi @ B[d].T for d in range(2))
+        self.stab, self.Tu, self.Fu, self.Ms = stab, Tu, Fu, Ms
+        self.BMi = np.hstack([Bx @ Mi, By @ Mi])                               # nb x 2nb
+        self.FqMi = np.hstack([Fq[:, :nb] @ Mi, Fq[:, nb:] @ Mi])             # 4n1 x 2nb
+
+    def condensed_loads(self, K, load_q, load_u, chunk=1 << 16):
+        """F L(K)^-1 [load_q; load_u] per element (local.py:236), the same elimination."""
+        import torch
+        dev = "cuda"
+        t = {k: torch.as_tensor(getattr(self, k), device=dev) for k in ("Lap", "C0", "stab", "Fu", "BMi", "FqMi")}
+        K = torch.as_tensor(np.asarray(K, float), device=dev)
+        fq = torch.as_tensor(load_q, device=dev)
+        fu = torch.as_tensor(load_u, device=dev)
+        out = torch.empty((K.numel(), 4 * self.n1), dtype=torch.float64, device=dev)
+        for s0 in range(0, K.numel(), chunk):
+            k = K[s0:s0 + chunk][:, None]
+            H = t["stab"] + k[:, :, None] * t["Lap"]
+            rhs = fu[s0:s0 + chunk] - k * (fq[s0:s0 + chunk] @ t["BMi"].T)
+            u = torch.linalg.solve(H, rhs[:, :, None])[:, :, 0]
+            out[s0:s0 + chunk] = k * (fq[s0:s0 + chunk] @ t["FqMi"].T) + \
+                k * (u @ t["C0"].T) + u @ t["Fu"].T
+        return out.cpu().numpy()
+
+    def blocks(self, K, chunk=1 << 15):
+        import torch
+        dev = "cuda"
+        t = {k: torch.as_tensor(getattr(self, k), device=dev) for k in ("Lap", "G", "A0", "C0", "stab", "Tu", "Fu", "Ms")}
+        K = torch.as_tensor(np.asarray(K, float), device=dev)
+        E = K.numel()
+        out = torch.empty((E, 4 * self.n1, 4 * self.n1), dtype=torch.float64, device=dev)
+        for s0 in range(0, E, chunk):
+            k = K[s0:s0 + chunk][:, None, None]
+            H = t["stab"] + k * t["Lap"]
+            U = torch.linalg.solve(H, t["Tu"] - k * t["G"])
+            out[s0:s0 + chunk] = k * t["A0"] + t["Ms"] + (k * t["C0"] + t["Fu"]) @ U
+        return out
+
+
 def classify_rows(rows):
     """Unique rows -> (unique_rows, inverse).  Fast path when every row is equal."""
     rows = np.ascontiguousarray(rows)
@@ -212,8 +296,16 @@ def p_transfer_matrix(p_fine):
 
 
 def galerkin_p(S, V):
-    """S_c = Q^T S Q with Q = I_4 (x) V (the p-prolongation acts facet-locally)."""
+    """S_c = Q^T S Q with Q = I_4 (x) V (the p-prolongation acts facet-locally).
+    numpy in -> numpy out; CUDA tensor in -> CUDA tensor out (batched on the device)."""
     Q = np.kron(np.eye(4), V)
+    if not isinstance(S, np.ndarray):
+        import torch
+        Qt = torch.as_tensor(Q, device=S.device)
+        out = torch.empty((S.shape[0], Q.shape[1], Q.shape[1]), dtype=S.dtype, device=S.device)
+        for s0 in range(0, S.shape[0], 1 << 16):
+            out[s0:s0 + (1 << 16)] = Qt.T @ S[s0:s0 + (1 << 16)] @ Qt
+        return out
     return np.einsum("ai,cij,jb->cab", Q.T, S, Q)
 
 
@@ -263,4 +355,8 @@ def h_child_maps(halves, cross):
 
 def galerkin_h(S_children, Q):
     """S_c = sum_k Q_k^T S_k Q_k.  S_children (C, 4, 8, 8), Q (C, 4, 8, 8)."""
+    if not isinstance(S_children, np.ndarray):
+        import torch
+        Qt = torch.as_tensor(Q, device=S_children.device)
+        return torch.einsum("ckia,ckij,ckjb->cab", Qt, S_children, Qt)
     return np.einsum("ckia,ckij,ckjb->cab", Q, S_children, Q)

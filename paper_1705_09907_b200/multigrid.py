@@ -271,7 +271,11 @@ def _h_level(fine_op, mesh_c, spec, tau_per_facet):
     kid_cls = fine_op.elem_class[kids]                # (Ec, 4)
     rows, inv = classify_rows(np.hstack([ucls[:, None], kid_cls]))
     Q = h_child_maps(halves, cross_u[rows[:, 0]])
-    S_children = fine_op.S_cls[rows[:, 1:]]           # (C, 4, 8, 8)
+    if isinstance(fine_op.S_cls, np.ndarray):
+        S_children = fine_op.S_cls[rows[:, 1:]]       # (C, 4, 8, 8)
+    else:
+        import torch
+        S_children = fine_op.S_cls[torch.as_tensor(rows[:, 1:], device=fine_op.S_cls.device)]
     S_c = galerkin_h(S_children, Q)
     cross = cross_u if cross_u.shape[0] == 1 else cross_u[ucls]
     return S_c, inv, halves, cross

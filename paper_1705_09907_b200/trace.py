@@ -16,7 +16,7 @@ import scipy.sparse as sp
 
 from . import _device as dev
 from ._lib import check, lib
-from .discretization import ElementClasses, classify_rows, ref_element
+from .discretization import ElementClasses, NumericalBreakdown, PiecewiseCondenser, classify_rows, ref_element
 
 
 class LocalOps:
@@ -90,7 +90,9 @@ class BlockOperator:
     def __init__(self, mesh, p, S_cls, elem_class):
         self.layout = TraceLayout(mesh, p)
         self.mesh, self.p = mesh, p
-        self.S_cls = np.ascontiguousarray(S_cls, dtype=np.float64)
+        # host numpy (few classes) or a CUDA tensor (GPU-condensed heterogeneous media)
+        self.S_cls = S_cls if not isinstance(S_cls, np.ndarray) and hasattr(S_cls, "is_cuda") \
+            else np.ascontiguousarray(S_cls, dtype=np.float64)
         self.elem_class = np.asarray(elem_class, np.int64)
         self._handle = None
         self._bj_omega = None
@@ -114,7 +116,7 @@ class BlockOperator:
                 check(lib.hdg_level_create_shared(nx, ny, self.p, blk.ctypes.data, ctypes.byref(h)))
             else:
                 import torch
-                S = torch.from_numpy(self.S_cls).cuda()
+                S = self.S_cls if isinstance(self.S_cls, torch.Tensor) else torch.from_numpy(self.S_cls).cuda()
                 idx = torch.from_numpy(self.elem_class).cuda()
                 blocks = S.index_select(0, idx).contiguous()
                 check(lib.hdg_level_create_stored(nx, ny, self.p, blocks.data_ptr(), ctypes.byref(h)))
@@ -153,9 +155,13 @@ class BlockOperator:
         return float(out.item()) ** 0.5
 
     # -- host views (tests, tooling, coarse inverse) -------------------------------------
+    def host_classes(self):
+        S = self.S_cls
+        return S if isinstance(S, np.ndarray) else S.cpu().numpy()
+
     def schur(self):
         """Reference-layout blocks (E, 4n1, 4n1) with Dirichlet columns zeroed (local.py:186-188)."""
-        S = self.S_cls[self.elem_class].copy()
+        S = self.host_classes()[self.elem_class].copy()
         cm = np.repeat(self.layout.side_mask(), self.p + 1, axis=1)
         return S * cm[:, None, :]
 
@@ -185,26 +191,67 @@ class BlockOperator:
 class TraceSystem:
     """Condensed HDG system A lam = b on the interior facet skeleton (trace.py:26-69)."""
 
+    # more distinct element classes than this are condensed on the GPU (PiecewiseCondenser)
+    GPU_CLASSES = 4096
+
     def __init__(self, mesh, p, spec, tau_per_facet=None, threads=1):
         self.mesh, self.p, self.spec = mesh, p, spec
         self.ops = LocalOps(mesh, p)
         self.layout = TraceLayout(mesh, p)
         self.n_blocks, self.ndof = self.layout.n_blocks, self.layout.ndof
-        ref = self.ops.ref
         nx, ny = mesh.n_x, mesh.n_y
         E = nx * ny
-        e = np.arange(E)
-        x0 = mesh.x0 + (e % nx) * mesh.dx
-        y0 = mesh.y0 + (e // nx) * mesh.dy
-        qx, qy = ref.element_quad_points(x0, y0, mesh.dx, mesh.dy)
-        kq = np.asarray(spec.coefficient(qx, qy), float).reshape(E, -1)    # local.py:138
         tau = self._element_tau(spec, tau_per_facet)
-        rows, inv = classify_rows(np.hstack([kq, tau]))
-        nq2 = kq.shape[1]
+        kq_rows, Ke = self._sample_coefficient(spec)                      # local.py:137-140
+        self.piecewise = None
+        if Ke is not None and np.all(tau == tau[0]):
+            # element-wise constant K, uniform tau: classes by K value
+            uk, inv = np.unique(Ke, return_inverse=True)
+            if uk.size > self.GPU_CLASSES:
+                self.piecewise = PiecewiseCondenser(p, mesh.dx, mesh.dy, float(tau[0, 0]))
+                self.classes = None
+                self.elem_class = inv.reshape(-1)
+                self.class_K = uk
+                self.operator = BlockOperator(mesh, p, self.piecewise.blocks(uk), self.elem_class)
+                self.rhs = self._condensed_rhs(spec)
+                return
+            nq2 = self.ops.ref.quad.nodes.size ** 2
+            rows = np.hstack([np.repeat(uk[:, None], nq2, axis=1), np.repeat(tau[:1], uk.size, axis=0)])
+        else:
+            rows, inv = classify_rows(np.hstack([kq_rows, tau]))
+        nq2 = rows.shape[1] - 4
         self.classes = ElementClasses(p, mesh.dx, mesh.dy, rows[:, :nq2], rows[:, nq2:])
-        self.elem_class = inv
-        self.operator = BlockOperator(mesh, p, self.classes.S, inv)
-        self.rhs = self._condensed_rhs(spec, qx, qy, x0, y0)
+        self.elem_class = np.asarray(inv).reshape(-1)
+        self.operator = BlockOperator(mesh, p, self.classes.S, self.elem_class)
+        self.rhs = self._condensed_rhs(spec)
+
+    def _quad_points(self, e0, e1):
+        m = self.mesh
+        e = np.arange(e0, e1)
+        x0 = m.x0 + (e % m.n_x) * m.dx
+        y0 = m.y0 + (e // m.n_x) * m.dy
+        return self.ops.ref.element_quad_points(x0, y0, m.dx, m.dy)
+
+    def _sample_coefficient(self, spec, chunk=1 << 16):
+        """K at every element's GL points (local.py:137-138), in chunks.  Returns
+        (None, K_e) when K is constant on every element, else (kq rows, None)."""
+        E = self.mesh.n_x * self.mesh.n_y
+        Ke = np.empty(E)
+        rows = []
+        const = True
+        for e0 in range(0, E, chunk):
+            qx, qy = self._quad_points(e0, min(E, e0 + chunk))
+            kq = np.asarray(spec.coefficient(qx, qy), float).reshape(qx.shape)
+            if np.any(kq <= 0.0):
+                raise NumericalBreakdown("coefficient not positive")
+            rows.append(kq)
+            if const and np.all(kq == kq[:, :1]):
+                Ke[e0:e0 + kq.shape[0]] = kq[:, 0]
+            else:
+                const = False
+        if const:
+            return None, Ke
+        return np.concatenate(rows), None
 
     @classmethod
     def from_blocks(cls, mesh, p, S_cls, elem_class=None, rhs=None):
@@ -238,22 +285,64 @@ class TraceSystem:
         return np.stack([j * nx + i, nh + (i + 1) * ny + j, (j + 1) * nx + i, nh + i * ny + j],
                         axis=-1).reshape(-1, 4)
 
-    def _condensed_rhs(self, spec, qx, qy, x0, y0):
-        """Loads (local.py:178-184) condensed per element (local.py:236), summed over owners."""
+    def _condense_loads(self, idx, load):
+        """condensed loads of elements idx (local.py:236)"""
+        nb = self.ops.nb
+        if self.piecewise is not None:
+            K = self.class_K[self.elem_class[idx]]
+            return self.piecewise.condensed_loads(K, load[:, :2 * nb], load[:, 2 * nb:])
+        if self.classes.n == 1:
+            return load @ self.classes.Z[0].T
+        return np.einsum("eij,ej->ei", self.classes.Z[self.elem_class[idx]], load)
+
+    def _trace_cols(self, idx):
+        """unmasked trace columns T (local.py:158-176) of elements idx"""
+        if self.piecewise is not None:
+            pc = self.piecewise
+            T = np.zeros((len(idx), 3 * pc.nb, 4 * pc.n1))
+            # T_q is K-independent; T_u = -tau m on the side nodes (also K-independent)
+            return T + self._Tfull()[None]
+        return self.classes.T[self.elem_class[idx]]
+
+    def _Tfull(self):
+        ref, m = self.ops.ref, self.mesh
+        n1, nb = ref.n1, ref.nb
+        tau = float(self.spec.tau)
+        lens = (m.dx, m.dy, m.dx, m.dy)
+        T = np.zeros((3 * nb, 4 * n1))
+        for s in range(4):
+            fm = 0.5 * lens[s] * ref.mass1
+            idx = ref.side_nodes[s]
+            cols = slice(s * n1, (s + 1) * n1)
+            for d in range(2):
+                ns = (0.0, -1.0, 1.0, 0.0, 0.0, 1.0, -1.0, 0.0)[2 * s + d]
+                if ns != 0.0:
+                    T[d * nb + idx, cols] += ns * fm
+            T[2 * nb + idx, cols] += -tau * fm
+        return T
+
+    def _condensed_rhs(self, spec, chunk=1 << 16):
+        """Loads (local.py:178-184) condensed per element (local.py:236), summed over owners.
+        Source evaluated in chunks; elements with no source and no Dirichlet side add 0."""
         ref = self.ops.ref
         n1, nb = ref.n1, ref.nb
-        E = qx.shape[0]
+        m = self.mesh
+        E = m.n_x * m.n_y
         if self.ndof == 0:
             return np.zeros(0)
-        m = self.mesh
         wj = ref.w2 * (m.dx * m.dy / 4.0)
-        fq = np.asarray(spec.source(qx, qy), float).reshape(E, -1)
-        load = np.zeros((E, 3 * nb))
-        load[:, 2 * nb:] = (fq * wj) @ ref.interp_2d
+        cl = np.zeros((E, 4 * n1))
+        for e0 in range(0, E, chunk):
+            qx, qy = self._quad_points(e0, min(E, e0 + chunk))
+            fs = np.asarray(spec.source(qx, qy), float).reshape(qx.shape)
+            if not np.any(fs):
+                continue
+            load = np.zeros((fs.shape[0], 3 * nb))
+            load[:, 2 * nb:] = (fs * wj) @ ref.interp_2d
+            cl[e0:e0 + fs.shape[0]] = self._condense_loads(np.arange(e0, e0 + fs.shape[0]), load)
         inner = self.layout.side_mask()
         bnd_e, bnd_s = np.nonzero(~inner)
         if bnd_e.size:
-            lam_bc = np.zeros((E, 4 * n1))
             t = ref.quad.nodes
             nx = m.n_x
             i, j = bnd_e % nx, bnd_e // nx
@@ -263,21 +352,19 @@ class TraceSystem:
             py = m.y0 + sy * m.dy
             horiz = (bnd_s == 0) | (bnd_s == 2)
             ln = np.where(horiz, m.dx, m.dy)
-            s = ln[:, None] * (t[None, :] + 1.0) / 2.0
-            X = px[:, None] + np.where(horiz, 1.0, 0.0)[:, None] * s
-            Y = py[:, None] + np.where(horiz, 0.0, 1.0)[:, None] * s
+            sl = ln[:, None] * (t[None, :] + 1.0) / 2.0
+            X = px[:, None] + np.where(horiz, 1.0, 0.0)[:, None] * sl
+            Y = py[:, None] + np.where(horiz, 0.0, 1.0)[:, None] * sl
             g = np.asarray(spec.dirichlet(X, Y), float).reshape(X.shape)
-            rhs1 = (g * ref.quad.weights[None, :]) @ ref.interp_1d
-            proj = np.linalg.solve(ref.mass1, rhs1.T).T                    # local.py:72-78
-            for k in range(n1):
-                lam_bc[bnd_e, bnd_s * n1 + k] = proj[:, k]
-            Tcls = self.classes.T[self.elem_class[np.unique(bnd_e)]]
-            ub = np.unique(bnd_e)
-            load[ub] -= np.einsum("eij,ej->ei", Tcls, lam_bc[ub])
-        if self.classes.n == 1:
-            cl = load @ self.classes.Z[0].T
-        else:
-            cl = np.einsum("eij,ej->ei", self.classes.Z[self.elem_class], load)
+            if np.any(g):
+                rhs1 = (g * ref.quad.weights[None, :]) @ ref.interp_1d
+                proj = np.linalg.solve(ref.mass1, rhs1.T).T                # local.py:72-78
+                ub, inv = np.unique(bnd_e, return_inverse=True)
+                lam_bc = np.zeros((ub.size, 4 * n1))
+                for k in range(n1):
+                    lam_bc[inv, bnd_s * n1 + k] = proj[:, k]
+                load_bc = -np.einsum("eij,ej->ei", self._trace_cols(ub), lam_bc)
+                cl[ub] += self._condense_loads(ub, load_bc)
         return self.layout.sum_owners(cl)
 
     # -- reference attributes -----------------------------------------------------------------

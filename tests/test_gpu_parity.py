@@ -283,3 +283,39 @@ def test_aggressive_fsai_converges_fast(P):
     lo = O.build_levels(O.Grid(8, 8), 3, specs.manufactured(O.Spec), smoother="aggressive")
     _, mo = O.solve_mg(lo, tol=1e-13)
     assert len(mon.residuals) == len(mo.residuals)
+
+
+# ------------------------------------------------------- GPU batched condensation (8f #1)
+
+
+@pytest.mark.parametrize("n,p", [(16, 2), (12, 4), (8, 8)])
+def test_gpu_condensation_matches_oracle(P, n, p, monkeypatch):
+    """Heterogeneous piecewise-constant K condensed on the device (flux eliminated first,
+    nb x nb solves) against the oracle's full local LU (local.py:204-237)."""
+    monkeypatch.setattr(P.tr.TraceSystem, "GPU_CLASSES", 0)
+    Kg = specs.hetero_K(n, seed=11)
+    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.bump_f, specs.bump_u, 1.0)
+    s = P.tr.TraceSystem(P.mesh(n, n), p, spec)
+    assert s.piecewise is not None
+    o = O.OracleTrace(O.Grid(n, n), p, O.Spec(O.piecewise_coefficient(Kg), specs.bump_f, specs.bump_u, 1.0))
+    assert rel(s.schur, o.schur) < 1e-11
+    assert rel(s.rhs, o.rhs) < 1e-11
+    x = np.random.default_rng(2).uniform(-1, 1, s.ndof)
+    assert rel(s.matvec_free(x), o.matvec(x)) < 1e-11
+
+
+def test_gpu_condensed_hierarchy_solve(P, monkeypatch):
+    """MG-PCG on a GPU-condensed heterogeneous hierarchy equals the oracle's iteration count."""
+    monkeypatch.setattr(P.tr.TraceSystem, "GPU_CLASSES", 0)
+    g = golden_het = None
+    n, p = 16, 2
+    Kg = specs.hetero_K(n, seed=2)
+    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+    levels = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother="blockjacobi")
+    lo = O.build_levels(O.Grid(n, n), p, O.Spec(O.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0),
+                        smoother="blockjacobi")
+    b = np.random.default_rng(9).uniform(-1, 1, levels[0].ndof)
+    x, it = levels[0].system.solve_cg(tol=1e-10, precond=P.mg.mg_preconditioner(levels), b=b)
+    xo, ito = lo[0].system.solve_cg(b=b, tol=1e-10, precond=O.mg_preconditioner(lo))
+    assert it == ito
+    assert rel(x, xo) < 1e-9
