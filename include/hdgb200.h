@@ -63,6 +63,14 @@ int64_t hdg_level_operator_bytes(const hdg_level* lev);
  * Computed and inverted in-library from the level's own blocks. */
 int hdg_level_set_blockjacobi(hdg_level* lev, double omega);
 
+/* Chebyshev-weighted block-Jacobi: step k of m uses weight 1/theta_k, theta_k the Chebyshev
+ * nodes of [lo, hi] (an interval of D^-1 A's spectrum; same rule as the reference FSAI sweep
+ * weights, multigrid.py:76-81).  Needs hdg_level_set_blockjacobi first. */
+int hdg_level_set_bj_chebyshev(hdg_level* lev, double lo, double hi);
+/* `steps` (weighted) Jacobi sweeps in place; work: ndof scratch */
+int hdg_bj_sweeps(const hdg_level* lev, const double* b, double* x, double* work, int steps,
+                  void* stream);
+
 /* y = A x  (trace.py:87-94) */
 int hdg_matvec(const hdg_level* lev, const double* x, double* y, void* stream);
 /* r = b - A x; if norm2_out != NULL also writes ||b - A x||^2 (one double, device) */

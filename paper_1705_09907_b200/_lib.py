@@ -31,6 +31,8 @@ SIGNATURES = [
     ("hdg_matvec", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     ("hdg_residual", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("hdg_bj_sweep", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("hdg_level_set_bj_chebyshev", c_int, [c_void_p, ctypes.c_double, ctypes.c_double]),
+    ("hdg_bj_sweeps", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     ("hdg_level_set_fsai", c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                                    c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_double]),
     ("hdg_fsai_apply", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),

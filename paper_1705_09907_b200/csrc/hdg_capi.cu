@@ -47,6 +47,10 @@ struct hdg_level {
   double *dDh = nullptr, *dDv = nullptr;
   bool has_bj = false;
   double omega = 0.8;
+  // Chebyshev-weighted block-Jacobi steps on [cheb_lo, cheb_hi] of D^-1 A (robust smoother
+  // for high-contrast K; same weighting rule as the reference FSAI sweeps, multigrid.py:76-81)
+  bool bj_cheb = false;
+  double bj_lo = 0.0, bj_hi = 1.0;
   double* partials = nullptr;                        // per-CTA norm partials
   int npart = 0;
   long long op_bytes = 0;
@@ -113,7 +117,7 @@ static constexpr int kThreads = HDG_WS ? NT + 32 : NT;
 
 template <int N1, bool STORED, int EPI>
 static int set_attr() {
-  const size_t smem = Cfg<N1>::SMEM_DOUBLES * sizeof(double);
+  const size_t smem = Cfg<N1>::smem_doubles(STORED) * sizeof(double);
   CK(cudaFuncSetAttribute(kernel_ptr<N1, STORED, EPI>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   return 0;
 }
@@ -144,7 +148,7 @@ static int grid_for(const hdg_level* L) {
   using C = Cfg<N1>;
   static int occ = -1;
   if (occ < 0) {
-    const size_t smem = C::SMEM_DOUBLES * sizeof(double);
+    const size_t smem = C::smem_doubles(STORED) * sizeof(double);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel_ptr<N1, STORED, EPI>(), kThreads, smem) !=
             cudaSuccess || occ < 1)
       occ = 1;
@@ -158,7 +162,7 @@ static int grid_for(const hdg_level* L) {
 template <int N1, bool STORED, int EPI>
 static int apply_t(const hdg_level* L, MvArgs& a, cudaStream_t s) {
   using C = Cfg<N1>;
-  const size_t smem = C::SMEM_DOUBLES * sizeof(double);
+  const size_t smem = C::smem_doubles(STORED) * sizeof(double);
   const int grid = grid_for<N1, STORED, EPI>(L);
   SharedOp<(STORED ? 1 : N1)> op;
   if constexpr (!STORED) {
@@ -187,10 +191,10 @@ static int apply_t(const hdg_level* L, MvArgs& a, cudaStream_t s) {
     default: return fail(HDG_EINVAL, "order p must be in [1, 12]");   \
   }
 
-static int apply(const hdg_level* L, int epi, MvArgs& a, cudaStream_t s) {
+static int apply(const hdg_level* L, int epi, MvArgs& a, cudaStream_t s, double omega_override = 0.0) {
   a.nx = L->nx; a.ny = L->ny; a.nxp = L->nxp; a.nh = (int)L->nh;
   a.Wh = L->dWh; a.Wv = L->dWv; a.Dh = L->dDh; a.Dv = L->dDv;
-  a.omega = L->omega;
+  a.omega = omega_override != 0.0 ? omega_override : L->omega;
   if (L->ndof == 0) return 0;
 #define APPLY_CASE(N)                                                                 \
   {                                                                                   \
@@ -348,6 +352,7 @@ int hdg_level_set_blockjacobi(hdg_level* L, double omega) {
   }
   L->has_bj = true;
   L->use_fsai = false;
+  L->bj_cheb = false;
   return 0;
 }
 
@@ -386,13 +391,47 @@ int hdg_residual(const hdg_level* L, const double* b, const double* x, double* r
   return finish_norm(L, norm2_out, S(stream));
 }
 
-int hdg_bj_sweep(const hdg_level* L, const double* b, const double* x_in, double* x_out, void* stream) {
+static int bj_sweep_w(const hdg_level* L, const double* b, const double* x_in, double* x_out, double w,
+                      cudaStream_t s) {
   if (!L) return fail(HDG_EINVAL, "null level");
   if (!L->has_bj) return fail(HDG_ESTATE, "block-Jacobi state not set (hdg_level_set_blockjacobi)");
   if (x_in == x_out && L->ndof > 0) return fail(HDG_EINVAL, "Jacobi sweep needs x_out != x_in");
   MvArgs a{};
   a.x = x_in; a.b = b; a.out = x_out;
-  return apply(L, EPI_BJ, a, S(stream));
+  return apply(L, EPI_BJ, a, s, w);
+}
+
+int hdg_bj_sweep(const hdg_level* L, const double* b, const double* x_in, double* x_out, void* stream) {
+  return bj_sweep_w(L, b, x_in, x_out, 0.0, S(stream));
+}
+
+// weight of Jacobi step k (1-based) of `steps`: omega, or 1/theta_k (Chebyshev nodes)
+static double bj_weight(const hdg_level* L, int k, int steps) {
+  if (!L->bj_cheb) return L->omega;
+  const double mid = 0.5 * (L->bj_hi + L->bj_lo), half = 0.5 * (L->bj_hi - L->bj_lo);
+  return 1.0 / (mid + half * std::cos(M_PI * (2.0 * k - 1.0) / (2.0 * steps)));
+}
+
+int hdg_level_set_bj_chebyshev(hdg_level* L, double lo, double hi) {
+  if (!L) return fail(HDG_EINVAL, "null level");
+  if (!L->has_bj) return fail(HDG_ESTATE, "set block-Jacobi first");
+  if (!(hi > lo && lo > 0.0)) return fail(HDG_EINVAL, "need 0 < lo < hi");
+  L->bj_cheb = true; L->bj_lo = lo; L->bj_hi = hi;
+  return 0;
+}
+
+int hdg_bj_sweeps(const hdg_level* L, const double* b, double* x, double* work, int steps, void* stream) {
+  // `steps` (Chebyshev-)weighted Jacobi sweeps in place (ping-pong through work)
+  double* cur = x;
+  double* oth = work;
+  int rc;
+  for (int k = 1; k <= steps; ++k) {
+    if ((rc = bj_sweep_w(L, b, cur, oth, bj_weight(L, k, steps), S(stream)))) return rc;
+    std::swap(cur, oth);
+  }
+  if (cur != x && L->ndof > 0)
+    CK(cudaMemcpyAsync(x, cur, sizeof(double) * L->ndof, cudaMemcpyDeviceToDevice, S(stream)));
+  return 0;
 }
 
 // -------------------------------------------------------------------------------- FSAI
@@ -677,7 +716,7 @@ static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1
     if ((rc = fsai_sweeps(L, b, cur, mg->R[k], oth, nu1, s))) return rc;
   } else {
     for (int it = 0; it < nu1; ++it) {
-      if ((rc = hdg_bj_sweep(L, b, cur, oth, s))) return rc;
+      if ((rc = bj_sweep_w(L, b, cur, oth, bj_weight(L, it + 1, nu1), s))) return rc;
       std::swap(cur, oth);
     }
   }
@@ -698,7 +737,7 @@ static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1
     if ((rc = fsai_sweeps(L, b, cur, mg->R[k], oth, nu2, s))) return rc;
   } else {
     for (int it = 0; it < nu2; ++it) {
-      if ((rc = hdg_bj_sweep(L, b, cur, oth, s))) return rc;
+      if ((rc = bj_sweep_w(L, b, cur, oth, bj_weight(L, it + 1, nu2), s))) return rc;
       std::swap(cur, oth);
     }
   }

@@ -77,10 +77,12 @@ template <int N1> struct Cfg {
   // output staging (reuses the consumed x buffer): h rows of TX facets, v columns of TY facets
   static constexpr int NOUT = N1;                                         // max outputs per facet
   static constexpr int YCS = (TY * NOUT) | 1;                             // odd column stride
-  static constexpr int BUF_Y = TY * TX * NOUT + TX * YCS;
+  static constexpr int BUF_Y = TX * YCS + TY * TX * NOUT;
   static constexpr int BUF = ((BUF_X > BUF_Y ? BUF_X : BUF_Y) + 1) & ~1;  // doubles per stage buffer
   static constexpr int NBUF = HDG_NBUF;
-  static constexpr int SMEM_DOUBLES = NBUF * BUF;
+  static constexpr int WSCR = 32 * NOUT;                                  // per-warp output transpose
+  // shared mode adds the per-warp transpose scratch; stored mode stages h outputs in BUF
+  static constexpr int smem_doubles(bool stored) { return NBUF * BUF + (stored ? 0 : (NWARP + 1) * WSCR); }
 };
 
 // Shared-mode operator: both merged facet matrices + block-Jacobi inverses, passed by value
@@ -406,9 +408,26 @@ __device__ __forceinline__ void facet_epilogue(const MvArgs& a, int blk, const d
 // element) and vertical facet v(i0+tx, j0+F w+f) (its left side); consecutive rows share
 // stencil blocks (the compiler CSEs the repeated shared-memory loads).  Outputs are staged through
 // shared memory (the consumed x buffer) and written back as contiguous runs.
+// h-facet outputs of one warp row (32 consecutive facets = one contiguous run in HBM):
+// transposed through the warp's private scratch and stored coalesced, right after compute
+template <int N1, int NO>
+__device__ __forceinline__ void store_h_row(const MvArgs& a, double* scr, int i0, int j, const double (&o)[N1],
+                                            int lane) {
+  if (a.out == nullptr || j < 1 || j > a.ny - 1) return;  // warp-uniform
+#pragma unroll
+  for (int k = 0; k < NO; ++k) scr[lane * NO + k] = o[k];
+  __syncwarp();
+  const int count = min(TX, a.nx - i0) * NO;
+  double* dst = a.out + hblk(a.nx, i0, j) * NO;
+#pragma unroll
+  for (int q = 0; q < NO; ++q)
+    if (lane + 32 * q < count) dst[lane + 32 * q] = scr[lane + 32 * q];
+  __syncwarp();
+}
+
 template <int N1, bool STORED, int EPI>
 __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(STORED ? 1 : N1)>& op,
-                                             double* buf, int i0, int j0, double& nrm) {
+                                             double* buf, double* scr, int i0, int j0, double& nrm) {
   using C = Cfg<N1>;
   constexpr int F = C::F;
   constexpr int NO = NOutOf<EPI, N1>::v;
@@ -420,7 +439,8 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
   const int hpar0 = h_run_start<N1>(a, i0, j0, 0), hstep = a.nx * N1;
   auto H = [&](int r, int c) { return Hs + r * C::RS + ((hpar0 + r * hstep) & 1) + c * C::S; };
   auto V = [&](int c, int r) { return Vs + (r * C::VCOLS + c) * C::SV; };
-  double oh[F][N1], ov[F][N1];
+  double ov[F][N1];
+  double ohs[STORED ? F : 1][N1];   // stored mode: h outputs wait for the CTA-staged write
   // ---- horizontal facets: owners (i, j-1) [TOP rows] and (i, j) [BOTTOM rows]
   {
     const double* nb[F][7];
@@ -436,8 +456,10 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
 #pragma unroll
       for (int f = 0; f < F; ++f) {
         const int j = j0 + F * w + f;
+        double oh[N1];
         if (i < a.nx && j >= 1 && j <= a.ny - 1)
-          facet_epilogue<N1, false, EPI>(a, hblk(a.nx, i, j), nb[f][1], op.Dh, nullptr, acc[f], oh[f], nrm);
+          facet_epilogue<N1, false, EPI>(a, hblk(a.nx, i, j), nb[f][1], op.Dh, nullptr, acc[f], oh, nrm);
+        store_h_row<N1, NO>(a, scr, i0, j, oh, tx);
       }
     } else {
 #pragma unroll
@@ -449,7 +471,7 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
           apply_stored<N1>(nb[f], a.Wh + (size_t)grp * C::WSZ * 32 + tx, acc);
           if (i < a.nx)
             facet_epilogue<N1, true, EPI>(a, hblk(a.nx, i, j), nb[f][1], nullptr,
-                                          a.Dh + (size_t)grp * C::DSZ * 32 + tx, acc, oh[f], nrm);
+                                          a.Dh + (size_t)grp * C::DSZ * 32 + tx, acc, ohs[f], nrm);
         }
       }
     }
@@ -489,15 +511,15 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
   }
   // ---- outputs -> shared (x buffer is consumed) -> contiguous global runs
   consumer_sync();
-  double* Yh = buf;                       // [row r][tx][NO]
-  double* Yv = buf + C::TY * TX * NO;     // [col tx][row r][NO], column stride YCS (odd)
+  double* Yv = buf;                       // [col tx][row r][NO], column stride YCS (odd)
+  double* Yh = buf + TX * C::YCS;         // stored mode: [row r][tx][NO]
 #pragma unroll
   for (int f = 0; f < F; ++f) {
     const int r = F * w + f;
 #pragma unroll
     for (int k = 0; k < NO; ++k) {
-      Yh[(r * TX + tx) * NO + k] = oh[f][k];
       Yv[tx * C::YCS + r * NO + k] = ov[f][k];
+      if constexpr (STORED) Yh[(r * TX + tx) * NO + k] = ohs[f][k];
     }
   }
   consumer_sync();
@@ -506,18 +528,20 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
   if (a.nx > 0) return;
 #endif
   const int lane = tx;
-  // h rows: facets h(i0 .. i0+TX-1, j) -> blocks (j-1)*nx + i, contiguous
-  const int hcount = min(TX, a.nx - i0) * NO;
+  if constexpr (STORED) {
+    // h rows: facets h(i0 .. i0+TX-1, j) -> blocks (j-1)*nx + i, contiguous
+    const int hcount = min(TX, a.nx - i0) * NO;
 #pragma unroll
-  for (int rr = 0; rr < C::TY / NWARP; ++rr) {
-    const int r = w + rr * NWARP;
-    const int j = j0 + r;
-    if (j >= 1 && j <= a.ny - 1) {
-      double* dst = a.out + hblk(a.nx, i0, j) * NO + lane;
-      const double* src = Yh + r * TX * NO + lane;
+    for (int rr = 0; rr < C::TY / NWARP; ++rr) {
+      const int r = w + rr * NWARP;
+      const int j = j0 + r;
+      if (j >= 1 && j <= a.ny - 1) {
+        double* dst = a.out + hblk(a.nx, i0, j) * NO + lane;
+        const double* src = Yh + r * TX * NO + lane;
 #pragma unroll
-      for (int q = 0; q < (TX * NO + 31) / 32; ++q)
-        if (lane + 32 * q < hcount) dst[32 * q] = src[32 * q];
+        for (int q = 0; q < (TX * NO + 31) / 32; ++q)
+          if (lane + 32 * q < hcount) dst[32 * q] = src[32 * q];
+      }
     }
   }
   // v columns: facets v(i, j0 .. j0+TY-1) -> blocks nh + (i-1)*ny + j, contiguous
@@ -539,7 +563,7 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
 // Persistent, double-buffered: CTA c walks tiles c, c + grid, ...; the next tile's stencil
 // values stream into the other shared buffer (cp.async group) while this tile computes.
 template <int N1, bool STORED, int EPI>
-__global__ void __launch_bounds__(NT, STORED ? 2 : HDG_MINB)
+__global__ void __launch_bounds__(NT, STORED ? 2 : (N1 <= 9 ? HDG_MINB : 1))
 trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 : N1)> op) {
   using C = Cfg<N1>;
   extern __shared__ __align__(16) double smem[];
@@ -570,7 +594,8 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
     }
     mbar_wait(&bars[slot], phase);
     __syncthreads();
-    compute_tile<N1, STORED, EPI>(a, op, smem + slot * C::BUF, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
+    compute_tile<N1, STORED, EPI>(a, op, smem + slot * C::BUF, smem + NB * C::BUF + (threadIdx.x >> 5) * C::WSCR,
+                                  (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
     __syncthreads();
     if (++slot == NB) { slot = 0; phase ^= 1u; }
   }
@@ -645,7 +670,8 @@ trace_apply_ws_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ?
   double nrm = 0.0;             // ---- compute warps
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     mbar_wait(&full[slot], phase);
-    compute_tile<N1, STORED, EPI>(a, op, smem + slot * C::BUF, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
+    compute_tile<N1, STORED, EPI>(a, op, smem + slot * C::BUF, smem + NB * C::BUF + (threadIdx.x >> 5) * C::WSCR,
+                                  (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
     consumer_sync();
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[slot])) : "memory");
     if (++slot == NB) { slot = 0; phase ^= 1u; }

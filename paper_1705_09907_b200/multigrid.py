@@ -29,6 +29,13 @@ class HierarchyError(ValueError):
     """multigrid.py:30."""
 
 
+# device-condensed levels above this size drop their element blocks after the hierarchy build
+RELEASE_NDOF = 4_000_000
+# Chebyshev block-Jacobi ("bj-chebyshev") interval on the spectrum of D^-1 A
+CHEB_BJ_LOWER = 0.15
+CHEB_BJ_SAFETY = 1.05
+
+
 # ------------------------------------------------------------------------- operators
 
 
@@ -139,6 +146,7 @@ class BlockJacobiSmoother:
         self.block_op = block_op
         self.omega = float(omega)
         self.aggressiveness = 0
+        self.lam_max = None
         block_op.set_blockjacobi(self.omega)
         lay = block_op.layout
         n1 = lay.n1
@@ -151,14 +159,36 @@ class BlockJacobiSmoother:
         if steps < 1:
             return x
         bd, was_np = dev.to_device(b)
-        xd, _ = dev.to_device(x)
-        cur = xd.clone()
-        oth = dev.empty(cur.numel())
-        s = dev.stream()
-        for _ in range(steps):
-            check(lib.hdg_bj_sweep(self.block_op.handle, dev.ptr(bd), dev.ptr(cur), dev.ptr(oth), s))
-            cur, oth = oth, cur
-        return dev.back(cur, was_np)
+        xd = dev.to_device(x)[0].clone()
+        work = dev.empty(xd.numel())
+        check(lib.hdg_bj_sweeps(self.block_op.handle, dev.ptr(bd), dev.ptr(xd), dev.ptr(work), int(steps),
+                                dev.stream()))
+        return dev.back(xd, was_np)
+
+    def sweep_weights(self, steps):
+        if self.lam_max is None:
+            return np.full(steps, self.omega)
+        lo, hi = self.cheb_lo, self.cheb_hi
+        k = np.arange(1, steps + 1)
+        return 1.0 / (0.5 * (hi + lo) + 0.5 * (hi - lo) * np.cos(np.pi * (2 * k - 1) / (2 * steps)))
+
+    def enable_chebyshev(self, frac=CHEB_BJ_LOWER, safety=CHEB_BJ_SAFETY, iters=20, seed=1234):
+        """Chebyshev weights on [frac lam, safety lam], lam = lambda_max(D^-1 A) from a 20-step
+        power iteration with seed 1234 (the reference FSAI estimate, multigrid.py:162-173)."""
+        n = self.block_op.ndof
+        v = dev.to_device(np.random.default_rng(seed).standard_normal(n))[0]
+        lam = 1.0
+        for _ in range(iters):
+            w = self.apply_inverse(self.block_op.apply(v))
+            lam = float(w.norm())
+            if lam == 0.0:
+                lam = 1.0
+                break
+            v = w / lam
+        self.lam_max = lam
+        self.cheb_lo, self.cheb_hi = frac * lam, safety * lam
+        check(lib.hdg_level_set_bj_chebyshev(self.block_op.handle, self.cheb_lo, self.cheb_hi))
+        return self
 
     def apply_inverse(self, r):
         """D^-1 r via one sweep from zero: omega D^-1 r, rescaled."""
@@ -301,12 +331,19 @@ def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother
     levels = [MGLevel(mesh, p, fine, kind="p-level", operator=DeviceOperator(fine.operator),
                       matrix_free=True, rhs=fine.rhs)]
     op = fine.operator
+
+    def retire(prev):
+        # large device-condensed levels: keep only the native facet stream (memory)
+        if not isinstance(prev.S_cls, np.ndarray) and prev.ndof > RELEASE_NDOF:
+            prev.release_blocks()
+
     for q in range(p - 1, 0, -1):                                   # multigrid.py:317-321
         V = p_transfer_matrix(q + 1)
         cop = BlockOperator(mesh, q, galerkin_p(op.S_cls, V), op.elem_class)
         levels[-1].prolong = Prolongation(op, cop, "p", V=V)
         levels.append(MGLevel(mesh, q, _LevelSystem(mesh, q, cop), kind="p-level",
                               operator=DeviceOperator(cop), matrix_free=False))
+        retire(op)
         op = cop
     m = mesh
     while m.n_x % 2 == 0 and m.n_y % 2 == 0 and m.n_x >= 4 and m.n_y >= 4:   # :322-327
@@ -316,6 +353,7 @@ def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother
         levels[-1].prolong = Prolongation(op, cop, "h", halves=halves, cross=cross)
         levels.append(MGLevel(m, 1, _LevelSystem(m, 1, cop), kind="h-level",
                               operator=DeviceOperator(cop), matrix_free=False))
+        retire(op)
         op = cop
     levels[-1].kind = "coarsest"
     if levels[-1].ndof > coarse_cap:                                  # :336-339
@@ -353,6 +391,10 @@ def attach_smoothers(levels, mode, omega=None):
         w = 0.8 if omega is None else float(omega)
         for lev in levels[:-1]:
             lev.smoother = BlockJacobiSmoother(lev.block_op, w)
+        return levels
+    if mode in ("bj-chebyshev", "chebyshev"):
+        for lev in levels[:-1]:
+            lev.smoother = BlockJacobiSmoother(lev.block_op, 1.0).enable_chebyshev()
         return levels
     power = {"baseline": 1, "aggressive": 2}.get(mode, mode)
     if not isinstance(power, int) or isinstance(power, bool) or power < 1:

@@ -117,10 +117,13 @@ class BlockOperator:
             else:
                 import torch
                 S = self.S_cls if isinstance(self.S_cls, torch.Tensor) else torch.from_numpy(self.S_cls).cuda()
-                idx = torch.from_numpy(self.elem_class).cuda()
-                blocks = S.index_select(0, idx).contiguous()
+                E = self.elem_class.size
+                if S.shape[0] == E and np.array_equal(self.elem_class, np.arange(E)):
+                    blocks = S.contiguous()          # identity classes: no gather copy
+                else:
+                    blocks = S.index_select(0, torch.from_numpy(self.elem_class).cuda()).contiguous()
                 check(lib.hdg_level_create_stored(nx, ny, self.p, blocks.data_ptr(), ctypes.byref(h)))
-                del blocks, S, idx
+                del blocks, S
             self._handle = h
         return self._handle
 
@@ -155,7 +158,17 @@ class BlockOperator:
         return float(out.item()) ** 0.5
 
     # -- host views (tests, tooling, coarse inverse) -------------------------------------
+    def release_blocks(self):
+        """Drop the element-class blocks once the native level holds its facet stream and the
+        next coarser level has been formed (large heterogeneous hierarchies)."""
+        _ = self.handle
+        self.S_cls = None
+        import torch
+        torch.cuda.empty_cache()   # the native library allocates with cudaMalloc, not torch
+
     def host_classes(self):
+        if self.S_cls is None:
+            raise RuntimeError("element blocks were released after building the hierarchy")
         S = self.S_cls
         return S if isinstance(S, np.ndarray) else S.cpu().numpy()
 
@@ -208,11 +221,13 @@ class TraceSystem:
             # element-wise constant K, uniform tau: classes by K value
             uk, inv = np.unique(Ke, return_inverse=True)
             if uk.size > self.GPU_CLASSES:
+                # many distinct elements: condense every element on the GPU, in element order
+                # (identity classes => the stored-block relayout reads S without a gather)
                 self.piecewise = PiecewiseCondenser(p, mesh.dx, mesh.dy, float(tau[0, 0]))
                 self.classes = None
-                self.elem_class = inv.reshape(-1)
-                self.class_K = uk
-                self.operator = BlockOperator(mesh, p, self.piecewise.blocks(uk), self.elem_class)
+                self.elem_class = np.arange(E, dtype=np.int64)
+                self.class_K = Ke
+                self.operator = BlockOperator(mesh, p, self.piecewise.blocks(Ke), self.elem_class)
                 self.rhs = self._condensed_rhs(spec)
                 return
             nq2 = self.ops.ref.quad.nodes.size ** 2

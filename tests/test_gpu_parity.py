@@ -319,3 +319,22 @@ def test_gpu_condensed_hierarchy_solve(P, monkeypatch):
     xo, ito = lo[0].system.solve_cg(b=b, tol=1e-10, precond=O.mg_preconditioner(lo))
     assert it == ito
     assert rel(x, xo) < 1e-9
+
+
+def test_chebyshev_blockjacobi_matches_oracle(P):
+    """Chebyshev-weighted block-Jacobi (robust smoother for high-contrast K): lambda_max, one
+    V-cycle and the MG-PCG iteration count agree with the oracle restatement."""
+    n, p = 16, 2
+    Kg = specs.hetero_K(n, seed=4)
+    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+    levels = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother="bj-chebyshev")
+    lo = O.build_levels(O.Grid(n, n), p, O.Spec(O.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0),
+                        smoother="bj-chebyshev")
+    for lev, ol in zip(levels[:-1], lo[:-1]):
+        assert abs(lev.smoother.lam_max - ol.smoother.lam_max) < 1e-10 * ol.smoother.lam_max
+    b = np.random.default_rng(6).uniform(-1, 1, levels[0].ndof)
+    assert rel(P.mg.v_cycle(levels, b), O.v_cycle(lo, b)) < TOL
+    x, it = levels[0].system.solve_cg(tol=1e-10, precond=P.mg.mg_preconditioner(levels), b=b)
+    xo, ito = lo[0].system.solve_cg(b=b, tol=1e-10, precond=O.mg_preconditioner(lo))
+    assert it == ito and it < 100
+    assert rel(x, xo) < 1e-9

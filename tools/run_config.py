@@ -1,0 +1,77 @@
+"""BASELINE configs[2] (and scaled variants): heterogeneous piecewise-constant isotropic K,
+log-uniform in [1e-2, 1e2] (seed 2), fp64; MG-preconditioned CG to relative
+residual 1e-10 with b ~ U[-1, 1] (same generator, after K).  Prints one JSON line.
+
+    python tools/run_config.py --n 2048 --p 8        # full configs[2]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_1705_09907_b200 import _lib
+from paper_1705_09907_b200.mesh import build_cartesian
+from paper_1705_09907_b200.multigrid import _native_mg, attach_smoothers, build_hierarchy
+from paper_1705_09907_b200.problem import ProblemSpec, piecewise_coefficient
+
+
+def zero(x, y):
+    return np.zeros_like(np.asarray(x, float))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=2048)
+    ap.add_argument("--p", type=int, default=8)
+    ap.add_argument("--tol", type=float, default=1e-10)
+    ap.add_argument("--maxiter", type=int, default=500)
+    ap.add_argument("--smoother", default="blockjacobi")
+    a = ap.parse_args()
+    rng = np.random.default_rng(2)
+    Kg = np.exp(rng.uniform(np.log(1e-2), np.log(1e2), (a.n, a.n)))
+    spec = ProblemSpec(piecewise_coefficient(Kg), zero, zero, 1.0)
+    t0 = time.time()
+    levels = build_hierarchy(build_cartesian(a.n, a.n), a.p, spec, smoother=None)
+    attach_smoothers(levels, a.smoother)
+    mg = _native_mg(levels)
+    torch.cuda.synchronize()
+    t_setup = time.time() - t0
+    ndof = levels[0].ndof
+    b = torch.from_numpy(rng.uniform(-1.0, 1.0, ndof)).cuda()
+    free, total = torch.cuda.mem_get_info()
+    # V-cycle time (graph replay)
+    x = torch.zeros_like(b)
+    st = torch.cuda.current_stream()
+    for _ in range(2):
+        _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), 0, x.data_ptr(), 2, 2, 1, 1, st.cuda_stream))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    R = 5
+    e0.record(st)
+    for _ in range(R):
+        _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), 0, x.data_ptr(), 2, 2, 1, 1, st.cuda_stream))
+    e1.record(st)
+    torch.cuda.synchronize()
+    vms = e0.elapsed_time(e1) / R
+    # MG-PCG solve (trace.py:142-163 with mg_preconditioner, multigrid.py:457-463)
+    from paper_1705_09907_b200.multigrid import mg_preconditioner
+    torch.cuda.synchronize()
+    t1 = time.time()
+    xs, iters = levels[0].system.solve_cg(tol=a.tol, maxiter=a.maxiter, precond=mg_preconditioner(levels), b=b)
+    torch.cuda.synchronize()
+    t_solve = time.time() - t1
+    r = b - levels[0].matvec(xs)
+    relres = float(torch.linalg.vector_norm(r) / torch.linalg.vector_norm(b))
+    print(json.dumps({"config": f"{a.n}^2 p={a.p} heterogeneous K log-U[1e-2,1e2] seed 2, MG-PCG ({a.smoother} V(2,2))",
+                      "ndof": ndof, "levels": len(levels), "setup_s": round(t_setup, 2),
+                      "vcycle_ms": round(vms, 3), "pcg_iterations": iters, "solve_s": round(t_solve, 3),
+                      "final_rel_residual": relres, "gpu_mem_used_GB": round((total - free) / 1e9, 1)}))
+
+
+if __name__ == "__main__":
+    main()
