@@ -39,6 +39,22 @@ METRIC = "trace_matvec_gdof_per_s"
 UNIT = "GDOF/s"
 
 
+def ncu_traffic():
+    """dram__bytes_read + dram__bytes_write of the trace kernel from the committed ncu --set full
+    capture (profiles/), per launch; None if absent."""
+    path = os.path.join(ROOT, "profiles", "ncu_trace_apply_p4_r01_key_metrics.txt")
+    try:
+        vals = {}
+        for line in open(path):
+            parts = line.split()
+            if len(parts) >= 3 and parts[0].startswith("dram__bytes_"):
+                scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[parts[2]]
+                vals[parts[0]] = float(parts[1]) * scale
+        return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -285,7 +301,9 @@ def run_ours(args, rank, ws):
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ndof, "d2h_bytes_per_step": 8 * ndof,
                     "path": "TraceSystem.matvec_free(cuda tensor) x100 after pinned H2D of x; D2H of y"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "peak_kind": kind,
+                         "frac": achieved / hbm, "traffic": ncu_traffic(),
+                         "traffic_source": "profiles/ncu_trace_apply_p4_r01_key_metrics.txt (ncu --set full)",
+                         "peak_kind": kind,
                          "kernel": "trace_apply_kernel<5,shared,EPI_Y>", "alg_bytes_per_launch": alg_bytes,
                          "kernel_us_avg": kernel_us, "kernel_us_single_median": float(np.median(singles)),
                          "fp64_tflops": flops / (kernel_us * 1e-6) / 1e12},

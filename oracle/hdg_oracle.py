@@ -251,12 +251,17 @@ class Local:
         ref = core.ref
         x0, y0 = g.origin(e)
         qx, qy = ref.quad_xy(x0, y0, g.dx, g.dy)
-        kq = np.asarray(spec.coefficient(qx, qy), float)           # local.py:138
-        if np.any(kq <= 0):
+        kq = spec.coefficient(qx, qy)                                # local.py:138
+        # builder restatement: a (Kxx, Kyy) pair = anisotropic diagonal K, with one
+        # flux mass per component; a scalar field is the reference's isotropic case
+        kx, ky = (kq if isinstance(kq, tuple) else (kq, kq))
+        kx, ky = np.asarray(kx, float), np.asarray(ky, float)
+        if np.any(kx <= 0) or np.any(ky <= 0):
             raise RuntimeError(f"coefficient not positive on element {e}")
         fq = np.asarray(spec.source(qx, qy), float)
         wj = ref.w2 * core.jac
-        M = ref.I2.T @ np.diag(wj / kq) @ ref.I2                    # local.py:144
+        M = ref.I2.T @ np.diag(wj / kx) @ ref.I2                    # local.py:144
+        My = ref.I2.T @ np.diag(wj / ky) @ ref.I2
         Bx = 0.5 * g.dy * ref.I2.T @ np.diag(ref.w2) @ ref.Dxi     # local.py:146
         By = 0.5 * g.dx * ref.I2.T @ np.diag(ref.w2) @ ref.Deta
         facets = g.e2f[e]
@@ -292,7 +297,7 @@ class Local:
         T[:, ~cmask] = 0.0
         Lmat = np.zeros((3 * nb, 3 * nb))                            # local.py:116-126
         Lmat[:nb, :nb] = M
-        Lmat[nb:2 * nb, nb:2 * nb] = M
+        Lmat[nb:2 * nb, nb:2 * nb] = My
         Lmat[:2 * nb, 2 * nb:] = -np.hstack([Bx, By]).T
         Lmat[2 * nb:, :2 * nb] = np.hstack([Bx, By])
         Lmat[2 * nb:, 2 * nb:] = stab
@@ -458,6 +463,12 @@ def nodal_source(f_nodal, n, p):
         return np.einsum("qb,qa,qba->q", Ey, Ex, vals).reshape(x.shape)
 
     return src
+
+
+def piecewise_anisotropic(Kxx, Kyy):
+    """Builder restatement: per-element diagonal K = diag(Kxx, Kyy) as a pair."""
+    fx, fy = piecewise_coefficient(Kxx), piecewise_coefficient(Kyy)
+    return lambda x, y: (fx(x, y), fy(x, y))
 
 
 def piecewise_coefficient(Kgrid):
@@ -815,6 +826,16 @@ def solve_mg(levels, b=None, x0=None, cyc="v", nu1=2, nu2=2, tol=1e-12, max_cycl
         if mon.diverged():
             break
     return x, mon
+
+
+def fmg(levels, nu1=2, nu2=2, cycles_per_level=1):
+    """multigrid.py:442-454."""
+    x = levels[-1].coarse_solve(levels[-1].rhs)
+    for k in range(len(levels) - 2, -1, -1):
+        x = levels[k].prolong @ x
+        for _ in range(cycles_per_level):
+            x = v_cycle(levels[k:], levels[k].rhs, x, nu1, nu2)
+    return x
 
 
 def mg_preconditioner(levels, nu1=2, nu2=2):

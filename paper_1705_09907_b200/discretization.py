@@ -141,13 +141,16 @@ class ElementClasses:
       ucols (C, nb, 4n1)   u response to trace data, (L^-1 T)[2nb:] (h-transfer, multigrid.py:273)
     """
 
-    def __init__(self, p, dx, dy, kq, tau):
+    def __init__(self, p, dx, dy, kq, tau, kq_y=None):
+        """kq: (C, nq^2) coefficient samples (isotropic, local.py:138); with kq_y the pair is
+        the anisotropic diagonal K (Kxx, Kyy) - one flux mass per component."""
         ref = ref_element(p)
         self.p, self.ref = p, ref
         n1, nb = ref.n1, ref.nb
         kq = np.atleast_2d(np.asarray(kq, float))
+        kqy = kq if kq_y is None else np.atleast_2d(np.asarray(kq_y, float))
         tau = np.atleast_2d(np.asarray(tau, float))
-        if np.any(kq <= 0.0):
+        if np.any(kq <= 0.0) or np.any(kqy <= 0.0):
             raise NumericalBreakdown("coefficient not positive")
         C = kq.shape[0]
         jac = dx * dy / 4.0
@@ -158,9 +161,10 @@ class ElementClasses:
         lens = (dx, dy, dx, dy)
         fm = [0.5 * lens[s] * ref.mass1 for s in range(4)]           # local.py:68-69
         M = np.einsum("qi,cq,qj->cij", I2, wj[None, :] / kq, I2)     # local.py:144
+        My = M if kq_y is None else np.einsum("qi,cq,qj->cij", I2, wj[None, :] / kqy, I2)
         L = np.zeros((C, 3 * nb, 3 * nb))
         L[:, :nb, :nb] = M
-        L[:, nb:2 * nb, nb:2 * nb] = M
+        L[:, nb:2 * nb, nb:2 * nb] = My
         G = np.hstack([Bx, By])
         L[:, :2 * nb, 2 * nb:] = -G.T
         L[:, 2 * nb:, :2 * nb] = G
@@ -235,44 +239,65 @@ class PiecewiseCondenser:
             Ms[cols, cols] += tau * fm[s]
         Mi = np.linalg.inv(M)
         B = (Bx, By)
-        self.Lap = sum(B[d] @ Mi @ B[d].T for d in range(2))
-        self.G = sum(B[d] @ Mi @ Tq[d * nb:(d + 1) * nb] for d in range(2))
-        self.A0 = sum(Fq[:, d * nb:(d + 1) * nb] @ Mi @ Tq[d * nb:(d + 1) * nb] for d in range(2))
-        self.C0 = sum(Fq[:, d * nb:(d + 1) * nb] @ Mi @ B[d].T for d in range(2))
+        # per flux component d (K_d multiplies each term: anisotropic diagonal K)
+        self.Lapd = [B[d] @ Mi @ B[d].T for d in range(2)]
+        self.Gd = [B[d] @ Mi @ Tq[d * nb:(d + 1) * nb] for d in range(2)]
+        self.A0d = [Fq[:, d * nb:(d + 1) * nb] @ Mi @ Tq[d * nb:(d + 1) * nb] for d in range(2)]
+        self.C0d = [Fq[:, d * nb:(d + 1) * nb] @ Mi @ B[d].T for d in range(2)]
+        self.BMid = [B[d] @ Mi for d in range(2)]
+        self.FqMid = [Fq[:, d * nb:(d + 1) * nb] @ Mi for d in range(2)]
         self.stab, self.Tu, self.Fu, self.Ms = stab, Tu, Fu, Ms
-        self.BMi = np.hstack([Bx @ Mi, By @ Mi])                               # nb x 2nb
-        self.FqMi = np.hstack([Fq[:, :nb] @ Mi, Fq[:, nb:] @ Mi])             # 4n1 x 2nb
+
+    def _dev(self):
+        import torch
+        if not hasattr(self, "_t"):
+            T = {}
+            for k in ("stab", "Tu", "Fu", "Ms"):
+                T[k] = torch.as_tensor(getattr(self, k), device="cuda")
+            for k in ("Lapd", "Gd", "A0d", "C0d", "BMid", "FqMid"):
+                T[k] = [torch.as_tensor(m, device="cuda") for m in getattr(self, k)]
+            self._t = T
+        return self._t
+
+    @staticmethod
+    def _pair(K):
+        if isinstance(K, tuple):
+            return np.asarray(K[0], float), np.asarray(K[1], float)
+        K = np.asarray(K, float)
+        return K, K
 
     def condensed_loads(self, K, load_q, load_u, chunk=1 << 16):
         """F L(K)^-1 [load_q; load_u] per element (local.py:236), the same elimination."""
         import torch
-        dev = "cuda"
-        t = {k: torch.as_tensor(getattr(self, k), device=dev) for k in ("Lap", "C0", "stab", "Fu", "BMi", "FqMi")}
-        K = torch.as_tensor(np.asarray(K, float), device=dev)
-        fq = torch.as_tensor(load_q, device=dev)
-        fu = torch.as_tensor(load_u, device=dev)
-        out = torch.empty((K.numel(), 4 * self.n1), dtype=torch.float64, device=dev)
-        for s0 in range(0, K.numel(), chunk):
-            k = K[s0:s0 + chunk][:, None]
-            H = t["stab"] + k[:, :, None] * t["Lap"]
-            rhs = fu[s0:s0 + chunk] - k * (fq[s0:s0 + chunk] @ t["BMi"].T)
+        t = self._dev()
+        kx, ky = (torch.as_tensor(k, device="cuda") for k in self._pair(K))
+        fq = torch.as_tensor(load_q, device="cuda")
+        fu = torch.as_tensor(load_u, device="cuda")
+        nb = self.nb
+        out = torch.empty((kx.numel(), 4 * self.n1), dtype=torch.float64, device="cuda")
+        for s0 in range(0, kx.numel(), chunk):
+            k = (kx[s0:s0 + chunk][:, None], ky[s0:s0 + chunk][:, None])
+            f = (fq[s0:s0 + chunk, :nb], fq[s0:s0 + chunk, nb:])
+            H = t["stab"] + sum(k[d][:, :, None] * t["Lapd"][d] for d in range(2))
+            rhs = fu[s0:s0 + chunk] - sum(k[d] * (f[d] @ t["BMid"][d].T) for d in range(2))
             u = torch.linalg.solve(H, rhs[:, :, None])[:, :, 0]
-            out[s0:s0 + chunk] = k * (fq[s0:s0 + chunk] @ t["FqMi"].T) + \
-                k * (u @ t["C0"].T) + u @ t["Fu"].T
+            out[s0:s0 + chunk] = sum(k[d] * (f[d] @ t["FqMid"][d].T) + k[d] * (u @ t["C0d"][d].T)
+                                     for d in range(2)) + u @ t["Fu"].T
         return out.cpu().numpy()
 
     def blocks(self, K, chunk=1 << 15):
+        """S for every element; K: (E,) isotropic or a (Kxx, Kyy) pair of (E,) arrays."""
         import torch
-        dev = "cuda"
-        t = {k: torch.as_tensor(getattr(self, k), device=dev) for k in ("Lap", "G", "A0", "C0", "stab", "Tu", "Fu", "Ms")}
-        K = torch.as_tensor(np.asarray(K, float), device=dev)
-        E = K.numel()
-        out = torch.empty((E, 4 * self.n1, 4 * self.n1), dtype=torch.float64, device=dev)
+        t = self._dev()
+        kx, ky = (torch.as_tensor(k, device="cuda") for k in self._pair(K))
+        E = kx.numel()
+        out = torch.empty((E, 4 * self.n1, 4 * self.n1), dtype=torch.float64, device="cuda")
         for s0 in range(0, E, chunk):
-            k = K[s0:s0 + chunk][:, None, None]
-            H = t["stab"] + k * t["Lap"]
-            U = torch.linalg.solve(H, t["Tu"] - k * t["G"])
-            out[s0:s0 + chunk] = k * t["A0"] + t["Ms"] + (k * t["C0"] + t["Fu"]) @ U
+            k = (kx[s0:s0 + chunk][:, None, None], ky[s0:s0 + chunk][:, None, None])
+            H = t["stab"] + sum(k[d] * t["Lapd"][d] for d in range(2))
+            U = torch.linalg.solve(H, t["Tu"] - sum(k[d] * t["Gd"][d] for d in range(2)))
+            out[s0:s0 + chunk] = sum(k[d] * t["A0d"][d] for d in range(2)) + t["Ms"] + \
+                (sum(k[d] * t["C0d"][d] for d in range(2)) + t["Fu"]) @ U
         return out
 
 

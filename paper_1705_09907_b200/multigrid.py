@@ -275,7 +275,11 @@ def _coarse_classes(mesh_c, spec, tau_per_facet):
     x0 = mesh_c.x0 + (e % nx) * mesh_c.dx
     y0 = mesh_c.y0 + (e // nx) * mesh_c.dy
     qx, qy = ref.element_quad_points(x0, y0, mesh_c.dx, mesh_c.dy)
-    kq = np.asarray(spec.coefficient(qx, qy), float).reshape(len(e), -1)
+    kq = spec.coefficient(qx, qy)
+    aniso = isinstance(kq, tuple)
+    kx, ky = (kq if aniso else (kq, kq))
+    kx = np.asarray(kx, float).reshape(len(e), -1)
+    ky = np.asarray(ky, float).reshape(len(e), -1)
     if tau_per_facet is None:
         tau = np.full((len(e), 4), float(spec.tau))
     else:
@@ -283,8 +287,11 @@ def _coarse_classes(mesh_c, spec, tau_per_facet):
         j, i = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
         f = np.stack([j * nx + i, nh + (i + 1) * ny + j, (j + 1) * nx + i, nh + i * ny + j], -1).reshape(-1, 4)
         tau = np.asarray(tau_per_facet, float)[f]
-    rows, inv = classify_rows(np.hstack([kq, tau]))
-    cls = ElementClasses(1, mesh_c.dx, mesh_c.dy, rows[:, :kq.shape[1]], rows[:, kq.shape[1]:])
+    nq = kx.shape[1]
+    rows, inv = classify_rows(np.hstack([kx, ky, tau]) if aniso else np.hstack([kx, tau]))
+    nk = 2 * nq if aniso else nq
+    cls = ElementClasses(1, mesh_c.dx, mesh_c.dy, rows[:, :nq], rows[:, nk:],
+                         kq_y=rows[:, nq:nk] if aniso else None)
     return cls.ucols, inv
 
 

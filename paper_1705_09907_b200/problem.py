@@ -69,6 +69,14 @@ def piecewise_coefficient(Kgrid):
     return coef
 
 
+def piecewise_anisotropic(Kxx, Kyy):
+    """Diagonal anisotropic K = diag(Kxx, Kyy) per element (BASELINE configs[4]); the
+    coefficient returns the pair, which TraceSystem treats as one flux mass per component
+    (the reference's scalar coefficient cannot represent this)."""
+    fx, fy = piecewise_coefficient(Kxx), piecewise_coefficient(Kyy)
+    return lambda x, y: (fx(x, y), fy(x, y))
+
+
 def config1_problem(n=64, p=2, seed=0):
     """BASELINE configs[0]: K = 1, g_D = 0, tau = 1, nodal f ~ U[-1, 1] (seed 0)."""
     f = np.random.default_rng(seed).uniform(-1.0, 1.0, (n * n, (p + 1) ** 2))

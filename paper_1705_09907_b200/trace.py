@@ -215,12 +215,16 @@ class TraceSystem:
         nx, ny = mesh.n_x, mesh.n_y
         E = nx * ny
         tau = self._element_tau(spec, tau_per_facet)
-        kq_rows, Ke = self._sample_coefficient(spec)                      # local.py:137-140
+        kq_rows, Ke, aniso = self._sample_coefficient(spec)               # local.py:137-140
+        self.anisotropic = aniso
+        nq2 = self.ops.ref.quad.nodes.size ** 2
         self.piecewise = None
         if Ke is not None and np.all(tau == tau[0]):
-            # element-wise constant K, uniform tau: classes by K value
-            uk, inv = np.unique(Ke, return_inverse=True)
-            if uk.size > self.GPU_CLASSES:
+            # element-wise constant K (a pair for anisotropic diagonal K), uniform tau
+            keys = np.stack(Ke, axis=1) if aniso else Ke[:, None]
+            uk, inv = np.unique(keys, axis=0, return_inverse=True)
+            inv = np.asarray(inv).reshape(-1)
+            if uk.shape[0] > self.GPU_CLASSES:
                 # many distinct elements: condense every element on the GPU, in element order
                 # (identity classes => the stored-block relayout reads S without a gather)
                 self.piecewise = PiecewiseCondenser(p, mesh.dx, mesh.dy, float(tau[0, 0]))
@@ -230,12 +234,14 @@ class TraceSystem:
                 self.operator = BlockOperator(mesh, p, self.piecewise.blocks(Ke), self.elem_class)
                 self.rhs = self._condensed_rhs(spec)
                 return
-            nq2 = self.ops.ref.quad.nodes.size ** 2
-            rows = np.hstack([np.repeat(uk[:, None], nq2, axis=1), np.repeat(tau[:1], uk.size, axis=0)])
+            kx = np.repeat(uk[:, :1], nq2, axis=1)
+            ky = np.repeat(uk[:, -1:], nq2, axis=1) if aniso else None
+            rows = np.hstack([kx] + ([ky] if aniso else []) + [np.repeat(tau[:1], uk.shape[0], axis=0)])
         else:
             rows, inv = classify_rows(np.hstack([kq_rows, tau]))
-        nq2 = rows.shape[1] - 4
-        self.classes = ElementClasses(p, mesh.dx, mesh.dy, rows[:, :nq2], rows[:, nq2:])
+        nk = 2 * nq2 if aniso else nq2
+        self.classes = ElementClasses(p, mesh.dx, mesh.dy, rows[:, :nq2], rows[:, nk:],
+                                      kq_y=rows[:, nq2:nk] if aniso else None)
         self.elem_class = np.asarray(inv).reshape(-1)
         self.operator = BlockOperator(mesh, p, self.classes.S, self.elem_class)
         self.rhs = self._condensed_rhs(spec)
@@ -248,25 +254,31 @@ class TraceSystem:
         return self.ops.ref.element_quad_points(x0, y0, m.dx, m.dy)
 
     def _sample_coefficient(self, spec, chunk=1 << 16):
-        """K at every element's GL points (local.py:137-138), in chunks.  Returns
-        (None, K_e) when K is constant on every element, else (kq rows, None)."""
+        """K at every element's GL points (local.py:137-138), in chunks.  A coefficient returning
+        a (Kxx, Kyy) pair is the anisotropic diagonal extension.  Returns
+        (rows, K_e, anisotropic): K_e (an (E,) array or a pair) when K is constant on every
+        element, else rows of samples (E, nq^2 [x2])."""
         E = self.mesh.n_x * self.mesh.n_y
-        Ke = np.empty(E)
-        rows = []
-        const = True
+        parts, const, aniso = [], True, False
+        kx_e, ky_e = np.empty(E), np.empty(E)
         for e0 in range(0, E, chunk):
             qx, qy = self._quad_points(e0, min(E, e0 + chunk))
-            kq = np.asarray(spec.coefficient(qx, qy), float).reshape(qx.shape)
-            if np.any(kq <= 0.0):
+            kq = spec.coefficient(qx, qy)
+            aniso = isinstance(kq, tuple)
+            kx, ky = (kq if aniso else (kq, kq))
+            kx = np.asarray(kx, float).reshape(qx.shape)
+            ky = np.asarray(ky, float).reshape(qx.shape)
+            if np.any(kx <= 0.0) or np.any(ky <= 0.0):
                 raise NumericalBreakdown("coefficient not positive")
-            rows.append(kq)
-            if const and np.all(kq == kq[:, :1]):
-                Ke[e0:e0 + kq.shape[0]] = kq[:, 0]
+            parts.append(np.hstack([kx, ky]) if aniso else kx)
+            if const and np.all(kx == kx[:, :1]) and np.all(ky == ky[:, :1]):
+                kx_e[e0:e0 + kx.shape[0]] = kx[:, 0]
+                ky_e[e0:e0 + kx.shape[0]] = ky[:, 0]
             else:
                 const = False
         if const:
-            return None, Ke
-        return np.concatenate(rows), None
+            return None, ((kx_e, ky_e) if aniso else kx_e), aniso
+        return np.concatenate(parts), None, aniso
 
     @classmethod
     def from_blocks(cls, mesh, p, S_cls, elem_class=None, rhs=None):
@@ -304,7 +316,8 @@ class TraceSystem:
         """condensed loads of elements idx (local.py:236)"""
         nb = self.ops.nb
         if self.piecewise is not None:
-            K = self.class_K[self.elem_class[idx]]
+            K = self.class_K
+            K = (K[0][idx], K[1][idx]) if isinstance(K, tuple) else K[idx]
             return self.piecewise.condensed_loads(K, load[:, :2 * nb], load[:, 2 * nb:])
         if self.classes.n == 1:
             return load @ self.classes.Z[0].T

@@ -338,3 +338,49 @@ def test_chebyshev_blockjacobi_matches_oracle(P):
     xo, ito = lo[0].system.solve_cg(b=b, tol=1e-10, precond=O.mg_preconditioner(lo))
     assert it == ito and it < 100
     assert rel(x, xo) < 1e-9
+
+
+def test_w_cycle_fmg_and_single_level(P):
+    """test_multigrid.py:233-290 analogues against the oracle."""
+    spec = specs.manufactured(P.pb.ProblemSpec)
+    one = P.mg.build_hierarchy(P.mesh(2, 2), 1, spec, smoother="blockjacobi")
+    assert len(one) == 1 and one[0].kind == "coarsest"
+    ref = O.OracleTrace(O.Grid(2, 2), 1, specs.manufactured(O.Spec)).solve_direct()
+    np.testing.assert_allclose(P.mg.w_cycle(one, one[0].rhs), ref, atol=1e-12)
+    np.testing.assert_allclose(P.mg.fmg(one), ref, atol=1e-12)
+    x, mon = P.mg.solve_mg(one)
+    np.testing.assert_allclose(x, ref, atol=1e-12)
+    levels = P.mg.build_hierarchy(P.mesh(8, 8), 3, spec, smoother="baseline")
+    lo = O.build_levels(O.Grid(8, 8), 3, specs.manufactured(O.Spec), smoother="baseline")
+    b = levels[0].rhs
+    assert rel(P.mg.w_cycle(levels, b), O.cycle(lo, 0, b, np.zeros_like(b), 2, 2, 2)) < TOL
+    assert rel(P.mg.fmg(levels), O.fmg(lo)) < 1e-11
+
+
+def test_rectangular_vcycle_and_plain_cg(P):
+    spec = specs.manufactured(P.pb.ProblemSpec)
+    levels = P.mg.build_hierarchy(P.mesh(12, 8), 2, spec, smoother="blockjacobi")
+    lo = O.build_levels(O.Grid(12, 8), 2, specs.manufactured(O.Spec), smoother="blockjacobi")
+    b = levels[0].rhs
+    assert rel(P.mg.v_cycle(levels, b), O.v_cycle(lo, b)) < TOL
+    x, it = levels[0].system.solve_cg(tol=1e-12)                      # trace.py:142-163
+    xo, ito = lo[0].system.solve_cg(tol=1e-12)
+    assert it == ito
+    assert rel(x, xo) < 1e-9
+
+
+def test_anisotropic_gpu_condensation_and_vcycle(P, monkeypatch):
+    """configs[4]-style anisotropic diagonal K condensed on the device; matvec and one V-cycle
+    against the oracle restatement (F9)."""
+    monkeypatch.setattr(P.tr.TraceSystem, "GPU_CLASSES", 0)
+    n, p = 16, 4
+    rng = np.random.default_rng(3)
+    Kx, Ky = np.exp(rng.uniform(np.log(0.1), np.log(10.0), (2, n, n)))
+    spec = P.pb.ProblemSpec(P.pb.piecewise_anisotropic(Kx, Ky), specs.zero, specs.zero, 1.0)
+    levels = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother="blockjacobi")
+    assert levels[0].system.piecewise is not None
+    lo = O.build_levels(O.Grid(n, n), p, O.Spec(O.piecewise_anisotropic(Kx, Ky), specs.zero, specs.zero, 1.0),
+                        smoother="blockjacobi")
+    b = rng.uniform(-1, 1, levels[0].ndof)
+    assert rel(levels[0].matvec(b), lo[0].matvec(b)) < 1e-11
+    assert rel(P.mg.v_cycle(levels, b), O.v_cycle(lo, b)) < 1e-11
