@@ -33,7 +33,7 @@
 namespace hdg {
 
 #ifndef HDG_NBUF
-#define HDG_NBUF 2         // stage buffers per CTA (2 = prefetch next tile while computing)
+#define HDG_NBUF 0         // stage buffers per CTA; 0 = per-order default (measured, see Cfg)
 #endif
 #ifndef HDG_F_MAXN1
 #define HDG_F_MAXN1 5      // two facets per thread per orientation up to this n1
@@ -43,6 +43,9 @@ namespace hdg {
 #endif
 #ifndef HDG_WS_MINB
 #define HDG_WS_MINB 2      // warp-specialized kernel: CTAs per SM the registers must allow
+#endif
+#ifndef HDG_DMMA
+#define HDG_DMMA 0         // shared mode: FP64 tensor-core (DMMA m8n8k4) stencil GEMM for n1 <= 8
 #endif
 #ifndef HDG_NWARP
 #define HDG_NWARP 8
@@ -79,8 +82,12 @@ template <int N1> struct Cfg {
   static constexpr int YCS = (TY * NOUT) | 1;                             // odd column stride
   static constexpr int BUF_Y = TX * YCS + TY * TX * NOUT;
   static constexpr int BUF = ((BUF_X > BUF_Y ? BUF_X : BUF_Y) + 1) & ~1;  // doubles per stage buffer
-  static constexpr int NBUF = HDG_NBUF;
-  static constexpr int WSCR = 32 * NOUT;                                  // per-warp output transpose
+  // measured on B200 (tools/tune_matvec.py): double buffering pays for p <= 2 (little compute
+  // per byte); for p >= 3 a single buffer (more L1, two CTAs per SM overlap each other) wins
+  static constexpr int NBUF = HDG_NBUF ? HDG_NBUF : (N1 <= 3 ? 2 : 1);
+  static constexpr bool DMMA = HDG_DMMA && N1 <= 8;
+  static constexpr int KS = (7 * N1 + 3) / 4;                             // DMMA k-steps (K = 7 n1)
+  static constexpr int WSCR = DMMA ? 32 * 9 : 32 * NOUT;                  // per-warp output transpose
   // shared mode adds the per-warp transpose scratch; stored mode stages h outputs in BUF
   static constexpr int smem_doubles(bool stored) { return NBUF * BUF + (stored ? 0 : (NWARP + 1) * WSCR); }
 };
@@ -333,6 +340,86 @@ __device__ __forceinline__ void apply_shared(const double* const (&nb)[FF][7], c
   }
 }
 
+// ------------------------------------------------------------------ FP64 tensor-core core
+// y (n1 x 32 facets of one warp row) = W (n1 x 7n1) . X (7n1 x 32) as 4 groups of
+// mma.sync.m8n8k4.f64 (DMMA): A = W padded to 8 rows (per-lane fragment in registers), B = the
+// facets' stencil values straight from the staged tile, D (8 x 8 facets) -> warp scratch.
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// per-lane A fragments: wa[s] = W[row = lane/4][stencil 4s + lane%4] (0 outside n1 x 7n1)
+template <int N1>
+__device__ __forceinline__ void dmma_wfrag(const double* W, double (&wa)[Cfg<N1>::KS], int lane) {
+  const int k = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int s = 0; s < Cfg<N1>::KS; ++s) {
+    const int st = 4 * s + t;
+    const int q = st / N1, m = st - q * N1;
+    wa[s] = (k < N1 && st < 7 * N1) ? W[(q * N1 + k) * N1 + m] : 0.0;
+  }
+}
+
+// stencil block q of facet (ii, jj): base pointer for lane's facet ii and stride along ii
+template <int N1, bool VERT>
+__device__ __forceinline__ const double* dmma_block(const double* Hs, const double* Vs, int hshift0, int hstep,
+                                                    int jj, int ii, int q, int& stride) {
+  using C = Cfg<N1>;
+  auto H = [&](int r, int c) { return Hs + r * C::RS + ((hshift0 + r * hstep) & 1) + c * C::S; };
+  auto V = [&](int c, int r) { return Vs + (r * C::VCOLS + c) * C::SV; };
+  if (!VERT) {
+    if (q < 3) { stride = C::S; return H(jj - 1 + q, ii); }
+    stride = C::SV;
+    const int dq = q - 3;
+    return V(ii + (dq & 1), jj - 1 + (dq >> 1));
+  }
+  if (q < 3) { stride = C::SV; return V(ii - 1 + q, jj); }
+  stride = C::S;
+  const int dq = q - 3;
+  return H(jj + (dq & 1), ii - 1 + (dq >> 1));
+}
+
+template <int N1, bool VERT>
+__device__ __forceinline__ void apply_dmma_row(const double* Hs, const double* Vs, int hshift0, int hstep, int jj,
+                                               const double (&wa)[Cfg<N1>::KS], double* scr, double (&acc)[N1],
+                                               int lane) {
+  using C = Cfg<N1>;
+  const int t = lane & 3, fl = lane >> 2;   // k-slot and facet-in-group of this lane's B element
+  const double* ptr[C::KS];
+  int inc[C::KS];
+#pragma unroll
+  for (int s = 0; s < C::KS; ++s) {
+    int st = 4 * s + t;
+    if (st >= 7 * N1) st = 0;                // padding column: any finite value (W is 0 there)
+    const int q = st / N1, m = st - q * N1;
+    int stride;
+    ptr[s] = dmma_block<N1, VERT>(Hs, Vs, hshift0, hstep, jj, fl + 1, q, stride) + m;
+    inc[s] = 8 * stride;
+  }
+  double d[4][2];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) { d[g][0] = 0.0; d[g][1] = 0.0; }
+#pragma unroll
+  for (int s = 0; s < C::KS; ++s) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) dmma_8x8x4(d[g][0], d[g][1], wa[s], ptr[s][g * inc[s]]);
+  }
+  // D[row = output k][col = facet 2t + c] -> scratch [facet][9], then each lane takes its facet
+  const int k = lane >> 2;
+  if (k < N1) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      scr[(8 * g + 2 * t) * 9 + k] = d[g][0];
+      scr[(8 * g + 2 * t + 1) * 9 + k] = d[g][1];
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int kk = 0; kk < N1; ++kk) acc[kk] = scr[lane * 9 + kk];
+  __syncwarp();
+}
+
 // Stored mode: this facet's merged matrix streams from HBM (coalesced across the warp).
 template <int N1>
 __device__ __forceinline__ void apply_stored(const double* const (&nb)[7], const double* Ws, double (&acc)[N1]) {
@@ -452,7 +539,14 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
     }
     if constexpr (!STORED) {
       double acc[F][N1];
-      apply_shared<N1, F>(nb, op.Wh, acc);
+      if constexpr (C::DMMA) {
+        double wa[C::KS];
+        dmma_wfrag<N1>(op.Wh, wa, tx);
+#pragma unroll
+        for (int f = 0; f < F; ++f) apply_dmma_row<N1, false>(Hs, Vs, hpar0, hstep, F * w + f + 1, wa, scr, acc[f], tx);
+      } else {
+        apply_shared<N1, F>(nb, op.Wh, acc);
+      }
 #pragma unroll
       for (int f = 0; f < F; ++f) {
         const int j = j0 + F * w + f;
@@ -487,7 +581,14 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
     }
     if constexpr (!STORED) {
       double acc[F][N1];
-      apply_shared<N1, F>(nb, op.Wv, acc);
+      if constexpr (C::DMMA) {
+        double wa[C::KS];
+        dmma_wfrag<N1>(op.Wv, wa, tx);
+#pragma unroll
+        for (int f = 0; f < F; ++f) apply_dmma_row<N1, true>(Hs, Vs, hpar0, hstep, F * w + f + 1, wa, scr, acc[f], tx);
+      } else {
+        apply_shared<N1, F>(nb, op.Wv, acc);
+      }
 #pragma unroll
       for (int f = 0; f < F; ++f) {
         const int j = j0 + F * w + f;

@@ -16,6 +16,17 @@ from paper_1705_09907_b200.problem import constant_problem
 from paper_1705_09907_b200.trace import TraceSystem
 import paper_1705_09907_b200._lib as L
 out = {"lib": os.path.basename(os.environ["HDGB200_LIB"])}
+# parity spot check of this variant (host formula of trace.py:87-94 with the same blocks)
+errs = []
+for (n, p) in [(37, 4), (40, 1), (33, 8), (35, 2)]:
+    m = build_cartesian(n, n + 3)
+    s = TraceSystem(m, p, constant_problem(0.0, 1.0))
+    x = np.random.default_rng(p).uniform(-1, 1, s.ndof)
+    lay = s.layout
+    S = s.operator.S_cls[0]
+    ref = lay.sum_owners(np.einsum("ij,ej->ei", S, lay.gather(x) * np.repeat(lay.side_mask(), p + 1, axis=1)))
+    errs.append(float(np.abs(s.matvec_free(x) - ref).max() / np.abs(ref).max()))
+out["parity_max_rel_err"] = max(errs)
 cases = [(1024, 4, False), (512, 4, True), (1024, 1, False), (768, 8, False), (384, 8, True)]
 for (n, p, stored) in cases:
     s = TraceSystem(build_cartesian(n, n), p, constant_problem(0.0, 1.0))
