@@ -405,6 +405,37 @@ int hdg_bj_sweep(const hdg_level* L, const double* b, const double* x_in, double
   return bj_sweep_w(L, b, x_in, x_out, 0.0, S(stream));
 }
 
+}  // extern "C"
+template <int N1, bool STORED>
+static int bj_zero_t(const hdg_level* L, MvArgs& a, double w, cudaStream_t s) {
+  SharedOp<(STORED ? 1 : N1)> op;
+  if constexpr (!STORED) {
+    std::memset(op.Wh, 0, sizeof(op.Wh));
+    std::memset(op.Wv, 0, sizeof(op.Wv));
+    std::memcpy(op.Dh, L->Dh.data(), sizeof(op.Dh));
+    std::memcpy(op.Dv, L->Dv.data(), sizeof(op.Dv));
+  } else {
+    std::memset(&op, 0, sizeof(op));
+  }
+  const int bs = 128;
+  bj_zero_kernel<N1, STORED><<<(unsigned)((L->n_blocks + bs - 1) / bs), bs, 0, s>>>(a, op, w, L->n_blocks);
+  CKL();
+  return 0;
+}
+
+// x_out = w D^-1 b  (the Jacobi step from x = 0, no operator apply)
+static int bj_sweep_zero(const hdg_level* L, const double* b, double* x_out, double w, cudaStream_t s) {
+  if (!L->has_bj) return fail(HDG_ESTATE, "block-Jacobi state not set");
+  if (L->ndof == 0) return 0;
+  MvArgs a{};
+  a.nx = L->nx; a.ny = L->ny; a.nxp = L->nxp; a.nh = (int)L->nh;
+  a.b = b; a.out = x_out; a.Dh = L->dDh; a.Dv = L->dDv;
+#define BJZ_CASE(N) return L->stored ? bj_zero_t<N, true>(L, a, w, s) : bj_zero_t<N, false>(L, a, w, s);
+  HDG_N1_SWITCH(L->n1, BJZ_CASE)
+#undef BJZ_CASE
+}
+extern "C" {
+
 // weight of Jacobi step k (1-based) of `steps`: omega, or 1/theta_k (Chebyshev nodes)
 static double bj_weight(const hdg_level* L, int k, int steps) {
   if (!L->bj_cheb) return L->omega;
@@ -707,15 +738,25 @@ static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1
   double* xk = mg->X[k];
   if (k == mg->n - 1) return coarse_apply(mg, b, xk, s);
   const size_t bytes = sizeof(double) * (size_t)L->ndof;
-  if (zero_init && L->ndof > 0) CK(cudaMemsetAsync(xk, 0, bytes, s));
   double* cur = xk;
   double* oth = mg->Tm[k];
   int rc;
   const bool fsai = L->use_fsai;   // the smoother attached last (FSAI or block-Jacobi)
+  int first = 0;
+  if (zero_init && L->ndof > 0) {
+    if (!fsai && nu1 >= 1) {
+      // x = 0: the first Jacobi step needs no operator apply (x_1 = w D^-1 b)
+      if ((rc = bj_sweep_zero(L, b, oth, bj_weight(L, 1, nu1), s))) return rc;
+      std::swap(cur, oth);
+      first = 1;
+    } else {
+      CK(cudaMemsetAsync(xk, 0, bytes, s));
+    }
+  }
   if (fsai) {
     if ((rc = fsai_sweeps(L, b, cur, mg->R[k], oth, nu1, s))) return rc;
   } else {
-    for (int it = 0; it < nu1; ++it) {
+    for (int it = first; it < nu1; ++it) {
       if ((rc = bj_sweep_w(L, b, cur, oth, bj_weight(L, it + 1, nu1), s))) return rc;
       std::swap(cur, oth);
     }

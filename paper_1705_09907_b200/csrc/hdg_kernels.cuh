@@ -1088,6 +1088,39 @@ __global__ void sum_partials_kernel(const double* __restrict__ partials, int n, 
   if (threadIdx.x == 0) *out = s;
 }
 
+// ------------------------------------------------------------------- Jacobi step from x = 0
+// First smoothing sweep of a coarse-level visit starts from x = 0 (multigrid.py:400): the
+// operator apply vanishes and the sweep is facet-local, x_f = w D_f^-1 b_f.
+template <int N1, bool STORED>
+__global__ void bj_zero_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 : N1)> op, double w,
+                               long long nblocks) {
+  const long long bk = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (bk >= nblocks) return;
+  const bool vert = bk >= a.nh;
+  double r[N1], dinv[N1 * N1];
+#pragma unroll
+  for (int k = 0; k < N1; ++k) r[k] = __ldg(a.b + bk * N1 + k);
+  if constexpr (!STORED) {
+#pragma unroll
+    for (int t = 0; t < N1 * N1; ++t) dinv[t] = vert ? op.Dv[t] : op.Dh[t];
+  } else {
+    int i, j;
+    if (!vert) { j = (int)(bk / a.nx) + 1; i = (int)(bk % a.nx); }
+    else { const long long u = bk - a.nh; i = (int)(u / a.ny) + 1; j = (int)(u % a.ny); }
+    const long long slot = (long long)j * a.nxp + i;
+    const double* D = (vert ? a.Dv : a.Dh) + (size_t)(slot >> 5) * N1 * N1 * 32 + (slot & 31);
+#pragma unroll
+    for (int t = 0; t < N1 * N1; ++t) dinv[t] = __ldg(D + (size_t)t * 32);
+  }
+#pragma unroll
+  for (int k = 0; k < N1; ++k) {
+    double s = 0.0;
+#pragma unroll
+    for (int m = 0; m < N1; ++m) s = fma(dinv[k * N1 + m], r[m], s);
+    a.out[bk * N1 + k] = w * s;
+  }
+}
+
 // ------------------------------------------------------------------------------ FSAI (CSR)
 // y = M x  or  x_out = x_in + w (M x)   (multigrid.py:72-74, 83-88); 4 lanes per row
 template <bool AXPY>
