@@ -117,7 +117,7 @@ static constexpr int kThreads = HDG_WS ? NT + 32 : NT;
 
 template <int N1, bool STORED, int EPI>
 static int set_attr() {
-  const size_t smem = Cfg<N1>::smem_doubles(STORED) * sizeof(double);
+  const size_t smem = Cfg<N1, STORED>::smem_doubles(STORED) * sizeof(double);
   CK(cudaFuncSetAttribute(kernel_ptr<N1, STORED, EPI>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   return 0;
 }
@@ -145,7 +145,7 @@ static int sm_count() {
 // persistent grid: every SM gets as many CTAs as fit (<= MAX_CTAS_PER_SM), never more than tiles
 template <int N1, bool STORED, int EPI>
 static int grid_for(const hdg_level* L) {
-  using C = Cfg<N1>;
+  using C = Cfg<N1, STORED>;
   static int occ = -1;
   if (occ < 0) {
     const size_t smem = C::smem_doubles(STORED) * sizeof(double);
@@ -161,7 +161,7 @@ static int grid_for(const hdg_level* L) {
 
 template <int N1, bool STORED, int EPI>
 static int apply_t(const hdg_level* L, MvArgs& a, cudaStream_t s) {
-  using C = Cfg<N1>;
+  using C = Cfg<N1, STORED>;
   const size_t smem = C::smem_doubles(STORED) * sizeof(double);
   const int grid = grid_for<N1, STORED, EPI>(L);
   SharedOp<(STORED ? 1 : N1)> op;

@@ -36,7 +36,10 @@ namespace hdg {
 #define HDG_NBUF 0         // stage buffers per CTA; 0 = per-order default (measured, see Cfg)
 #endif
 #ifndef HDG_F_MAXN1
-#define HDG_F_MAXN1 5      // two facets per thread per orientation up to this n1
+#define HDG_F_MAXN1 13     // cap on the two-facets-per-thread rule (tuning knob)
+#endif
+#ifndef HDG_F_MAXN1_SHARED
+#define HDG_F_MAXN1_SHARED 9
 #endif
 #ifndef HDG_MINB
 #define HDG_MINB 2         // __launch_bounds__ min blocks per SM for the trace kernel
@@ -59,9 +62,11 @@ constexpr int MAX_CTAS_PER_SM = 8;
 
 enum Epi { EPI_Y = 0, EPI_RES = 1, EPI_BJ = 2, EPI_RESPR = 3 };
 
-template <int N1> struct Cfg {
+template <int N1, bool ST = false> struct Cfg {
   static constexpr int S = N1;                      // facet blocks contiguous in a staged run
-  static constexpr int F = (N1 <= HDG_F_MAXN1) ? 2 : 1;  // facets per thread per orientation
+  // facets per thread per orientation (measured: 2 pays up to p=8 when W is in the constant
+  // bank, up to p=4 when W streams from HBM)
+  static constexpr int F = (N1 <= (ST ? 5 : HDG_F_MAXN1_SHARED)) && (N1 <= HDG_F_MAXN1) ? 2 : 1;
   static constexpr int TY = NWARP * F;              // tile height in elements
   static constexpr int WSZ = 7 * N1 * N1;           // merged facet operator entries
   static constexpr int DSZ = N1 * N1;               // block-Jacobi inverse entries
@@ -223,8 +228,8 @@ __device__ __forceinline__ void run_zero(double* buf, const Run& r, int lane) {
   for (int e = r.ehi + lane; e < r.len; e += 32) d[e] = 0.0;
 }
 
-template <int N1> __device__ __forceinline__ Run h_run(const MvArgs& a, int i0, int j0, int r) {
-  using C = Cfg<N1>;
+template <int N1, bool ST> __device__ __forceinline__ Run h_run(const MvArgs& a, int i0, int j0, int r) {
+  using C = Cfg<N1, ST>;
   const int j = j0 - 1 + r;
   Run q;
   q.g0 = h_run_start<N1>(a, i0, j0, r);
@@ -237,10 +242,10 @@ template <int N1> __device__ __forceinline__ Run h_run(const MvArgs& a, int i0, 
 }
 // V columns c = c0, c0 + cstep, ... of the tile: lane-constant element offsets hoisted out of
 // the column loop, so each copy is a pointer add, a predicate and the LDGSTS.
-template <int N1>
+template <int N1, bool ST>
 __device__ __forceinline__ void stage_v_columns(const MvArgs& a, double* Vs, int i0, int j0, int c0, int cstep,
                                                 int lane) {
-  using C = Cfg<N1>;
+  using C = Cfg<N1, ST>;
   constexpr int LEN = C::VROWS * N1;
   constexpr int NQ = (LEN + 31) / 32;
   const int elo = (j0 == 0) ? N1 : 0;                          // row j = -1
@@ -276,9 +281,9 @@ __device__ __forceinline__ void stage_v_columns(const MvArgs& a, double* Vs, int
 // most two 8-byte LDGSTS for a misaligned head/tail.  Completion: `bar` (2 arrivals per warp).
 //   H region: h(i, j), i in [i0-1, i0+TX), j in [j0-1, j0+TY]      ((TY+2) x (TX+1) blocks)
 //   V region: v(i, j), i in [i0-1, i0+TX], j in [j0-1, j0+TY)      ((TX+2) x (TY+1) blocks)
-template <int N1>
+template <int N1, bool ST>
 __device__ __forceinline__ void stage_tile(const MvArgs& a, double* buf, int i0, int j0, uint64_t* bar) {
-  using C = Cfg<N1>;
+  using C = Cfg<N1, ST>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool edge = (i0 == 0) || (j0 == 0) || (i0 + TX >= a.nx) || (j0 + C::TY >= a.ny);
 #ifdef HDG_EXP_NOSTAGE
@@ -288,17 +293,17 @@ __device__ __forceinline__ void stage_tile(const MvArgs& a, double* buf, int i0,
 #endif
   if (lane == 0) {
     unsigned bytes = 0;
-    for (int r = warp; r < C::HROWS; r += NWARP) bytes += run_bytes(h_run<N1>(a, i0, j0, r));
+    for (int r = warp; r < C::HROWS; r += NWARP) bytes += run_bytes(h_run<N1, ST>(a, i0, j0, r));
     fence_proxy_async();               // prior generic reads/writes of this buffer -> async proxy
     mbar_arrive_expect_tx(bar, bytes);
-    for (int r = warp; r < C::HROWS; r += NWARP) run_issue(a.x, buf, h_run<N1>(a, i0, j0, r), bar);
+    for (int r = warp; r < C::HROWS; r += NWARP) run_issue(a.x, buf, h_run<N1, ST>(a, i0, j0, r), bar);
   }
   if (edge) {  // zero Dirichlet / out-of-mesh parts of H rows (interior tiles skip this)
-    for (int r = warp; r < C::HROWS; r += NWARP) run_zero(buf, h_run<N1>(a, i0, j0, r), lane);
+    for (int r = warp; r < C::HROWS; r += NWARP) run_zero(buf, h_run<N1, ST>(a, i0, j0, r), lane);
   }
   // V columns: coalesced 8-byte LDGSTS from the contiguous run, transposed into [row][col];
   // src-size 0 zero-fills Dirichlet / out-of-mesh blocks
-  stage_v_columns<N1>(a, buf + C::HSZ, i0, j0, warp, NWARP, lane);
+  stage_v_columns<N1, ST>(a, buf + C::HSZ, i0, j0, warp, NWARP, lane);
   cp_async_mbar_arrive(bar);           // every thread: one arrival when its LDGSTS land
 }
 
@@ -515,7 +520,7 @@ __device__ __forceinline__ void store_h_row(const MvArgs& a, double* scr, int i0
 template <int N1, bool STORED, int EPI>
 __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(STORED ? 1 : N1)>& op,
                                              double* buf, double* scr, int i0, int j0, double& nrm) {
-  using C = Cfg<N1>;
+  using C = Cfg<N1, STORED>;
   constexpr int F = C::F;
   constexpr int NO = NOutOf<EPI, N1>::v;
   const int tx = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -666,7 +671,7 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
 template <int N1, bool STORED, int EPI>
 __global__ void __launch_bounds__(NT, STORED ? 2 : (N1 <= 9 ? HDG_MINB : 1))
 trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 : N1)> op) {
-  using C = Cfg<N1>;
+  using C = Cfg<N1, STORED>;
   extern __shared__ __align__(16) double smem[];
   const int tiles_x = (a.nx + TX - 1) / TX;
   const int ntiles = tiles_x * ((a.ny + C::TY - 1) / C::TY);
@@ -683,7 +688,7 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
 #pragma unroll
   for (int q = 0; q < NB - 1; ++q) {
     const int t = blockIdx.x + q * gridDim.x;
-    if (t < ntiles) stage_tile<N1>(a, smem + q * C::BUF, (t % tiles_x) * TX, (t / tiles_x) * C::TY, &bars[q]);
+    if (t < ntiles) stage_tile<N1, STORED>(a, smem + q * C::BUF, (t % tiles_x) * TX, (t / tiles_x) * C::TY, &bars[q]);
   }
   int slot = 0;
   unsigned phase = 0;
@@ -691,7 +696,7 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
     const int pre = tile + (NB - 1) * gridDim.x;
     if (pre < ntiles) {
       const int ps = (slot + NB - 1) % NB;
-      stage_tile<N1>(a, smem + ps * C::BUF, (pre % tiles_x) * TX, (pre / tiles_x) * C::TY, &bars[ps]);
+      stage_tile<N1, STORED>(a, smem + ps * C::BUF, (pre % tiles_x) * TX, (pre / tiles_x) * C::TY, &bars[ps]);
     }
     mbar_wait(&bars[slot], phase);
     __syncthreads();
@@ -720,22 +725,22 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
 // One producer warp (warp NWARP) streams tiles into an NB-slot ring; the NWARP compute warps
 // only compute.  full[slot]: 1 expect_tx arrival (producer lane 0) + 32 LDGSTS arrivals;
 // empty[slot]: NT consumer arrivals.
-template <int N1>
+template <int N1, bool ST>
 __device__ __forceinline__ void produce_tile(const MvArgs& a, double* buf, int i0, int j0, uint64_t* full) {
-  using C = Cfg<N1>;
+  using C = Cfg<N1, ST>;
   const int lane = threadIdx.x & 31;
   const bool edge = (i0 == 0) || (j0 == 0) || (i0 + TX >= a.nx) || (j0 + C::TY >= a.ny);
   if (edge) {
-    for (int r = 0; r < C::HROWS; ++r) run_zero(buf, h_run<N1>(a, i0, j0, r), lane);
+    for (int r = 0; r < C::HROWS; ++r) run_zero(buf, h_run<N1, ST>(a, i0, j0, r), lane);
   }
-  stage_v_columns<N1>(a, buf + C::HSZ, i0, j0, 0, 1, lane);
+  stage_v_columns<N1, ST>(a, buf + C::HSZ, i0, j0, 0, 1, lane);
   __syncwarp();
   if (lane == 0) {
     unsigned bytes = 0;
-    for (int r = 0; r < C::HROWS; ++r) bytes += run_bytes(h_run<N1>(a, i0, j0, r));
+    for (int r = 0; r < C::HROWS; ++r) bytes += run_bytes(h_run<N1, ST>(a, i0, j0, r));
     fence_proxy_async();
     mbar_arrive_expect_tx(full, bytes);
-    for (int r = 0; r < C::HROWS; ++r) run_issue(a.x, buf, h_run<N1>(a, i0, j0, r), full);
+    for (int r = 0; r < C::HROWS; ++r) run_issue(a.x, buf, h_run<N1, ST>(a, i0, j0, r), full);
   }
   cp_async_mbar_arrive(full);
 }
@@ -743,7 +748,7 @@ __device__ __forceinline__ void produce_tile(const MvArgs& a, double* buf, int i
 template <int N1, bool STORED, int EPI>
 __global__ void __launch_bounds__(NT + 32, HDG_WS_MINB)
 trace_apply_ws_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 : N1)> op) {
-  using C = Cfg<N1>;
+  using C = Cfg<N1, STORED>;
   constexpr int NB = C::NBUF;
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t full[NB], empty[NB];
@@ -763,7 +768,7 @@ trace_apply_ws_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ?
   if (threadIdx.x >= NT) {  // ---- producer warp
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       mbar_wait(&empty[slot], phase ^ 1u);
-      produce_tile<N1>(a, smem + slot * C::BUF, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, &full[slot]);
+      produce_tile<N1, STORED>(a, smem + slot * C::BUF, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, &full[slot]);
       if (++slot == NB) { slot = 0; phase ^= 1u; }
     }
     return;
