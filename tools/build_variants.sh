@@ -3,8 +3,6 @@
 cd "$(dirname "$0")/.."
 rm -rf build/variants; mkdir -p build/variants
 build() { name=$1; shift; nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -shared -Xcompiler -fPIC -Iinclude "$@" -o build/variants/$name.so paper_1705_09907_b200/csrc/hdg_capi.cu 2>build/variants/$name.log & }
-build base
-build f9 -DHDG_F_MAXN1=9
-build f13 -DHDG_F_MAXN1=13
+build f13 -DHDG_F_MAXN1_SHARED=13
 wait
 ls build/variants/*.so
