@@ -451,14 +451,14 @@ template <int EPI, int N1> struct NOutOf { static constexpr int v = (EPI == EPI_
 template <int N1, bool STORED, int EPI>
 __device__ __forceinline__ void facet_epilogue(const MvArgs& a, int blk, const double* xf, const double* Dc,
                                                const double* Ds, const double (&acc)[N1], double (&o)[N1],
-                                               double& nrm) {
+                                               double& nrm, const double* bsm = nullptr) {
   if constexpr (EPI == EPI_Y) {
 #pragma unroll
     for (int k = 0; k < N1; ++k) o[k] = acc[k];
   } else {
     double r[N1];
 #pragma unroll
-    for (int k = 0; k < N1; ++k) r[k] = __ldg(a.b + blk * N1 + k) - acc[k];
+    for (int k = 0; k < N1; ++k) r[k] = (bsm ? bsm[k] : __ldg(a.b + blk * N1 + k)) - acc[k];
     if constexpr (EPI == EPI_RES) {
 #pragma unroll
       for (int k = 0; k < N1; ++k) {
@@ -555,9 +555,25 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
 #pragma unroll
       for (int f = 0; f < F; ++f) {
         const int j = j0 + F * w + f;
+        const bool rowok = (j >= 1 && j <= a.ny - 1);   // warp-uniform
         double oh[N1];
-        if (i < a.nx && j >= 1 && j <= a.ny - 1)
-          facet_epilogue<N1, false, EPI>(a, hblk(a.nx, i, j), nb[f][1], op.Dh, nullptr, acc[f], oh, nrm);
+        const double* bsm = nullptr;
+        if constexpr (EPI != EPI_Y) {
+          // the row's right-hand side is one contiguous run: load it coalesced into the
+          // warp scratch, then each lane reads its facet's n1 values
+          if (rowok) {
+            const int count = min(TX, a.nx - i0) * N1;
+            const double* src = a.b + hblk(a.nx, i0, j) * N1;
+#pragma unroll
+            for (int q = 0; q < N1; ++q)
+              if (tx + 32 * q < count) scr[tx + 32 * q] = __ldg(src + tx + 32 * q);
+            __syncwarp();
+            bsm = scr + tx * N1;
+          }
+        }
+        if (i < a.nx && rowok)
+          facet_epilogue<N1, false, EPI>(a, hblk(a.nx, i, j), nb[f][1], op.Dh, nullptr, acc[f], oh, nrm, bsm);
+        if constexpr (EPI != EPI_Y) __syncwarp();
         store_h_row<N1, NO>(a, scr, i0, j, oh, tx);
       }
     } else {
@@ -956,54 +972,54 @@ __device__ __forceinline__ void coarse_side(const HArgs& h, const double* ec, in
   if (s == 2 && J + 1 <= h.nyc - 1) blk = (long long)J * h.nxc + I;
   if (s == 3 && I >= 1) blk = h.nhc + (long long)(I - 1) * h.nyc + J;
   if (s == 1 && I + 1 <= h.nxc - 1) blk = h.nhc + (long long)I * h.nyc + J;
-  if (blk >= 0) { v[0] = __ldg(ec + 2 * blk); v[1] = __ldg(ec + 2 * blk + 1); }
-  else { v[0] = 0.0; v[1] = 0.0; }
+  if (blk >= 0) {
+    const double2 e = __ldg(reinterpret_cast<const double2*>(ec) + blk);
+    v[0] = e.x; v[1] = e.y;
+  } else {
+    v[0] = 0.0; v[1] = 0.0;
+  }
 }
 
+// fine facet t (n1 = 2, one double2 per facet) += its prolongation from the coarse level
 __global__ void h_prolong_add_kernel(const HArgs h, const double* __restrict__ ec, double* __restrict__ xf) {
   const int nxf = 2 * h.nxc, nyf = 2 * h.nyc;
   const long long nvf = (long long)(nxf - 1) * nyf;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= h.nhf + nvf) return;
   double add[2] = {0.0, 0.0};
+  bool half;
+  int I, J, hf, cf;
+  long long cb = 0;
   if (t < h.nhf) {  // fine h(i, j), block (j-1)*nxf + i
     const int j = (int)(t / nxf) + 1, i = (int)(t % nxf);
-    const int I = i >> 1;
-    if ((j & 1) == 0) {
-      const int J = j >> 1, hf = i & 1;
-      const long long cb = (long long)(J - 1) * h.nxc + I;
-      const double e0 = __ldg(ec + 2 * cb), e1 = __ldg(ec + 2 * cb + 1);
-      for (int k = 0; k < 2; ++k) add[k] = h.halves[hf * 4 + k * 2] * e0 + h.halves[hf * 4 + k * 2 + 1] * e1;
-    } else {
-      const int J = (j - 1) >> 1, cf = (i & 1) ? 3 : 2;
-      const double* tm = hcross(h, I, J, cf);
-      for (int s = 0; s < 4; ++s) {
-        double v[2];
-        coarse_side(h, ec, I, J, s, v);
-        for (int k = 0; k < 2; ++k) add[k] += tm[k * 8 + s * 2] * v[0] + tm[k * 8 + s * 2 + 1] * v[1];
-      }
-    }
-  } else {  // fine v(i, j), block nhf + (i-1)*nyf + j
+    I = i >> 1;
+    half = (j & 1) == 0;
+    if (half) { J = j >> 1; hf = i & 1; cb = (long long)(J - 1) * h.nxc + I; }
+    else { J = (j - 1) >> 1; cf = (i & 1) ? 3 : 2; }
+  } else {          // fine v(i, j), block nhf + (i-1)*nyf + j
     const long long u = t - h.nhf;
     const int i = (int)(u / nyf) + 1, j = (int)(u % nyf);
-    const int J = j >> 1;
-    if ((i & 1) == 0) {
-      const int I = i >> 1, hf = j & 1;
-      const long long cb = h.nhc + (long long)(I - 1) * h.nyc + J;
-      const double e0 = __ldg(ec + 2 * cb), e1 = __ldg(ec + 2 * cb + 1);
-      for (int k = 0; k < 2; ++k) add[k] = h.halves[hf * 4 + k * 2] * e0 + h.halves[hf * 4 + k * 2 + 1] * e1;
-    } else {
-      const int I = (i - 1) >> 1, cf = (j & 1) ? 1 : 0;
-      const double* tm = hcross(h, I, J, cf);
-      for (int s = 0; s < 4; ++s) {
-        double v[2];
-        coarse_side(h, ec, I, J, s, v);
-        for (int k = 0; k < 2; ++k) add[k] += tm[k * 8 + s * 2] * v[0] + tm[k * 8 + s * 2 + 1] * v[1];
-      }
+    J = j >> 1;
+    half = (i & 1) == 0;
+    if (half) { I = i >> 1; hf = j & 1; cb = h.nhc + (long long)(I - 1) * h.nyc + J; }
+    else { I = (i - 1) >> 1; cf = (j & 1) ? 1 : 0; }
+  }
+  if (half) {
+    const double2 e = __ldg(reinterpret_cast<const double2*>(ec) + cb);
+    for (int k = 0; k < 2; ++k) add[k] = h.halves[hf * 4 + k * 2] * e.x + h.halves[hf * 4 + k * 2 + 1] * e.y;
+  } else {
+    const double* tm = hcross(h, I, J, cf);
+    for (int s = 0; s < 4; ++s) {
+      double v[2];
+      coarse_side(h, ec, I, J, s, v);
+      for (int k = 0; k < 2; ++k) add[k] += __ldg(tm + k * 8 + s * 2) * v[0] + __ldg(tm + k * 8 + s * 2 + 1) * v[1];
     }
   }
-  xf[2 * t] += add[0];
-  xf[2 * t + 1] += add[1];
+  double2* xp = reinterpret_cast<double2*>(xf) + t;
+  double2 x = *xp;
+  x.x += add[0];
+  x.y += add[1];
+  *xp = x;
 }
 
 // contribution of coarse element (I, J)'s 4 cross facets to its side-s coarse dofs
