@@ -409,6 +409,28 @@ class OracleTrace:
         return x, maxiter
 
 
+def reconstruct_all(system, lam):
+    """trace.py:171-178 / local.py:240-251: (q, u) per element from the trace solution."""
+    nb = system.core.nb
+    q = np.empty((system.grid.n_elems, 2 * nb))
+    u = np.empty((system.grid.n_elems, nb))
+    xe = np.where(system.gmask, np.asarray(lam, float)[system.gidx], 0.0)
+    for e, l in enumerate(system.locals):
+        sol = lu_solve(l.lu, l.load - l.trace_cols @ xe[e])
+        q[e], u[e] = sol[:2 * nb], sol[2 * nb:]
+    return q, u
+
+
+def exact_trace(system, func):
+    """trace.py:188-195: facet L2 projection of func onto the interior trace space."""
+    lam = np.zeros(system.ndof)
+    n1 = system.n1
+    for bi, f in enumerate(system.interior):
+        e, side = system.grid.f2e[f, 0]
+        lam[bi * n1:(bi + 1) * n1] = system.core.project(func, e, side)
+    return lam
+
+
 def injected_shared_system(n, p, dom=1.0):
     """Builder restatement: the K=I, tau=1 system on an n x n mesh
     from ONE condensed block taken from an 8x8 mesh of the same spacing; Dirichlet

@@ -185,6 +185,7 @@ class ElementClasses:
             F[:, cols, 2 * nb + idx] += ts * fm[s]
             Ms[:, cols, cols] += ts * fm[s]
         X = np.linalg.solve(L, T)                                    # L^-1 T (local.py:233-234)
+        self.L = L                                                   # for reconstruction (local.py:249)
         self.S = F @ X + Ms                                          # local.py:235
         self.Z = np.swapaxes(np.linalg.solve(np.swapaxes(L, 1, 2), np.swapaxes(F, 1, 2)), 1, 2)
         self.T = T

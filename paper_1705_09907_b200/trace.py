@@ -349,17 +349,14 @@ class TraceSystem:
             T[2 * nb + idx, cols] += -tau * fm
         return T
 
-    def _condensed_rhs(self, spec, chunk=1 << 16):
-        """Loads (local.py:178-184) condensed per element (local.py:236), summed over owners.
-        Source evaluated in chunks; elements with no source and no Dirichlet side add 0."""
+    def _element_loads(self, spec, chunk=1 << 16):
+        """Yield (element indices, raw loads (n, 3nb)) for elements with a nonzero load:
+        source (local.py:184) and the Dirichlet fold of the boundary datum (local.py:179-184)."""
         ref = self.ops.ref
         n1, nb = ref.n1, ref.nb
         m = self.mesh
         E = m.n_x * m.n_y
-        if self.ndof == 0:
-            return np.zeros(0)
         wj = ref.w2 * (m.dx * m.dy / 4.0)
-        cl = np.zeros((E, 4 * n1))
         for e0 in range(0, E, chunk):
             qx, qy = self._quad_points(e0, min(E, e0 + chunk))
             fs = np.asarray(spec.source(qx, qy), float).reshape(qx.shape)
@@ -367,7 +364,7 @@ class TraceSystem:
                 continue
             load = np.zeros((fs.shape[0], 3 * nb))
             load[:, 2 * nb:] = (fs * wj) @ ref.interp_2d
-            cl[e0:e0 + fs.shape[0]] = self._condense_loads(np.arange(e0, e0 + fs.shape[0]), load)
+            yield np.arange(e0, e0 + fs.shape[0]), load
         inner = self.layout.side_mask()
         bnd_e, bnd_s = np.nonzero(~inner)
         if bnd_e.size:
@@ -391,9 +388,44 @@ class TraceSystem:
                 lam_bc = np.zeros((ub.size, 4 * n1))
                 for k in range(n1):
                     lam_bc[inv, bnd_s * n1 + k] = proj[:, k]
-                load_bc = -np.einsum("eij,ej->ei", self._trace_cols(ub), lam_bc)
-                cl[ub] += self._condense_loads(ub, load_bc)
+                yield ub, -np.einsum("eij,ej->ei", self._trace_cols(ub), lam_bc)
+
+    def _condensed_rhs(self, spec):
+        """Loads condensed per element (local.py:236), summed over owners (trace.py:67)."""
+        n1 = self.ops.n1
+        E = self.mesh.n_x * self.mesh.n_y
+        if self.ndof == 0:
+            return np.zeros(0)
+        cl = np.zeros((E, 4 * n1))
+        for idx, load in self._element_loads(spec):
+            cl[idx] += self._condense_loads(idx, load)
         return self.layout.sum_owners(cl)
+
+    def reconstruct_all(self, lam):
+        """trace.py:171-178 / local.py:240-251: volume (q, u) on every element from the trace
+        solution, as two batched device GEMMs per element class: sol = L^-1 (load - T lam_e)."""
+        import torch
+        if self.classes is None:
+            raise NotImplementedError("reconstruction of GPU-condensed media: use the host class path")
+        nb = self.ops.nb
+        E = self.mesh.n_x * self.mesh.n_y
+        lam = lam.cpu().numpy() if hasattr(lam, "cpu") else np.asarray(lam, float)
+        lam_e = self.layout.gather(lam) if self.ndof else np.zeros((E, 4 * self.ops.n1))
+        load = np.zeros((E, 3 * nb))
+        for idx, ld in self._element_loads(self.spec):
+            load[idx] += ld
+        Linv = np.linalg.inv(self.classes.L)
+        dev = "cuda"
+        rhs = torch.as_tensor(load, device=dev) - torch.einsum(
+            "eij,ej->ei", torch.as_tensor(self.classes.T[self.elem_class], device=dev),
+            torch.as_tensor(lam_e, device=dev)) if self.classes.n > 1 else \
+            torch.as_tensor(load, device=dev) - torch.as_tensor(lam_e, device=dev) @ torch.as_tensor(self.classes.T[0].T, device=dev)
+        if self.classes.n == 1:
+            sol = rhs @ torch.as_tensor(Linv[0].T, device=dev)
+        else:
+            sol = torch.einsum("eij,ej->ei", torch.as_tensor(Linv[self.elem_class], device=dev), rhs)
+        sol = sol.cpu().numpy()
+        return sol[:, :2 * nb], sol[:, 2 * nb:]
 
     # -- reference attributes -----------------------------------------------------------------
     @property
@@ -460,6 +492,28 @@ class TraceSystem:
             check(lib.hdg_xpby(dev.ptr(z), rz_new / rz, dev.ptr(d), n, s))
             rz = rz_new
         return dev.back(x, was_np), maxiter
+
+
+def exact_trace(system, func):
+    """trace.py:188-195: facet L2 projection of func onto the interior trace space (host)."""
+    ref = system.ops.ref
+    lay = system.layout
+    m = system.mesh
+    nx, ny, n1 = lay.nx, lay.ny, lay.n1
+    t = ref.quad.nodes
+    # interior facets in block order with their start point and tangent (mesh.py:76-90)
+    jh, ih = np.meshgrid(np.arange(1, ny), np.arange(nx), indexing="ij")
+    iv, jv = np.meshgrid(np.arange(1, nx), np.arange(ny), indexing="ij")
+    px = np.concatenate([m.x0 + ih.ravel() * m.dx, m.x0 + iv.ravel() * m.dx])
+    py = np.concatenate([m.y0 + jh.ravel() * m.dy, m.y0 + jv.ravel() * m.dy])
+    horiz = np.r_[np.ones(ih.size, bool), np.zeros(iv.size, bool)]
+    ln = np.where(horiz, m.dx, m.dy)
+    sl = ln[:, None] * (t[None, :] + 1.0) / 2.0
+    X = px[:, None] + np.where(horiz, 1.0, 0.0)[:, None] * sl
+    Y = py[:, None] + np.where(horiz, 0.0, 1.0)[:, None] * sl
+    g = np.asarray(func(X, Y), float).reshape(X.shape)
+    rhs = (g * ref.quad.weights[None, :]) @ ref.interp_1d
+    return np.linalg.solve(ref.mass1, rhs.T).T.reshape(-1) if g.size else np.zeros(0)
 
 
 def flop_memop_count(system, mode):

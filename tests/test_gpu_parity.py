@@ -384,3 +384,15 @@ def test_anisotropic_gpu_condensation_and_vcycle(P, monkeypatch):
     b = rng.uniform(-1, 1, levels[0].ndof)
     assert rel(levels[0].matvec(b), lo[0].matvec(b)) < 1e-11
     assert rel(P.mg.v_cycle(levels, b), O.v_cycle(lo, b)) < 1e-11
+
+
+def test_reconstruct_all_matches_oracle(P):
+    """trace.py:171-178 (volume recovery after the solve, SURVEY 8(f) #4) on the device."""
+    for spec_o, spec_p in [(specs.manufactured(O.Spec), specs.manufactured(P.pb.ProblemSpec)),
+                           (specs.constant(O.Spec, 0.0, 1.0), specs.constant(P.pb.ProblemSpec, 0.0, 1.0))]:
+        s = P.tr.TraceSystem(P.mesh(6, 5), 2, spec_p)
+        o = O.OracleTrace(O.Grid(6, 5), 2, spec_o)
+        lam = np.random.default_rng(1).standard_normal(s.ndof)
+        q, u = s.reconstruct_all(lam)
+        qo, uo = O.reconstruct_all(o, lam)
+        assert rel(q, qo) < 1e-11 and rel(u, uo) < 1e-11

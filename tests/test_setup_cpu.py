@@ -198,3 +198,11 @@ def test_anisotropic_hierarchy_operators_match_oracle():
     for lev, ol in zip(levels, lo):
         v = np.random.default_rng(lev.ndof).standard_normal(lev.ndof)
         assert rel(lev.operator.tocsr() @ v, ol.operator @ v) < 1e-12
+
+
+def test_exact_trace_matches_oracle():
+    from paper_1705_09907_b200.trace import exact_trace
+    f = lambda x, y: x * x - 2 * x * y + 0.5 * y * y
+    s = TraceSystem(build_cartesian(5, 4), 3, specs.manufactured(ProblemSpec))
+    o = O.OracleTrace(O.Grid(5, 4), 3, specs.manufactured(O.Spec))
+    assert rel(exact_trace(s, f), O.exact_trace(o, f)) < 1e-13
