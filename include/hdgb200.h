@@ -107,6 +107,12 @@ int hdg_transfer_create_p(const hdg_level* fine, const hdg_level* coarse, const 
  * ncross_sets = 1 (shared by every coarse element) or Ec = coarse element count. */
 int hdg_transfer_create_h(const hdg_level* fine, const hdg_level* coarse, const double* halves,
                           const double* cross, int64_t ncross_sets, hdg_transfer** out);
+/* the same on row WINDOWS of the meshes (multi-GPU strips): the fine level's mesh is rows
+ * [fine_row0, fine_row0 + ny_fine) of the global fine mesh, the coarse level's rows
+ * [coarse_row0, ...) of the global coarse mesh; cross maps are per WINDOW coarse element. */
+int hdg_transfer_create_h_window(const hdg_level* fine, const hdg_level* coarse, const double* halves,
+                                 const double* cross, int64_t ncross_sets, int fine_row0,
+                                 int coarse_row0, hdg_transfer** out);
 int hdg_transfer_destroy(hdg_transfer* t);
 int hdg_prolong_add(const hdg_transfer* t, const double* e_coarse, double* x_fine, void* stream);
 int hdg_restrict(const hdg_transfer* t, const double* r_fine, double* r_coarse, void* stream);

@@ -40,6 +40,8 @@ SIGNATURES = [
     ("hdg_transfer_create_p", c_int, [c_void_p, c_void_p, c_void_p, ctypes.POINTER(c_void_p)]),
     ("hdg_transfer_create_h", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
                                       ctypes.POINTER(c_void_p)]),
+    ("hdg_transfer_create_h_window", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int,
+                                             ctypes.POINTER(c_void_p)]),
     ("hdg_transfer_destroy", c_int, [c_void_p]),
     ("hdg_prolong_add", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     ("hdg_restrict", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -559,17 +559,19 @@ int hdg_transfer_create_p(const hdg_level* fine, const hdg_level* coarse, const 
   return 0;
 }
 
-int hdg_transfer_create_h(const hdg_level* fine, const hdg_level* coarse, const double* halves, const double* cross,
-                          int64_t nsets, hdg_transfer** out) {
+int hdg_transfer_create_h_window(const hdg_level* fine, const hdg_level* coarse, const double* halves,
+                                 const double* cross, int64_t nsets, int fine_row0, int coarse_row0,
+                                 hdg_transfer** out) {
   if (!fine || !coarse || !halves || !cross || !out) return fail(HDG_EINVAL, "null argument");
   if (fine->n1 != 2 || coarse->n1 != 2) return fail(HDG_EINVAL, "h-transfer runs at p = 1");
-  if (fine->nx != 2 * coarse->nx || fine->ny != 2 * coarse->ny)
-    return fail(HDG_EINVAL, "h-transfer needs the fine mesh = 2x the coarse mesh");
+  if (fine->nx != 2 * coarse->nx) return fail(HDG_EINVAL, "h-transfer needs nx_fine = 2 nx_coarse");
+  if (fine_row0 < 0 || coarse_row0 < 0) return fail(HDG_EINVAL, "negative window offset");
   const long long Ec = (long long)coarse->nx * coarse->ny;
   if (nsets != 1 && nsets != Ec) return fail(HDG_EINVAL, "cross maps: 1 shared set or one per coarse element");
   hdg_transfer* t = new hdg_transfer();
   t->is_h = true; t->fine = fine; t->coarse = coarse;
-  t->ha.nxc = coarse->nx; t->ha.nyc = coarse->ny;
+  t->ha.nxc = coarse->nx; t->ha.nyc = coarse->ny; t->ha.nyf = fine->ny;
+  t->ha.jf0 = fine_row0; t->ha.jc0 = coarse_row0;
   t->ha.nhf = fine->nh; t->ha.nhc = coarse->nh;
   std::memcpy(t->ha.halves, halves, sizeof(double) * 8);
   const size_t bytes = sizeof(double) * 64 * (size_t)nsets;
@@ -579,6 +581,13 @@ int hdg_transfer_create_h(const hdg_level* fine, const hdg_level* coarse, const 
   t->ha.shared_cross = (nsets == 1) ? 1 : 0;
   *out = t;
   return 0;
+}
+
+int hdg_transfer_create_h(const hdg_level* fine, const hdg_level* coarse, const double* halves, const double* cross,
+                          int64_t nsets, hdg_transfer** out) {
+  if (fine && coarse && fine->ny != 2 * coarse->ny)
+    return fail(HDG_EINVAL, "h-transfer needs the fine mesh = 2x the coarse mesh");
+  return hdg_transfer_create_h_window(fine, coarse, halves, cross, nsets, 0, 0, out);
 }
 
 int hdg_transfer_destroy(hdg_transfer* t) {

@@ -38,6 +38,9 @@ namespace hdg {
 #ifndef HDG_F_MAXN1
 #define HDG_F_MAXN1 13     // cap on the two-facets-per-thread rule (tuning knob)
 #endif
+#ifndef HDG_F3_MAXN1
+#define HDG_F3_MAXN1 0     // shared mode: three facets per thread up to this n1 (tuning knob)
+#endif
 #ifndef HDG_F_MAXN1_SHARED
 #define HDG_F_MAXN1_SHARED 9
 #endif
@@ -66,7 +69,8 @@ template <int N1, bool ST = false> struct Cfg {
   static constexpr int S = N1;                      // facet blocks contiguous in a staged run
   // facets per thread per orientation (measured: 2 pays up to p=8 when W is in the constant
   // bank, up to p=4 when W streams from HBM)
-  static constexpr int F = (N1 <= (ST ? 5 : HDG_F_MAXN1_SHARED)) && (N1 <= HDG_F_MAXN1) ? 2 : 1;
+  static constexpr int F = (N1 <= (ST ? 5 : HDG_F_MAXN1_SHARED)) && (N1 <= HDG_F_MAXN1)
+                               ? ((!ST && N1 <= HDG_F3_MAXN1) ? 3 : 2) : 1;
   static constexpr int TY = NWARP * F;              // tile height in elements
   static constexpr int WSZ = 7 * N1 * N1;           // merged facet operator entries
   static constexpr int DSZ = N1 * N1;               // block-Jacobi inverse entries
@@ -952,26 +956,33 @@ __global__ void p_restrict_kernel(const double* __restrict__ rf, double* __restr
 }
 
 // h-transfer at p = 1 (multigrid.py:229-298).  halves[h][k][c]; cross[set][cf][k][s*2+c]
+// Meshes may be row WINDOWS of the global fine / coarse meshes (multi-GPU strips): the fine
+// window has nyf rows starting at global row jf0, the coarse window nyc rows from jc0; on one
+// GPU jf0 = jc0 = 0 and nyf = 2 nyc.  Facets whose transfer needs data outside the windows are
+// left untouched (prolongation) or written as 0 (restriction): those are ghost facets, never owned.
 struct HArgs {
-  int nxc, nyc;           // coarse mesh
-  long long nhf, nhc;     // interior horizontal block counts (fine, coarse)
+  int nxc, nyc;           // coarse window (x: whole mesh)
+  int nyf;                // fine window rows
+  int jf0, jc0;           // global row of window row 0 (fine, coarse)
+  long long nhf, nhc;     // interior horizontal block counts of the windows
   double halves[8];
   const double* cross;    // device, (nsets, 4, 2, 8)
-  int shared_cross;       // 1 => one set for every coarse element
+  int shared_cross;       // 1 => one set for every coarse element (else one per window element)
 };
 
-__device__ __forceinline__ const double* hcross(const HArgs& h, int I, int J, int cf) {
-  const long long set = h.shared_cross ? 0 : ((long long)J * h.nxc + I);
+__device__ __forceinline__ const double* hcross(const HArgs& h, int I, int Jl, int cf) {
+  const long long set = h.shared_cross ? 0 : ((long long)Jl * h.nxc + I);
   return h.cross + (set * 4 + cf) * 16;
 }
 
-// coarse side value (2 doubles) of coarse element (I, J), side s; zero when Dirichlet
-__device__ __forceinline__ void coarse_side(const HArgs& h, const double* ec, int I, int J, int s, double* v) {
+// coarse side value (2 doubles) of coarse window element (I, Jl), side s; zero when the side is
+// a Dirichlet facet or outside the window
+__device__ __forceinline__ void coarse_side(const HArgs& h, const double* ec, int I, int Jl, int s, double* v) {
   long long blk = -1;
-  if (s == 0 && J >= 1) blk = (long long)(J - 1) * h.nxc + I;
-  if (s == 2 && J + 1 <= h.nyc - 1) blk = (long long)J * h.nxc + I;
-  if (s == 3 && I >= 1) blk = h.nhc + (long long)(I - 1) * h.nyc + J;
-  if (s == 1 && I + 1 <= h.nxc - 1) blk = h.nhc + (long long)I * h.nyc + J;
+  if (s == 0 && Jl >= 1) blk = (long long)(Jl - 1) * h.nxc + I;
+  if (s == 2 && Jl + 1 <= h.nyc - 1) blk = (long long)Jl * h.nxc + I;
+  if (s == 3 && I >= 1) blk = h.nhc + (long long)(I - 1) * h.nyc + Jl;
+  if (s == 1 && I + 1 <= h.nxc - 1) blk = h.nhc + (long long)I * h.nyc + Jl;
   if (blk >= 0) {
     const double2 e = __ldg(reinterpret_cast<const double2*>(ec) + blk);
     v[0] = e.x; v[1] = e.y;
@@ -980,38 +991,47 @@ __device__ __forceinline__ void coarse_side(const HArgs& h, const double* ec, in
   }
 }
 
-// fine facet t (n1 = 2, one double2 per facet) += its prolongation from the coarse level
+// fine window facet t (n1 = 2, one double2 per facet) += its prolongation from the coarse level
 __global__ void h_prolong_add_kernel(const HArgs h, const double* __restrict__ ec, double* __restrict__ xf) {
-  const int nxf = 2 * h.nxc, nyf = 2 * h.nyc;
+  const int nxf = 2 * h.nxc, nyf = h.nyf;
   const long long nvf = (long long)(nxf - 1) * nyf;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= h.nhf + nvf) return;
   double add[2] = {0.0, 0.0};
   bool half;
-  int I, J, hf, cf;
+  int I, Jl, hf, cf;
   long long cb = 0;
-  if (t < h.nhf) {  // fine h(i, j), block (j-1)*nxf + i
-    const int j = (int)(t / nxf) + 1, i = (int)(t % nxf);
+  if (t < h.nhf) {  // fine h(i, jl), block (jl-1)*nxf + i
+    const int jg = (int)(t / nxf) + 1 + h.jf0, i = (int)(t % nxf);
     I = i >> 1;
-    half = (j & 1) == 0;
-    if (half) { J = j >> 1; hf = i & 1; cb = (long long)(J - 1) * h.nxc + I; }
-    else { J = (j - 1) >> 1; cf = (i & 1) ? 3 : 2; }
-  } else {          // fine v(i, j), block nhf + (i-1)*nyf + j
+    half = (jg & 1) == 0;
+    if (half) {
+      Jl = (jg >> 1) - h.jc0;
+      if (Jl < 1 || Jl > h.nyc - 1) return;
+      hf = i & 1;
+      cb = (long long)(Jl - 1) * h.nxc + I;
+    } else {
+      Jl = ((jg - 1) >> 1) - h.jc0;
+      if (Jl < 0 || Jl >= h.nyc) return;
+      cf = (i & 1) ? 3 : 2;
+    }
+  } else {          // fine v(i, jl), block nhf + (i-1)*nyf + jl
     const long long u = t - h.nhf;
-    const int i = (int)(u / nyf) + 1, j = (int)(u % nyf);
-    J = j >> 1;
+    const int i = (int)(u / nyf) + 1, jg = (int)(u % nyf) + h.jf0;
+    Jl = (jg >> 1) - h.jc0;
+    if (Jl < 0 || Jl >= h.nyc) return;
     half = (i & 1) == 0;
-    if (half) { I = i >> 1; hf = j & 1; cb = h.nhc + (long long)(I - 1) * h.nyc + J; }
-    else { I = (i - 1) >> 1; cf = (j & 1) ? 1 : 0; }
+    if (half) { I = i >> 1; hf = jg & 1; cb = h.nhc + (long long)(I - 1) * h.nyc + Jl; }
+    else { I = (i - 1) >> 1; cf = (jg & 1) ? 1 : 0; }
   }
   if (half) {
     const double2 e = __ldg(reinterpret_cast<const double2*>(ec) + cb);
     for (int k = 0; k < 2; ++k) add[k] = h.halves[hf * 4 + k * 2] * e.x + h.halves[hf * 4 + k * 2 + 1] * e.y;
   } else {
-    const double* tm = hcross(h, I, J, cf);
+    const double* tm = hcross(h, I, Jl, cf);
     for (int s = 0; s < 4; ++s) {
       double v[2];
-      coarse_side(h, ec, I, J, s, v);
+      coarse_side(h, ec, I, Jl, s, v);
       for (int k = 0; k < 2; ++k) add[k] += __ldg(tm + k * 8 + s * 2) * v[0] + __ldg(tm + k * 8 + s * 2 + 1) * v[1];
     }
   }
@@ -1022,50 +1042,71 @@ __global__ void h_prolong_add_kernel(const HArgs h, const double* __restrict__ e
   *xp = x;
 }
 
-// contribution of coarse element (I, J)'s 4 cross facets to its side-s coarse dofs
-__device__ __forceinline__ void cross_restrict(const HArgs& h, const double* rf, int I, int J, int s, double* acc) {
-  const int nxf = 2 * h.nxc, nyf = 2 * h.nyc;
-  const long long cfb[4] = {
-      h.nhf + (long long)(2 * I + 1 - 1) * nyf + 2 * J,       // right of SW = v(2I+1, 2J)
-      h.nhf + (long long)(2 * I + 1 - 1) * nyf + 2 * J + 1,   // right of NW = v(2I+1, 2J+1)
-      (long long)(2 * J + 1 - 1) * nxf + 2 * I,               // top of SW   = h(2I, 2J+1)
-      (long long)(2 * J + 1 - 1) * nxf + 2 * I + 1};          // top of SE   = h(2I+1, 2J+1)
+// fine window blocks of h(i, jg) / v(i, jg) (global row jg), -1 when outside the window
+__device__ __forceinline__ long long fine_h(const HArgs& h, int i, int jg) {
+  const int jl = jg - h.jf0;
+  return (jl >= 1 && jl <= h.nyf - 1) ? (long long)(jl - 1) * (2 * h.nxc) + i : -1;
+}
+__device__ __forceinline__ long long fine_v(const HArgs& h, int i, int jg) {
+  const int jl = jg - h.jf0;
+  return (jl >= 0 && jl < h.nyf) ? h.nhf + (long long)(i - 1) * h.nyf + jl : -1;
+}
+
+// contribution of coarse element (I, Jl)'s 4 cross facets to its side-s coarse dofs
+__device__ __forceinline__ bool cross_restrict(const HArgs& h, const double* rf, int I, int Jl, int s, double* acc) {
+  const int J = Jl + h.jc0;
+  const long long cfb[4] = {fine_v(h, 2 * I + 1, 2 * J),       // right of SW = v(2I+1, 2J)
+                            fine_v(h, 2 * I + 1, 2 * J + 1),   // right of NW = v(2I+1, 2J+1)
+                            fine_h(h, 2 * I, 2 * J + 1),       // top of SW   = h(2I, 2J+1)
+                            fine_h(h, 2 * I + 1, 2 * J + 1)};  // top of SE   = h(2I+1, 2J+1)
+  if (cfb[0] < 0 || cfb[1] < 0 || cfb[2] < 0 || cfb[3] < 0 || Jl < 0 || Jl >= h.nyc) return false;
   for (int cf = 0; cf < 4; ++cf) {
-    const double* tm = hcross(h, I, J, cf);
+    const double* tm = hcross(h, I, Jl, cf);
     const double r0 = __ldg(rf + 2 * cfb[cf]), r1 = __ldg(rf + 2 * cfb[cf] + 1);
     for (int c = 0; c < 2; ++c) acc[c] += tm[0 * 8 + s * 2 + c] * r0 + tm[1 * 8 + s * 2 + c] * r1;
   }
+  return true;
 }
 
 __global__ void h_restrict_kernel(const HArgs h, const double* __restrict__ rf, double* __restrict__ rc) {
-  const int nxf = 2 * h.nxc, nyf = 2 * h.nyc;
   const long long nvc = (long long)(h.nxc - 1) * h.nyc;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= h.nhc + nvc) return;
   double acc[2] = {0.0, 0.0};
-  long long k0;
-  if (t < h.nhc) {  // coarse h(I, J)
-    const int J = (int)(t / h.nxc) + 1, I = (int)(t % h.nxc);
-    k0 = (long long)(2 * J - 1) * nxf + 2 * I;  // fine h(2I, 2J); +1 is h(2I+1, 2J)
-    for (int hf = 0; hf < 2; ++hf) {
-      const double r0 = __ldg(rf + 2 * (k0 + hf)), r1 = __ldg(rf + 2 * (k0 + hf) + 1);
-      for (int c = 0; c < 2; ++c) acc[c] += h.halves[hf * 4 + 0 * 2 + c] * r0 + h.halves[hf * 4 + 1 * 2 + c] * r1;
+  bool ok = true;
+  long long kf[2];
+  if (t < h.nhc) {  // coarse h(I, Jl)
+    const int Jl = (int)(t / h.nxc) + 1, I = (int)(t % h.nxc);
+    const int J = Jl + h.jc0;
+    kf[0] = fine_h(h, 2 * I, 2 * J);          // children: fine h(2I, 2J), h(2I+1, 2J)
+    kf[1] = fine_h(h, 2 * I + 1, 2 * J);
+    ok = kf[0] >= 0 && kf[1] >= 0;
+    if (ok) {
+      for (int hf = 0; hf < 2; ++hf) {
+        const double r0 = __ldg(rf + 2 * kf[hf]), r1 = __ldg(rf + 2 * kf[hf] + 1);
+        for (int c = 0; c < 2; ++c) acc[c] += h.halves[hf * 4 + 0 * 2 + c] * r0 + h.halves[hf * 4 + 1 * 2 + c] * r1;
+      }
+      ok = cross_restrict(h, rf, I, Jl - 1, 2, acc)   // element below: this facet is its TOP side
+           && cross_restrict(h, rf, I, Jl, 0, acc);   // element above: BOTTOM side
     }
-    cross_restrict(h, rf, I, J - 1, 2, acc);  // element below: this facet is its TOP side
-    cross_restrict(h, rf, I, J, 0, acc);      // element above: BOTTOM side
-  } else {          // coarse v(I, J)
+  } else {          // coarse v(I, Jl)
     const long long u = t - h.nhc;
-    const int I = (int)(u / h.nyc) + 1, J = (int)(u % h.nyc);
-    k0 = h.nhf + (long long)(2 * I - 1) * nyf + 2 * J;  // fine v(2I, 2J); +1 is v(2I, 2J+1)
-    for (int hf = 0; hf < 2; ++hf) {
-      const double r0 = __ldg(rf + 2 * (k0 + hf)), r1 = __ldg(rf + 2 * (k0 + hf) + 1);
-      for (int c = 0; c < 2; ++c) acc[c] += h.halves[hf * 4 + 0 * 2 + c] * r0 + h.halves[hf * 4 + 1 * 2 + c] * r1;
+    const int I = (int)(u / h.nyc) + 1, Jl = (int)(u % h.nyc);
+    const int J = Jl + h.jc0;
+    kf[0] = fine_v(h, 2 * I, 2 * J);          // children: fine v(2I, 2J), v(2I, 2J+1)
+    kf[1] = fine_v(h, 2 * I, 2 * J + 1);
+    ok = kf[0] >= 0 && kf[1] >= 0;
+    if (ok) {
+      for (int hf = 0; hf < 2; ++hf) {
+        const double r0 = __ldg(rf + 2 * kf[hf]), r1 = __ldg(rf + 2 * kf[hf] + 1);
+        for (int c = 0; c < 2; ++c) acc[c] += h.halves[hf * 4 + 0 * 2 + c] * r0 + h.halves[hf * 4 + 1 * 2 + c] * r1;
+      }
+      ok = cross_restrict(h, rf, I - 1, Jl, 1, acc)   // element left: RIGHT side
+           && cross_restrict(h, rf, I, Jl, 3, acc);   // element right: LEFT side
     }
-    cross_restrict(h, rf, I - 1, J, 1, acc);  // element left: RIGHT side
-    cross_restrict(h, rf, I, J, 3, acc);      // element right: LEFT side
   }
-  rc[2 * t] = acc[0];
-  rc[2 * t + 1] = acc[1];
+  rc[2 * t] = ok ? acc[0] : 0.0;
+  rc[2 * t + 1] = ok ? acc[1] : 0.0;
 }
 
 // ---------------------------------------------------------------------------- small kernels

@@ -35,10 +35,10 @@ def split_rows(ny, world, align=1):
 class StripLayout:
     """Index maps of one rank's strip (host, int64)."""
 
-    def __init__(self, nx, ny, p, world, rank, align=1):
+    def __init__(self, nx, ny, p, world, rank, align=1, rows=None):
         self.nx, self.ny, self.p, self.n1 = nx, ny, p, p + 1
         self.world, self.rank = world, rank
-        self.r0, self.r1 = split_rows(ny, world, align)[rank]
+        self.r0, self.r1 = rows if rows is not None else split_rows(ny, world, align)[rank]
         self.lo, self.hi = max(self.r0 - 2, 0), min(self.r1 + 1, ny)
         self.nyl = self.hi - self.lo
         n1 = self.n1
@@ -75,6 +75,14 @@ class StripLayout:
             self.recv_down = np.concatenate([self._h_row(self.r0 - 1), self._v_row(self.r0 - 1)])
         else:
             self.recv_down = np.zeros(0, np.int64)
+        # residual halo for the h-restriction: the coarse facets of this strip's bottom coarse row
+        # gather fine residuals of the two fine rows below it (cross facets, multigrid.py:276-281)
+        empty = np.zeros(0, np.int64)
+        self.rsend_up = np.concatenate([self._v_row(self.r1 - 2), self._v_row(self.r1 - 1),
+                                        self._h_row(self.r1 - 1)]) if rank < world - 1 else empty
+        self.rrecv_down = np.concatenate([self._v_row(self.r0 - 2), self._v_row(self.r0 - 1),
+                                          self._h_row(self.r0 - 1)]) if rank > 0 else empty
+        self.rsend_down = self.rrecv_up = empty
 
     def _h_row(self, j):
         """local dofs of h(0..nx-1, j) (empty on the Dirichlet rows j = 0, ny)."""
@@ -120,27 +128,29 @@ class StripOperator:
             self._idx[key] = self.torch.as_tensor(getattr(self.L, name), device=device)
         return self._idx[key]
 
-    def exchange(self, x):
-        """Refresh x's ghost rows from the neighbours (one send/recv pair per boundary)."""
+    def exchange(self, x, kind=""):
+        """Refresh x's ghost rows from the neighbours (one send/recv pair per boundary).
+        kind "" = operator halo (before an apply), "r" = residual halo (before an h-restriction)."""
         L, dist, torch = self.L, self.dist, self.torch
         if L.world == 1:
             return x
         ops, recvs = [], []
         dev = x.device
-        if L.rank > 0:
-            sd = x[self._index("send_down", dev)].contiguous()
-            rd = torch.empty(L.recv_down.size, dtype=x.dtype, device=dev)
-            ops += [dist.P2POp(dist.isend, sd, L.rank - 1, self.group),
-                    dist.P2POp(dist.irecv, rd, L.rank - 1, self.group)]
-            recvs.append(("recv_down", rd))
-        if L.rank < L.world - 1:
-            su = x[self._index("send_up", dev)].contiguous()
-            ru = torch.empty(L.recv_up.size, dtype=x.dtype, device=dev)
-            ops += [dist.P2POp(dist.isend, su, L.rank + 1, self.group),
-                    dist.P2POp(dist.irecv, ru, L.rank + 1, self.group)]
-            recvs.append(("recv_up", ru))
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        names = {"sd": kind + "send_down" if kind else "send_down", "rd": kind + "recv_down" if kind else "recv_down",
+                 "su": kind + "send_up" if kind else "send_up", "ru": kind + "recv_up" if kind else "recv_up"}
+        for peer, snd, rcv in ((L.rank - 1, names["sd"], names["rd"]), (L.rank + 1, names["su"], names["ru"])):
+            if not (0 <= peer < L.world):
+                continue
+            sidx, ridx = getattr(L, snd), getattr(L, rcv)
+            if sidx.size:
+                ops.append(dist.P2POp(dist.isend, x[self._index(snd, dev)].contiguous(), peer, self.group))
+            if ridx.size:
+                buf = torch.empty(ridx.size, dtype=x.dtype, device=dev)
+                ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+                recvs.append((rcv, buf))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
         for name, buf in recvs:
             x[self._index(name, dev)] = buf
         return x
@@ -162,3 +172,116 @@ class StripOperator:
         if key not in self._idx:
             self._idx[key] = self.torch.as_tensor(self.L.owned.astype(np.float64), device=device, dtype=dtype)
         return self._idx[key]
+
+
+# ------------------------------------------------------------------------ distributed V-cycle
+
+
+def plan_strips(shapes, world, min_rows=4):
+    """shapes: [(nx, ny, p, link_to_next)] of a hierarchy (link "p" / "h" / None).  Returns
+    (d, rows): levels 0..d are strip-distributed (>= min_rows element rows per rank), levels
+    d+1.. run replicated on every rank (agglomeration); rows[l] = (r0, r1) of this
+    partition for every distributed level l and for level d+1 (the restriction target)."""
+    d = -1
+    for l, (nx, ny, p, link) in enumerate(shapes[:-1]):
+        if ny // world >= min_rows:
+            d = l
+        else:
+            break
+    if d < 0:
+        return -1, []
+    base = shapes[d + 1][1]
+    parts = split_rows(base, world)
+    rows = []
+    for l in range(d + 2):
+        f = shapes[l][1] // base
+        rows.append([(r0 * f, r1 * f) for r0, r1 in parts])
+    return d, rows
+
+
+class StripMG:
+    """Multiplicative V/W cycle (multigrid.py:393-406) on strip-partitioned levels.
+
+    Per distributed level: operator-halo exchange before every block-Jacobi sweep and residual,
+    residual-halo exchange before an h-restriction, operator-halo exchange of the coarse
+    correction before the prolongation; p-transfers are facet-local.  Below level d the
+    restricted residual is all-gathered and the remaining levels run replicated.  The local
+    operations come from `backend` (GPU: the sm_100a kernels on row windows; tests: CSR
+    restrictions of the oracle), so the orchestration here is device-agnostic."""
+
+    def __init__(self, backend, layouts, d, group=None):
+        import torch
+        import torch.distributed as dist
+        self.B, self.layouts, self.d = backend, layouts, d
+        self.ops = [StripOperator(L, None, group) for L in layouts]
+        self.torch, self.dist, self.group = torch, dist, group
+
+    def _gather_owned(self, l, v):
+        """assemble the global vector of level l from every rank's owned values"""
+        torch, dist = self.torch, self.dist
+        L = self.layouts[l]
+        loc, glob = L.owned_pairs()
+        vals = v[torch.as_tensor(loc, device=v.device)]
+        idx = torch.as_tensor(glob, device=v.device)
+        if L.world == 1:
+            out = torch.zeros(L.ndof_g, dtype=v.dtype, device=v.device)
+            out[idx] = vals
+            return out
+        n = torch.tensor([vals.numel()], device=v.device)
+        sizes = [torch.zeros_like(n) for _ in range(L.world)]
+        dist.all_gather(sizes, n, group=self.group)
+        m = int(max(s.item() for s in sizes))
+        pv = torch.zeros(m, dtype=v.dtype, device=v.device)
+        pi = torch.full((m,), -1, dtype=torch.int64, device=v.device)
+        pv[:vals.numel()] = vals
+        pi[:idx.numel()] = idx
+        allv = [torch.empty_like(pv) for _ in range(L.world)]
+        alli = [torch.empty_like(pi) for _ in range(L.world)]
+        dist.all_gather(allv, pv, group=self.group)
+        dist.all_gather(alli, pi, group=self.group)
+        out = torch.zeros(L.ndof_g, dtype=v.dtype, device=v.device)
+        for vv, ii in zip(allv, alli):
+            k = ii >= 0
+            out[ii[k]] = vv[k]
+        return out
+
+    def cycle(self, l, b, x, zero_init, nu1, nu2, visits):
+        B = self.B
+        op = self.ops[l]
+        if zero_init:
+            x = B.bj_zero(l, b, 1, nu1) if nu1 >= 1 else self.torch.zeros_like(b)
+            start = 1 if nu1 >= 1 else 0
+        else:
+            start = 0
+        for k in range(start, nu1):
+            op.exchange(x)
+            x = B.bj_sweep(l, b, x, k + 1, nu1)
+        op.exchange(x)
+        if B.link(l) == "p":
+            bc = B.residual_restrict_p(l, b, x)
+        else:
+            r = B.residual(l, b, x)
+            op.exchange(r, "r")
+            bc = B.restrict_h(l, r)
+        if l + 1 <= self.d:
+            xc = None
+            for v in range(visits):
+                xc = self.cycle(l + 1, bc, xc, v == 0, nu1, nu2, visits)
+            self.ops[l + 1].exchange(xc)
+        else:
+            bg = self._gather_owned(l + 1, bc)
+            xg = None
+            for v in range(visits):
+                xg = B.global_cycle(bg, xg, nu1, nu2, visits)
+            xc = xg[self.torch.as_tensor(self.layouts[l + 1].local_to_global, device=xg.device)]
+        x = B.prolong_add(l, xc, x)
+        for k in range(nu2):
+            op.exchange(x)
+            x = B.bj_sweep(l, b, x, k + 1, nu2)
+        return x
+
+    def v_cycle(self, b, x0=None, nu1=2, nu2=2, visits=1):
+        """one cycle on the strip of level 0 (b, x0: this rank's local window vectors)"""
+        if x0 is None:
+            return self.cycle(0, b, None, True, nu1, nu2, visits)
+        return self.cycle(0, b, x0.clone(), False, nu1, nu2, visits)

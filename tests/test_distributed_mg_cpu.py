@@ -1,0 +1,114 @@
+"""Strip-partitioned V-cycle on CPU: world 2 and 3 over gloo.  The per-window
+operations are CSR restrictions of the oracle's global level operators, so this checks the
+distributed orchestration (operator and residual halos, h-restriction across strips,
+agglomeration of the coarse levels) against the oracle's global V-cycle."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch.multiprocessing as mp
+
+import specs
+from oracle import hdg_oracle as O
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+class OracleWindowBackend:
+    """Window ops from the oracle's global CSR operators (A, D^-1, P) restricted to rows/cols of
+    each rank's local window."""
+
+    def __init__(self, levels, layouts, d, omega=0.8):
+        import torch
+        self.t, self.levels, self.layouts, self.d, self.w = torch, levels, layouts, d, omega
+        self.A, self.Dinv, self.P = [], [], []
+        for l in range(d + 1):
+            loc = layouts[l].local_to_global
+            A = levels[l].operator.tocsr()
+            self.A.append(A[loc][:, loc])
+            sm = levels[l].smoother
+            n1 = levels[l].p + 1
+            blocks = loc.reshape(-1, n1)[:, 0] // n1
+            self.Dinv.append(sp.block_diag(list(sm.Dinv[blocks])).tocsr())
+            locc = layouts[l + 1].local_to_global
+            self.P.append(levels[l].prolong.tocsr()[loc][:, locc])
+
+    def _T(self, a):
+        return self.t.from_numpy(np.ascontiguousarray(a))
+
+    def link(self, l):
+        return "p" if self.levels[l + 1].grid.n_x == self.levels[l].grid.n_x else "h"
+
+    def bj_zero(self, l, b, k, steps):
+        return self._T(self.w * (self.Dinv[l] @ b.numpy()))
+
+    def bj_sweep(self, l, b, x, k, steps):
+        xn = x.numpy()
+        return self._T(xn + self.w * (self.Dinv[l] @ (b.numpy() - self.A[l] @ xn)))
+
+    def residual(self, l, b, x):
+        return self._T(b.numpy() - self.A[l] @ x.numpy())
+
+    def residual_restrict_p(self, l, b, x):
+        return self._T(self.P[l].T @ (b.numpy() - self.A[l] @ x.numpy()))
+
+    def restrict_h(self, l, r):
+        return self._T(self.P[l].T @ r.numpy())
+
+    def prolong_add(self, l, ec, x):
+        return self._T(x.numpy() + self.P[l] @ ec.numpy())
+
+    def global_cycle(self, bg, xg, nu1, nu2, visits):
+        sub = self.levels[self.d + 1:]
+        bgn = bg.numpy()
+        x0 = np.zeros_like(bgn) if xg is None else xg.numpy()
+        return self._T(O.cycle(sub, 0, bgn, x0, nu1, nu2, visits))
+
+
+def _worker(rank, world, port, n, p, visits, out):
+    import torch
+    import torch.distributed as dist
+    from paper_1705_09907_b200.distributed import StripLayout, StripMG, plan_strips
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        levels = O.build_levels(O.Grid(n, n), p, specs.manufactured(O.Spec), smoother="blockjacobi")
+        shapes = [(l.grid.n_x, l.grid.n_y, l.p, None) for l in levels]
+        d, rows = plan_strips(shapes, world)
+        assert d >= 1
+        layouts = [StripLayout(shapes[l][0], shapes[l][1], shapes[l][2], world, rank, rows=rows[l][rank])
+                   for l in range(d + 2)]
+        mg = StripMG(OracleWindowBackend(levels, layouts, d), layouts, d)
+        b = levels[0].rhs
+        bl = torch.from_numpy(b[layouts[0].local_to_global].copy())
+        x = mg.v_cycle(bl, None, 2, 2, visits)
+        li, gi = layouts[0].owned_pairs()
+        out[rank] = (gi, x.numpy()[li], d)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,p,visits", [(2, 16, 2, 1), (3, 24, 2, 1), (2, 16, 3, 2)])
+def test_strip_vcycle_matches_global(world, n, p, visits):
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_worker, args=(world, _free_port(), n, p, visits, out), nprocs=world, join=True)
+        res = dict(out)
+    levels = O.build_levels(O.Grid(n, n), p, specs.manufactured(O.Spec), smoother="blockjacobi")
+    b = levels[0].rhs
+    ref = O.cycle(levels, 0, b, np.zeros_like(b), 2, 2, visits)
+    x = np.full(ref.size, np.nan)
+    for g in range(world):
+        gi, vals, d = res[g]
+        x[gi] = vals
+    assert np.isfinite(x).all()
+    assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()
