@@ -285,3 +285,117 @@ class StripMG:
         if x0 is None:
             return self.cycle(0, b, None, True, nu1, nu2, visits)
         return self.cycle(0, b, x0.clone(), False, nu1, nu2, visits)
+
+
+class DeviceStripBackend:
+    """StripMG's local operations on this rank's row windows, all in the sm_100a kernels.
+
+    Window level l is the reference-layout trace operator of element rows [lo, hi) of level l
+    (its element classes sliced from the global level), so hdg_bj_sweep / hdg_residual apply
+    unchanged: every window facet has both of its elements inside the window.  p-links use
+    hdg_transfer_create_p on the two windows (facet-local); h-links use
+    hdg_transfer_create_h_window with the windows' global row offsets, whose kernels drop
+    contributions from outside the window (only ghost facets are affected).  Levels d+1.. run
+    replicated through the single-GPU device cycle (hdg_mg_cycle)."""
+
+    def __init__(self, levels, layouts, d, omega=0.8):
+        import ctypes
+
+        import torch
+        from . import _device as dev
+        from ._lib import check, lib
+        from .mesh import build_cartesian
+        from .multigrid import BlockJacobiSmoother, Prolongation
+        from .trace import BlockOperator
+        self.torch, self.dev, self.lib, self.check, self.ct = torch, dev, lib, check, ctypes
+        self.levels, self.layouts, self.d, self.omega = levels, layouts, d, float(omega)
+        self.ops, self.links, self.transfers, self._own = [], [], [], []
+        for l in range(d + 2):
+            L, g = layouts[l], levels[l].block_op
+            nx = L.nx
+            ec = g.elem_class[L.lo * nx:L.hi * nx]
+            op = BlockOperator(build_cartesian(nx, L.nyl), L.p, g.S_cls, ec)
+            if l <= d:
+                op.set_blockjacobi(self.omega)
+            self.ops.append(op)
+        for l in range(d + 1):
+            P = levels[l].prolong
+            if P.kind == "p":
+                self.links.append("p")
+                self.transfers.append(Prolongation(self.ops[l], self.ops[l + 1], "p", V=P.V))
+            else:
+                self.links.append("h")
+                Lc = layouts[l + 1]
+                cross = np.ascontiguousarray(P.cross)
+                if cross.shape[0] != 1:
+                    cross = np.ascontiguousarray(cross[Lc.lo * Lc.nx:Lc.hi * Lc.nx])
+                hv = np.ascontiguousarray(P.halves)
+                h = ctypes.c_void_p()
+                check(lib.hdg_transfer_create_h_window(self.ops[l].handle, self.ops[l + 1].handle, hv.ctypes.data,
+                                                       cross.ctypes.data, cross.shape[0], layouts[l].lo, Lc.lo,
+                                                       ctypes.byref(h)))
+                t = Prolongation(self.ops[l], self.ops[l + 1], "h", halves=hv, cross=cross)
+                t._handle = h
+                self.transfers.append(t)
+        self.sub = levels[d + 1:]
+        for lev in self.sub[:-1]:
+            if not isinstance(lev.smoother, BlockJacobiSmoother) or lev.smoother.omega != self.omega:
+                lev.smoother = BlockJacobiSmoother(lev.block_op, self.omega)
+        self._zero = {}
+
+    def _empty(self, l):
+        return self.dev.empty(self.ops[l].ndof)
+
+    def link(self, l):
+        return self.links[l]
+
+    def bj_sweep(self, l, b, x, k, steps):
+        out = self._empty(l)
+        dev = self.dev
+        self.check(self.lib.hdg_bj_sweep(self.ops[l].handle, dev.ptr(b), dev.ptr(x), dev.ptr(out), dev.stream()))
+        return out
+
+    def bj_zero(self, l, b, k, steps):
+        if l not in self._zero:
+            self._zero[l] = self.dev.zeros(self.ops[l].ndof)
+        return self.bj_sweep(l, b, self._zero[l], k, steps)
+
+    def residual(self, l, b, x):
+        r = self._empty(l)
+        dev = self.dev
+        self.check(self.lib.hdg_residual(self.ops[l].handle, dev.ptr(b), dev.ptr(x), dev.ptr(r), None, dev.stream()))
+        return r
+
+    def restrict_h(self, l, r):
+        out = self._empty(l + 1)
+        dev = self.dev
+        self.check(self.lib.hdg_restrict(self.transfers[l].handle, dev.ptr(r), dev.ptr(out), dev.stream()))
+        return out
+
+    def residual_restrict_p(self, l, b, x):
+        return self.restrict_h(l, self.residual(l, b, x))
+
+    def prolong_add(self, l, ec, x):
+        dev = self.dev
+        self.check(self.lib.hdg_prolong_add(self.transfers[l].handle, dev.ptr(ec), dev.ptr(x), dev.stream()))
+        return x
+
+    def global_cycle(self, bg, xg, nu1, nu2, visits):
+        from .multigrid import _run_cycle
+        return _run_cycle(self.sub, bg, xg, nu1, nu2, visits)
+
+
+def strip_multigrid(levels, world=None, rank=None, group=None, omega=0.8, min_rows=4):
+    """StripMG over a hierarchy from build_hierarchy(..., smoother=None): levels whose strips
+    keep >= min_rows element rows per rank are distributed, the rest replicated."""
+    import torch.distributed as dist
+    if world is None:
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+    shapes = [(lev.mesh.n_x, lev.mesh.n_y, lev.p, None) for lev in levels]
+    d, rows = plan_strips(shapes, world, min_rows)
+    if d < 0:
+        raise ValueError("mesh too small to distribute")
+    layouts = [StripLayout(shapes[l][0], shapes[l][1], shapes[l][2], world, rank, rows=rows[l][rank])
+               for l in range(d + 2)]
+    return StripMG(DeviceStripBackend(levels, layouts, d, omega), layouts, d, group)

@@ -26,3 +26,19 @@ def golden():
 TESTS = os.path.dirname(os.path.abspath(__file__))
 if TESTS not in sys.path:
     sys.path.insert(0, TESTS)
+
+
+@pytest.fixture(scope="session")
+def P():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_1705_09907_b200.multigrid as mg
+    import paper_1705_09907_b200.problem as pb
+    import paper_1705_09907_b200.trace as tr
+    from paper_1705_09907_b200.mesh import build_cartesian
+
+    class NS:
+        pass
+    ns = NS()
+    ns.mg, ns.pb, ns.tr, ns.mesh = mg, pb, tr, build_cartesian
+    return ns

@@ -18,20 +18,6 @@ def rel(a, b):
     return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
 
 
-@pytest.fixture(scope="module")
-def P():
-    import torch
-    assert torch.cuda.is_available()
-    import paper_1705_09907_b200.multigrid as mg
-    import paper_1705_09907_b200.problem as pb
-    import paper_1705_09907_b200.trace as tr
-    from paper_1705_09907_b200.mesh import build_cartesian
-
-    class NS:
-        pass
-    ns = NS()
-    ns.mg, ns.pb, ns.tr, ns.mesh = mg, pb, tr, build_cartesian
-    return ns
 
 
 # ------------------------------------------------------------------------------ matvec
