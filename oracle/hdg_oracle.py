@@ -317,6 +317,7 @@ class OracleTrace:
 
     def __init__(self, grid, p, spec, tau_per_facet=None, *, _blocks=None):
         self.mesh = self.grid = grid
+        self.spec = spec
         self.p, self.n1 = p, p + 1
         self.core = ElementCore(grid, p)
         self.interior = grid.interior
@@ -419,6 +420,40 @@ def reconstruct_all(system, lam):
         sol = lu_solve(l.lu, l.load - l.trace_cols @ xe[e])
         q[e], u[e] = sol[:2 * nb], sol[2 * nb:]
     return q, u
+
+
+def postprocess_all(system, q, u):
+    """trace.py:180-185 / local.py:254-299: superconvergent potential of order p+1 per element,
+    a local Neumann problem (grad u*, grad w) = -(K^-1 q_h, grad w) with the element mean of u*
+    pinned to that of u_h (KKT system, LU-solved).  A (Kxx, Kyy) pair divides each flux
+    component by its own coefficient (builder extension)."""
+    g, p = system.grid, system.p
+    ref_p, ref = RefElem(p), RefElem(p + 1)
+    nb, nb2 = (p + 1) ** 2, (p + 2) ** 2
+    cross = lagrange_at(ref_p.basis, ref.quad.nodes)
+    interp = np.kron(cross, cross)
+    w2 = ref.w2
+    stiff = (g.dy / g.dx) * ref.Dxi.T @ (w2[:, None] * ref.Dxi) \
+        + (g.dx / g.dy) * ref.Deta.T @ (w2[:, None] * ref.Deta)
+    jac = g.dx * g.dy / 4.0
+    mean_row = jac * (ref.I2.T @ w2)
+    kkt = np.zeros((nb2 + 1, nb2 + 1))
+    kkt[:nb2, :nb2] = stiff
+    kkt[:nb2, nb2] = mean_row
+    kkt[nb2, :nb2] = mean_row
+    lu = lu_factor(kkt)
+    out = np.empty((g.n_elems, nb2))
+    for e in range(g.n_elems):
+        qx, qy = ref.quad_xy(*g.origin(e), g.dx, g.dy)
+        kq = system.spec.coefficient(qx, qy)
+        kx, ky = (kq if isinstance(kq, tuple) else (kq, kq))
+        qh_x = interp @ q[e, :nb]
+        qh_y = interp @ q[e, nb:]
+        rhs = -0.5 * g.dy * ref.Dxi.T @ (w2 * qh_x / np.asarray(kx, float))
+        rhs += -0.5 * g.dx * ref.Deta.T @ (w2 * qh_y / np.asarray(ky, float))
+        mean_u = jac * w2 @ (interp @ u[e])
+        out[e] = lu_solve(lu, np.concatenate([rhs, [mean_u]]))[:-1]
+    return out
 
 
 def exact_trace(system, func):

@@ -247,6 +247,8 @@ class PiecewiseCondenser:
         self.C0d = [Fq[:, d * nb:(d + 1) * nb] @ Mi @ B[d].T for d in range(2)]
         self.BMid = [B[d] @ Mi for d in range(2)]
         self.FqMid = [Fq[:, d * nb:(d + 1) * nb] @ Mi for d in range(2)]
+        self.MiBt = [Mi @ B[d].T for d in range(2)]
+        self.Mi, self.Tq = Mi, Tq
         self.stab, self.Tu, self.Fu, self.Ms = stab, Tu, Fu, Ms
 
     def _dev(self):
@@ -255,7 +257,9 @@ class PiecewiseCondenser:
             T = {}
             for k in ("stab", "Tu", "Fu", "Ms"):
                 T[k] = torch.as_tensor(getattr(self, k), device="cuda")
-            for k in ("Lapd", "Gd", "A0d", "C0d", "BMid", "FqMid"):
+            for k in ("Mi", "Tq"):
+                T[k] = torch.as_tensor(getattr(self, k), device="cuda")
+            for k in ("Lapd", "Gd", "A0d", "C0d", "BMid", "FqMid", "MiBt"):
                 T[k] = [torch.as_tensor(m, device="cuda") for m in getattr(self, k)]
             self._t = T
         return self._t
@@ -286,6 +290,31 @@ class PiecewiseCondenser:
                                      for d in range(2)) + u @ t["Fu"].T
         return out.cpu().numpy()
 
+    def reconstruct(self, K, load, lam_e, chunk=1 << 16):
+        """(q, u) of every element from its trace values (local.py:240-251) by the same
+        elimination: f = load - T lam_e, (Stab + sum_d K_d Lap_d) u = f_u - sum_d K_d B_d M^-1 f_q,d,
+        q_d = K_d M^-1 (f_q,d + B_d^T u).  load (E, 3nb), lam_e (E, 4n1) CUDA tensors."""
+        import torch
+        t = self._dev()
+        kx, ky = (torch.as_tensor(k, device="cuda") for k in self._pair(K))
+        nb, E = self.nb, kx.numel()
+        q = torch.empty((E, 2 * nb), dtype=torch.float64, device="cuda")
+        u = torch.empty((E, nb), dtype=torch.float64, device="cuda")
+        for s0 in range(0, E, chunk):
+            sl = slice(s0, min(E, s0 + chunk))
+            k = (kx[sl][:, None], ky[sl][:, None])
+            lam = lam_e[sl]
+            fq = load[sl, :2 * nb] - lam @ t["Tq"].T
+            fu = load[sl, 2 * nb:] - lam @ t["Tu"].T
+            f = (fq[:, :nb], fq[:, nb:])
+            H = t["stab"] + sum(k[d][:, :, None] * t["Lapd"][d] for d in range(2))
+            rhs = fu - sum(k[d] * (f[d] @ t["BMid"][d].T) for d in range(2))
+            uu = torch.linalg.solve(H, rhs[:, :, None])[:, :, 0]
+            u[sl] = uu
+            for d in range(2):
+                q[sl, d * nb:(d + 1) * nb] = k[d] * (f[d] @ t["Mi"].T + uu @ t["MiBt"][d].T)
+        return q, u
+
     def blocks(self, K, chunk=1 << 15):
         """S for every element; K: (E,) isotropic or a (Kxx, Kyy) pair of (E,) arrays."""
         import torch
@@ -300,6 +329,34 @@ class PiecewiseCondenser:
             out[s0:s0 + chunk] = sum(k[d] * t["A0d"][d] for d in range(2)) + t["Ms"] + \
                 (sum(k[d] * t["C0d"][d] for d in range(2)) + t["Fu"]) @ U
         return out
+
+
+class UnsupportedOrder(ValueError):
+    """local.py:31."""
+
+
+class PostprocessOps:
+    """Shared data of the order-raising local Neumann solve p -> p+1 (local.py:254-279):
+    order-p basis at the order-(p+1) GL points, stiffness, mean constraint, KKT matrix."""
+
+    def __init__(self, p, dx, dy):
+        if p < 1:
+            raise UnsupportedOrder("postprocessing needs p >= 1")
+        lo, ref = ref_element(p), ref_element(p + 1)
+        self.p, self.ref, self.nb = p, ref, ref.nb
+        cross = eval_matrix(lo.basis, ref.quad.nodes)
+        self.interp_from_p = np.kron(cross, cross)
+        self.w2 = ref.w2
+        self.dxi2, self.deta2 = ref.dxi_2d, ref.deta_2d
+        self.stiff = (dy / dx) * self.dxi2.T @ (self.w2[:, None] * self.dxi2) \
+            + (dx / dy) * self.deta2.T @ (self.w2[:, None] * self.deta2)
+        self.jac = dx * dy / 4.0
+        self.mean_row = self.jac * (ref.interp_2d.T @ self.w2)
+        n = self.nb
+        self.kkt = np.zeros((n + 1, n + 1))
+        self.kkt[:n, :n] = self.stiff
+        self.kkt[:n, n] = self.mean_row
+        self.kkt[n, :n] = self.mean_row
 
 
 def classify_rows(rows):

@@ -16,7 +16,8 @@ import scipy.sparse as sp
 
 from . import _device as dev
 from ._lib import check, lib
-from .discretization import ElementClasses, NumericalBreakdown, PiecewiseCondenser, classify_rows, ref_element
+from .discretization import (ElementClasses, NumericalBreakdown, PiecewiseCondenser, PostprocessOps,  # noqa: F401
+                             UnsupportedOrder, classify_rows, ref_element)
 
 
 class LocalOps:
@@ -403,29 +404,86 @@ class TraceSystem:
 
     def reconstruct_all(self, lam):
         """trace.py:171-178 / local.py:240-251: volume (q, u) on every element from the trace
-        solution, as two batched device GEMMs per element class: sol = L^-1 (load - T lam_e)."""
+        solution, batched on the device: sol = L^-1 (load - T lam_e) per element class (two
+        GEMMs), or the flux-first elimination per element for GPU-condensed media.  numpy in ->
+        numpy out; a CUDA tensor in -> CUDA tensors out."""
         import torch
-        if self.classes is None:
-            raise NotImplementedError("reconstruction of GPU-condensed media: use the host class path")
-        nb = self.ops.nb
+        nb, n1 = self.ops.nb, self.ops.n1
         E = self.mesh.n_x * self.mesh.n_y
-        lam = lam.cpu().numpy() if hasattr(lam, "cpu") else np.asarray(lam, float)
-        lam_e = self.layout.gather(lam) if self.ndof else np.zeros((E, 4 * self.ops.n1))
-        load = np.zeros((E, 3 * nb))
+        lam_d, was_np = dev.to_device(lam)
+        if lam_d.numel() != self.ndof:
+            raise ValueError(f"expected {self.ndof} trace values, got {lam_d.numel()}")
+        lam_e = self._gather_device(lam_d)
+        load = torch.zeros((E, 3 * nb), dtype=torch.float64, device="cuda")
         for idx, ld in self._element_loads(self.spec):
-            load[idx] += ld
-        Linv = np.linalg.inv(self.classes.L)
-        dev = "cuda"
-        rhs = torch.as_tensor(load, device=dev) - torch.einsum(
-            "eij,ej->ei", torch.as_tensor(self.classes.T[self.elem_class], device=dev),
-            torch.as_tensor(lam_e, device=dev)) if self.classes.n > 1 else \
-            torch.as_tensor(load, device=dev) - torch.as_tensor(lam_e, device=dev) @ torch.as_tensor(self.classes.T[0].T, device=dev)
+            load[torch.as_tensor(idx, device="cuda")] += torch.as_tensor(ld, device="cuda")
+        if self.piecewise is not None:
+            q, u = self.piecewise.reconstruct(self.class_K, load, lam_e)
+            return dev.back(q, was_np), dev.back(u, was_np)
+        if self.classes is None:
+            raise NotImplementedError("reconstruction needs the element classes (from_blocks system)")
+        Linv = torch.as_tensor(np.linalg.inv(self.classes.L), device="cuda")
+        T = torch.as_tensor(self.classes.T, device="cuda")
         if self.classes.n == 1:
-            sol = rhs @ torch.as_tensor(Linv[0].T, device=dev)
+            sol = (load - lam_e @ T[0].T) @ Linv[0].T
         else:
-            sol = torch.einsum("eij,ej->ei", torch.as_tensor(Linv[self.elem_class], device=dev), rhs)
-        sol = sol.cpu().numpy()
-        return sol[:, :2 * nb], sol[:, 2 * nb:]
+            cls = torch.as_tensor(self.elem_class, device="cuda")
+            sol = torch.empty_like(load)
+            for s0 in range(0, E, 1 << 16):
+                c = cls[s0:s0 + (1 << 16)]
+                rhs = load[s0:s0 + (1 << 16)] - torch.einsum("eij,ej->ei", T[c], lam_e[s0:s0 + (1 << 16)])
+                sol[s0:s0 + (1 << 16)] = torch.einsum("eij,ej->ei", Linv[c], rhs)
+        return dev.back(sol[:, :2 * nb].contiguous(), was_np), dev.back(sol[:, 2 * nb:].contiguous(), was_np)
+
+    def _gather_device(self, lam_d):
+        """(E, 4n1) element trace values, 0 on Dirichlet sides (trace.py:81-85), on the device:
+        the TraceLayout.gather arithmetic on torch views."""
+        import torch
+        lay = self.layout
+        n1, nx, ny = lay.n1, lay.nx, lay.ny
+        H = torch.zeros((ny + 1, nx, n1), dtype=torch.float64, device="cuda")
+        V = torch.zeros((nx + 1, ny, n1), dtype=torch.float64, device="cuda")
+        if self.ndof:
+            H[1:ny] = lam_d[:lay.nh * n1].reshape(ny - 1, nx, n1)
+            V[1:nx] = lam_d[lay.nh * n1:].reshape(nx - 1, ny, n1)
+        return torch.stack([H[:-1], V[1:].transpose(0, 1), H[1:], V[:-1].transpose(0, 1)],
+                           dim=2).reshape(nx * ny, 4 * n1)
+
+    def postprocess_all(self, q, u, chunk=1 << 16):
+        """trace.py:180-185 / local.py:282-299: superconvergent order-(p+1) potential per element,
+        batched on the device: order-raising interpolation and the K^-1 weighted flux load as
+        GEMMs, then one LU-factored KKT solve for all elements at once (E right-hand sides).
+        A (Kxx, Kyy) coefficient divides each flux component by its own K."""
+        import torch
+        m = self.mesh
+        pops = PostprocessOps(self.p, m.dx, m.dy)
+        qd, was_np = dev.to_device(q)
+        ud, _ = dev.to_device(u)
+        nb = self.ops.nb
+        E = m.n_x * m.n_y
+        qd, ud = qd.reshape(E, 2 * nb), ud.reshape(E, nb)
+        T = {k: torch.as_tensor(getattr(pops, k), device="cuda")
+             for k in ("interp_from_p", "w2", "dxi2", "deta2")}
+        lu, piv = torch.linalg.lu_factor(torch.as_tensor(pops.kkt, device="cuda"))
+        out = torch.empty((E, pops.nb), dtype=torch.float64, device="cuda")
+        ref = pops.ref
+        for e0 in range(0, E, chunk):
+            e1 = min(E, e0 + chunk)
+            e = np.arange(e0, e1)
+            qx, qy = ref.element_quad_points(m.x0 + (e % m.n_x) * m.dx, m.y0 + (e // m.n_x) * m.dy, m.dx, m.dy)
+            kq = self.spec.coefficient(qx, qy)
+            aniso = isinstance(kq, tuple)
+            kx_h, ky_h = kq if aniso else (kq, kq)
+            kx = torch.as_tensor(np.asarray(kx_h, float).reshape(qx.shape), device="cuda")
+            ky = torch.as_tensor(np.asarray(ky_h, float).reshape(qx.shape), device="cuda") if aniso else kx
+            qh_x = qd[e0:e1, :nb] @ T["interp_from_p"].T
+            qh_y = qd[e0:e1, nb:] @ T["interp_from_p"].T
+            rhs = (-0.5 * m.dy) * ((T["w2"] * qh_x / kx) @ T["dxi2"]) \
+                + (-0.5 * m.dx) * ((T["w2"] * qh_y / ky) @ T["deta2"])
+            mean_u = pops.jac * ((ud[e0:e1] @ T["interp_from_p"].T) @ T["w2"])
+            B = torch.cat([rhs, mean_u[:, None]], dim=1).T.contiguous()
+            out[e0:e1] = torch.linalg.lu_solve(lu, piv, B).T[:, :-1]
+        return dev.back(out, was_np)
 
     # -- reference attributes -----------------------------------------------------------------
     @property

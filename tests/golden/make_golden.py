@@ -175,6 +175,19 @@ def hierarchies():
     save("hierarchies.npz", **out)
 
 
+def postprocessing():
+    """reconstruct_all (trace.py:171-178) and postprocess_all (:180-185) of random traces."""
+    out = {}
+    for tag, spec, n, p in [("m4p2", manufactured_problem(), 4, 2), ("m5p3", manufactured_problem(), 5, 3),
+                            ("m6p1", manufactured_problem(), 6, 1), ("kI4p4", constant_problem(0.0, 1.0), 4, 4)]:
+        s = TraceSystem(build_cartesian(n, n), p, spec)
+        lam = np.random.default_rng(7 * n + p).standard_normal(s.ndof)
+        q, u = s.reconstruct_all(lam)
+        out[f"{tag}_lam"], out[f"{tag}_q"], out[f"{tag}_u"] = lam, q, u
+        out[f"{tag}_ustar"] = s.postprocess_all(q, u)
+    save("postprocess.npz", **out)
+
+
 def config1():
     """BASELINE configs[0]: 64x64, p=2, K=1, g_D=0, nodal f ~ U[-1,1] (seed 0);
     one matvec + one V(2,2) BJ(0.8) cycle on levels[:6] (down to 4x4); full solve."""
@@ -197,10 +210,12 @@ def config1():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["small", "hier", "cfg1"]
+    which = sys.argv[1:] or ["small", "hier", "cfg1", "post"]
     if "small" in which:
         small_systems()
     if "hier" in which:
         hierarchies()
     if "cfg1" in which:
         config1()
+    if "post" in which:
+        postprocessing()

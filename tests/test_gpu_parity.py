@@ -382,3 +382,44 @@ def test_reconstruct_all_matches_oracle(P):
         q, u = s.reconstruct_all(lam)
         qo, uo = O.reconstruct_all(o, lam)
         assert rel(q, qo) < 1e-11 and rel(u, uo) < 1e-11
+        assert rel(s.postprocess_all(q, u), O.postprocess_all(o, qo, uo)) < 1e-11
+
+
+@pytest.mark.parametrize("tag,kind,n,p", [("m4p2", "m", 4, 2), ("m5p3", "m", 5, 3), ("m6p1", "m", 6, 1),
+                                          ("kI4p4", "kI", 4, 4)])
+def test_reconstruct_postprocess_match_golden(P, golden, tag, kind, n, p):
+    """reconstruct_all / postprocess_all against the unmodified reference (trace.py:171-185)."""
+    import torch
+    g = golden("postprocess.npz")
+    spec = specs.manufactured(P.pb.ProblemSpec) if kind == "m" else specs.constant(P.pb.ProblemSpec, 0.0, 1.0)
+    s = P.tr.TraceSystem(P.mesh(n, n), p, spec)
+    q, u = s.reconstruct_all(g[f"{tag}_lam"])
+    assert rel(q, g[f"{tag}_q"]) < TOL and rel(u, g[f"{tag}_u"]) < TOL
+    assert rel(s.postprocess_all(g[f"{tag}_q"], g[f"{tag}_u"]), g[f"{tag}_ustar"]) < TOL
+    qt, ut = s.reconstruct_all(torch.as_tensor(g[f"{tag}_lam"], device="cuda"))   # tensor in -> tensors out
+    assert qt.is_cuda and rel(qt.cpu().numpy(), g[f"{tag}_q"]) < TOL
+    assert s.postprocess_all(qt, ut).is_cuda
+
+
+@pytest.mark.parametrize("aniso", [False, True])
+def test_reconstruct_postprocess_gpu_condensed(P, aniso):
+    """Element-wise constant media with more distinct elements than GPU_CLASSES take the
+    flux-first device elimination (PiecewiseCondenser.reconstruct); checked against the oracle."""
+    n, p = 66, 1
+    rng = np.random.default_rng(21)
+    if aniso:
+        Kx, Ky = np.exp(rng.uniform(-2, 2, (2, n, n)))
+        spec_p = P.pb.ProblemSpec(P.pb.piecewise_anisotropic(Kx, Ky), specs.bump_f, specs.zero, 1.0)
+        spec_o = O.Spec(O.piecewise_anisotropic(Kx, Ky), specs.bump_f, specs.zero, 1.0)
+    else:
+        Kg = specs.hetero_K(n, seed=21)
+        spec_p = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.bump_f, specs.bump_u, 1.0)
+        spec_o = O.Spec(O.piecewise_coefficient(Kg), specs.bump_f, specs.bump_u, 1.0)
+    s = P.tr.TraceSystem(P.mesh(n, n), p, spec_p)
+    assert s.piecewise is not None
+    o = O.OracleTrace(O.Grid(n, n), p, spec_o)
+    lam = rng.standard_normal(s.ndof)
+    q, u = s.reconstruct_all(lam)
+    qo, uo = O.reconstruct_all(o, lam)
+    assert rel(q, qo) < 1e-11 and rel(u, uo) < 1e-11
+    assert rel(s.postprocess_all(q, u), O.postprocess_all(o, qo, uo)) < 1e-11

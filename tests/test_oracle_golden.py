@@ -121,3 +121,19 @@ def test_oracle_config1(golden):
     _, mon = O.solve_mg(levels, b=b, tol=1e-10, max_cycles=400)
     assert len(mon.residuals) == len(g["res"]) == 93
     np.testing.assert_allclose(mon.rho, np.array(g["res"][1:]) / g["res"][:-1], rtol=1e-5)
+
+
+POST_CASES = [("m4p2", "m", 4, 2), ("m5p3", "m", 5, 3), ("m6p1", "m", 6, 1), ("kI4p4", "kI", 4, 4)]
+
+
+@pytest.mark.parametrize("tag,kind,n,p", POST_CASES)
+def test_oracle_reconstruct_postprocess(golden, tag, kind, n, p):
+    g = golden("postprocess.npz")
+    spec = specs.manufactured(O.Spec) if kind == "m" else specs.constant(O.Spec, 0.0, 1.0)
+    s = O.OracleTrace(O.Grid(n, n), p, spec)
+    q, u = O.reconstruct_all(s, g[f"{tag}_lam"])
+    scale = lambda a: max(np.abs(a).max(), 1e-300)
+    assert np.abs(q - g[f"{tag}_q"]).max() <= 1e-12 * scale(g[f"{tag}_q"])
+    assert np.abs(u - g[f"{tag}_u"]).max() <= 1e-12 * scale(g[f"{tag}_u"])
+    us = O.postprocess_all(s, g[f"{tag}_q"], g[f"{tag}_u"])
+    assert np.abs(us - g[f"{tag}_ustar"]).max() <= 1e-12 * scale(g[f"{tag}_ustar"])
