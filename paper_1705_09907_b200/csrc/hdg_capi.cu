@@ -43,6 +43,7 @@ struct hdg_level {
   long long nh = 0, n_blocks = 0, ndof = 0;
   bool stored = false;
   std::vector<double> Wh, Wv, Dh, Dv;                // shared mode (host copies -> kernel params)
+  std::vector<double> Gh, Gv;                        // shared mode: mirror-reduced stencils (Sym<N1>)
   double *dWh = nullptr, *dWv = nullptr;             // stored mode streams
   double *dDh = nullptr, *dDv = nullptr;
   bool has_bj = false;
@@ -166,8 +167,15 @@ static int apply_t(const hdg_level* L, MvArgs& a, cudaStream_t s) {
   const int grid = grid_for<N1, STORED, EPI>(L);
   SharedOp<(STORED ? 1 : N1)> op;
   if constexpr (!STORED) {
-    std::memcpy(op.Wh, L->Wh.data(), sizeof(op.Wh));
-    std::memcpy(op.Wv, L->Wv.data(), sizeof(op.Wv));
+    if constexpr (HDG_SHARED_SYM) {   // kernel reads the reduced stencils from op.Wh / op.Wv
+      std::memset(op.Wh, 0, sizeof(op.Wh));
+      std::memset(op.Wv, 0, sizeof(op.Wv));
+      std::memcpy(op.Wh, L->Gh.data(), sizeof(double) * Sym<N1>::SIZE);
+      std::memcpy(op.Wv, L->Gv.data(), sizeof(double) * Sym<N1>::SIZE);
+    } else {
+      std::memcpy(op.Wh, L->Wh.data(), sizeof(op.Wh));
+      std::memcpy(op.Wv, L->Wv.data(), sizeof(op.Wv));
+    }
     if (L->has_bj) {
       std::memcpy(op.Dh, L->Dh.data(), sizeof(op.Dh));
       std::memcpy(op.Dv, L->Dv.data(), sizeof(op.Dv));
@@ -233,6 +241,68 @@ static int init_level(hdg_level* L, int nx, int ny, int p) {
   return 0;
 }
 
+// Mirror reduction of a merged facet stencil W (7 n1 x n1 blocks, stencil order of
+// merged_entry_src) into Sym<N1> form (hdg_kernels.cuh, apply_shared_sym).  Returns false when
+// W is not invariant under the two facet mirrors to 1e-11 of max|W|; otherwise G receives the
+// group-averaged (in exact arithmetic: identical) operator's even / odd blocks.
+static bool mirror_reduce(const std::vector<double>& W, int n1, std::vector<double>& G) {
+  const int h = (n1 + 1) / 2, l = n1 / 2, ke = 2 * h + n1, ko = 2 * l + n1;
+  auto w = [&](int q, int k, int m) { return W[(q * n1 + k) * n1 + m]; };
+  auto rv = [&](int k) { return n1 - 1 - k; };
+  std::vector<double> B0(n1 * n1), B1(n1 * n1), B3(n1 * n1), B4(n1 * n1);
+  double scale = 0.0, defect = 0.0;
+  for (double v : W) scale = std::fmax(scale, std::fabs(v));
+  auto dev = [&](double a, double b) { defect = std::fmax(defect, std::fabs(a - b)); };
+  for (int k = 0; k < n1; ++k)
+    for (int m = 0; m < n1; ++m) {   // normal mirror: W q0 = q2, q3 = q5 R, q4 = q6 R
+      dev(w(0, k, m), w(2, k, m));
+      dev(w(3, k, m), w(5, k, rv(m)));
+      dev(w(4, k, m), w(6, k, rv(m)));
+      B0[k * n1 + m] = 0.5 * (w(0, k, m) + w(2, k, m));
+      B1[k * n1 + m] = w(1, k, m);
+      B3[k * n1 + m] = 0.5 * (w(3, k, m) + w(5, k, rv(m)));
+      B4[k * n1 + m] = 0.5 * (w(4, k, m) + w(6, k, rv(m)));
+    }
+  std::vector<double> C0(n1 * n1), C1(n1 * n1), C3(n1 * n1);
+  for (int k = 0; k < n1; ++k)
+    for (int m = 0; m < n1; ++m) {   // tangential mirror: R B0 R = B0, R B1 R = B1, R B4 = B3
+      dev(B0[k * n1 + m], B0[rv(k) * n1 + rv(m)]);
+      dev(B1[k * n1 + m], B1[rv(k) * n1 + rv(m)]);
+      dev(B3[k * n1 + m], B4[rv(k) * n1 + m]);
+      C0[k * n1 + m] = 0.5 * (B0[k * n1 + m] + B0[rv(k) * n1 + rv(m)]);
+      C1[k * n1 + m] = 0.5 * (B1[k * n1 + m] + B1[rv(k) * n1 + rv(m)]);
+      C3[k * n1 + m] = 0.5 * (B3[k * n1 + m] + B4[rv(k) * n1 + m]);
+    }
+  if (!(defect <= 1e-11 * scale)) return false;
+  G.assign(h * ke + l * ko, 0.0);
+  double* Ge = G.data();
+  double* Go = G.data() + h * ke;
+  for (int k = 0; k < h; ++k) {
+    for (int m = 0; m < l; ++m) {
+      Ge[k * ke + m] = 0.5 * (C0[k * n1 + m] + C0[k * n1 + rv(m)]);
+      Ge[k * ke + h + m] = 0.5 * (C1[k * n1 + m] + C1[k * n1 + rv(m)]);
+    }
+    if (n1 & 1) {
+      Ge[k * ke + h - 1] = C0[k * n1 + h - 1];
+      Ge[k * ke + 2 * h - 1] = C1[k * n1 + h - 1];
+    }
+    for (int m = 0; m < n1; ++m) Ge[k * ke + 2 * h + m] = 0.5 * (C3[k * n1 + m] + C3[rv(k) * n1 + m]);
+  }
+  for (int k = 0; k < l; ++k) {
+    for (int m = 0; m < l; ++m) {
+      Go[k * ko + m] = 0.5 * (C0[k * n1 + m] - C0[k * n1 + rv(m)]);
+      Go[k * ko + l + m] = 0.5 * (C1[k * n1 + m] - C1[k * n1 + rv(m)]);
+    }
+    for (int m = 0; m < n1; ++m) Go[k * ko + 2 * l + m] = 0.5 * (C3[k * n1 + m] - C3[rv(k) * n1 + m]);
+  }
+  return true;
+}
+
+static void delete_level_keep_error(hdg_level* L) {
+  cudaFree(L->partials);
+  delete L;
+}
+
 // ------------------------------------------------------------------------------- C ABI
 
 extern "C" {
@@ -240,6 +310,8 @@ extern "C" {
 const char* hdg_last_error(void) { return g_err.c_str(); }
 int hdg_version(void) { return 1; }
 int64_t hdg_launch_count(void) { return g_launches.load(); }
+
+static int create_stored(int nx, int ny, int p, const double* blocks, bool bcast, hdg_level** out);
 
 int hdg_level_create_shared(int nx, int ny, int p, const double* block, hdg_level** out) {
   if (!out || !block) return fail(HDG_EINVAL, "null argument");
@@ -261,12 +333,31 @@ int hdg_level_create_shared(int nx, int ny, int p, const double* block, hdg_leve
           W[(q * n1 + k) * n1 + m] = v;
         }
   }
+  if (HDG_SHARED_SYM) {
+    const bool ok = mirror_reduce(L->Wh, n1, L->Gh) && mirror_reduce(L->Wv, n1, L->Gv);
+    if (!ok) {
+      // not mirror-symmetric (e.g. side-dependent tau): stream the one block as stored facets
+      delete_level_keep_error(L);
+      if (nx < 1 || ny < 1 || p < 1 || p > MAXN1 - 1) return fail(HDG_EINVAL, "bad level shape");
+      const size_t bb = sizeof(double) * 16 * (size_t)n1 * n1;
+      double* dblk = nullptr;
+      CK(cudaMalloc(&dblk, bb));
+      CK(cudaMemcpy(dblk, block, bb, cudaMemcpyHostToDevice));
+      rc = create_stored(nx, ny, p, dblk, true, out);
+      cudaFree(dblk);
+      return rc;
+    }
+  }
   if ((rc = prepare(n1, false))) { hdg_level_destroy(L); return rc; }
   *out = L;
   return 0;
 }
 
 int hdg_level_create_stored(int nx, int ny, int p, const double* blocks, hdg_level** out) {
+  return create_stored(nx, ny, p, blocks, false, out);
+}
+
+static int create_stored(int nx, int ny, int p, const double* blocks, bool bcast, hdg_level** out) {
   if (!out) return fail(HDG_EINVAL, "null argument");
   hdg_level* L = new hdg_level();
   L->stored = true;
@@ -287,9 +378,9 @@ int hdg_level_create_stored(int nx, int ny, int p, const double* blocks, hdg_lev
     const long long nbk = (nthr + bs - 1) / bs;
 #define RELAYOUT_CASE(N)                                                                         \
   {                                                                                              \
-    relayout_kernel<N><<<(unsigned)nbk, bs>>>(blocks, nx, ny, L->nxp, false, L->dWh);   \
+    relayout_kernel<N><<<(unsigned)nbk, bs>>>(blocks, nx, ny, L->nxp, false, L->dWh, bcast);   \
     CKL();                                                                                       \
-    relayout_kernel<N><<<(unsigned)nbk, bs>>>(blocks, nx, ny, L->nxp, true, L->dWv);    \
+    relayout_kernel<N><<<(unsigned)nbk, bs>>>(blocks, nx, ny, L->nxp, true, L->dWv, bcast);    \
     CKL();                                                                                       \
     break;                                                                                       \
   }

@@ -56,6 +56,13 @@ namespace hdg {
 #ifndef HDG_NWARP
 #define HDG_NWARP 8
 #endif
+#ifndef HDG_SHARED_SYM
+#define HDG_SHARED_SYM 1   // shared mode: mirror-reduced stencil (apply_shared_sym); 0 = full n1 x 7n1
+#endif
+#if HDG_DMMA
+#undef HDG_SHARED_SYM
+#define HDG_SHARED_SYM 0
+#endif
 
 constexpr int TX = 32;     // tile width in elements (= warp width: lanes walk i)
 constexpr int NWARP = HDG_NWARP;   // warps per CTA
@@ -297,17 +304,23 @@ __device__ __forceinline__ void stage_tile(const MvArgs& a, double* buf, int i0,
 #endif
   if (lane == 0) {
     unsigned bytes = 0;
+#ifndef HDG_EXP_NOH
     for (int r = warp; r < C::HROWS; r += NWARP) bytes += run_bytes(h_run<N1, ST>(a, i0, j0, r));
+#endif
     fence_proxy_async();               // prior generic reads/writes of this buffer -> async proxy
     mbar_arrive_expect_tx(bar, bytes);
+#ifndef HDG_EXP_NOH
     for (int r = warp; r < C::HROWS; r += NWARP) run_issue(a.x, buf, h_run<N1, ST>(a, i0, j0, r), bar);
+#endif
   }
   if (edge) {  // zero Dirichlet / out-of-mesh parts of H rows (interior tiles skip this)
     for (int r = warp; r < C::HROWS; r += NWARP) run_zero(buf, h_run<N1, ST>(a, i0, j0, r), lane);
   }
   // V columns: coalesced 8-byte LDGSTS from the contiguous run, transposed into [row][col];
   // src-size 0 zero-fills Dirichlet / out-of-mesh blocks
+#ifndef HDG_EXP_NOV
   stage_v_columns<N1, ST>(a, buf + C::HSZ, i0, j0, warp, NWARP, lane);
+#endif
   cp_async_mbar_arrive(bar);           // every thread: one arrival when its LDGSTS land
 }
 
@@ -346,6 +359,85 @@ __device__ __forceinline__ void apply_shared(const double* const (&nb)[FF][7], c
 #pragma unroll
         for (int f = 0; f < FF; ++f) acc[f][k] = fma(w, xv[f][m], acc[f][k]);
       }
+  }
+}
+
+// Shared mode, mirror-reduced form (default).  A constant-coefficient block on a uniform
+// Cartesian mesh is invariant under the two mirrors of a facet's stencil (hdg_capi.cu checks
+// this at setup to 1e-11 and falls back to stored blocks otherwise):
+//   normal mirror      q0 <-> q2, q3 <-> R q5, q4 <-> R q6          (output unchanged)
+//   tangential mirror  q0, q1, q2 reversed, q3 <-> q4, q5 <-> q6     (output reversed)
+// (R = reversal of a facet's n1 nodes; GLL nodes are symmetric).  Folding the stencil with
+// them, a = q0 + q2, c = q3 + R q5, d = q4 + R q6, and splitting a, q1 and c +/- d into their
+// even / odd halves, the n1 x 7n1 stencil becomes two small dense blocks:
+//   ye (H x KE) . [a_e, q1_e, c + d],   yo (L x KO) . [a_o, q1_o, c - d],
+//   y[k] = ye[k] + yo[k],  y[n1-1-k] = ye[k] - yo[k]
+// i.e. H KE + L KO FMAs (51 at n1 = 5) instead of 7 n1^2 (175), plus ~7 n1 adds.
+template <int N1> struct Sym {
+  static constexpr int H = (N1 + 1) / 2, L = N1 / 2;
+  static constexpr int KE = 2 * H + N1, KO = 2 * L + N1;
+  static constexpr int SIZE = H * KE + L * KO;   // <= 7 n1^2: lives in SharedOp::Wh / Wv
+};
+
+template <int N1, int FF>
+__device__ __forceinline__ void apply_shared_sym(const double* const (&nb)[FF][7], const double* G,
+                                                 double (&acc)[FF][N1]) {
+  using Y = Sym<N1>;
+  constexpr int H = Y::H, L = Y::L, KE = Y::KE, KO = Y::KO;
+  const double* Ge = G;
+  const double* Go = G + H * KE;
+  double ze[FF][KE], zo[FF][KO > 0 ? KO : 1];
+#pragma unroll
+  for (int f = 0; f < FF; ++f) {
+    const double* x0 = nb[f][0]; const double* x1 = nb[f][1]; const double* x2 = nb[f][2];
+#pragma unroll
+    for (int m = 0; m < L; ++m) {
+      const double am = x0[m] + x2[m], ar = x0[N1 - 1 - m] + x2[N1 - 1 - m];
+      ze[f][m] = am + ar;
+      zo[f][m] = am - ar;
+      const double om = x1[m], orr = x1[N1 - 1 - m];
+      ze[f][H + m] = om + orr;
+      zo[f][L + m] = om - orr;
+    }
+    if constexpr (N1 & 1) {
+      ze[f][H - 1] = x0[H - 1] + x2[H - 1];
+      ze[f][2 * H - 1] = x1[H - 1];
+    }
+#pragma unroll
+    for (int m = 0; m < N1; ++m) {
+      const double c = nb[f][3][m] + nb[f][5][N1 - 1 - m];
+      const double d = nb[f][4][m] + nb[f][6][N1 - 1 - m];
+      ze[f][2 * H + m] = c + d;
+      zo[f][2 * L + m] = c - d;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    double ye[FF], yo[FF];
+#pragma unroll
+    for (int f = 0; f < FF; ++f) ye[f] = 0.0, yo[f] = 0.0;
+#pragma unroll
+    for (int t = 0; t < KE; ++t) {
+      const double g = Ge[k * KE + t];
+#pragma unroll
+      for (int f = 0; f < FF; ++f) ye[f] = fma(g, ze[f][t], ye[f]);
+    }
+    if (k < L) {
+#pragma unroll
+      for (int t = 0; t < KO; ++t) {
+        const double g = Go[k * KO + t];
+#pragma unroll
+        for (int f = 0; f < FF; ++f) yo[f] = fma(g, zo[f][t], yo[f]);
+      }
+#pragma unroll
+      for (int f = 0; f < FF; ++f) {
+        acc[f][k] = ye[f] + yo[f];
+        acc[f][N1 - 1 - k] = ye[f] - yo[f];
+      }
+    } else {
+#pragma unroll
+      for (int f = 0; f < FF; ++f) acc[f][k] = ye[f];
+    }
   }
 }
 
@@ -554,7 +646,8 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
 #pragma unroll
         for (int f = 0; f < F; ++f) apply_dmma_row<N1, false>(Hs, Vs, hpar0, hstep, F * w + f + 1, wa, scr, acc[f], tx);
       } else {
-        apply_shared<N1, F>(nb, op.Wh, acc);
+        if constexpr (HDG_SHARED_SYM) apply_shared_sym<N1, F>(nb, op.Wh, acc);
+        else apply_shared<N1, F>(nb, op.Wh, acc);
       }
 #pragma unroll
       for (int f = 0; f < F; ++f) {
@@ -612,7 +705,8 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
 #pragma unroll
         for (int f = 0; f < F; ++f) apply_dmma_row<N1, true>(Hs, Vs, hpar0, hstep, F * w + f + 1, wa, scr, acc[f], tx);
       } else {
-        apply_shared<N1, F>(nb, op.Wv, acc);
+        if constexpr (HDG_SHARED_SYM) apply_shared_sym<N1, F>(nb, op.Wv, acc);
+        else apply_shared<N1, F>(nb, op.Wv, acc);
       }
 #pragma unroll
       for (int f = 0; f < F; ++f) {
@@ -853,7 +947,7 @@ __host__ __device__ inline void merged_entry_src(bool vert, int q, int k, int m,
 
 template <int N1>
 __global__ void relayout_kernel(const double* __restrict__ S, int nx, int ny, int nxp, bool vert,
-                                double* __restrict__ W) {
+                                double* __restrict__ W, bool bcast = false) {
   using C = Cfg<N1>;
   const long long nslots = (long long)ny * nxp;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -870,6 +964,7 @@ __global__ void relayout_kernel(const double* __restrict__ S, int nx, int ny, in
   if (valid) {
     e1 = vert ? ((long long)j * nx + (i - 1)) : ((long long)(j - 1) * nx + i);
     e2 = (long long)j * nx + i;
+    if (bcast) e1 = e2 = 0;   // one block for every element (asymmetric constant operator)
   }
   const int L = 4 * N1;
   const int q = idx / (N1 * N1), k = (idx / N1) % N1, m = idx % N1;

@@ -62,6 +62,25 @@ def test_matvec_stored_equals_shared(P, p):
     assert rel(st.matvec_free(x), s.matvec_free(x)) < TOL
 
 
+@pytest.mark.parametrize("p", [2, 4, 7])
+def test_matvec_shared_asymmetric_block_falls_back(P, p):
+    """A single-class block that is NOT invariant under the facet mirrors (the mirror-reduced
+    constant-bank kernel would be wrong for it) is streamed as stored facets instead."""
+    nx, ny = 23, 17
+    s = P.tr.TraceSystem(P.mesh(nx, ny), p, specs.constant(P.pb.ProblemSpec))
+    S = s.operator.S_cls[0].copy()
+    rng = np.random.default_rng(p)
+    Pm = rng.uniform(-0.05, 0.05, S.shape) * np.abs(S).max()
+    S = S + Pm + Pm.T                          # still symmetric, no longer mirror-invariant
+    m = P.mesh(nx, ny)
+    a = P.tr.TraceSystem.from_blocks(m, p, S[None], np.zeros(nx * ny, np.int64))
+    assert a.operator.shared
+    o = O.OracleTrace(O.Grid(nx, ny), p, None, _blocks=np.broadcast_to(S, (nx * ny,) + S.shape).copy())
+    o.schur *= o.gmask[:, None, :]
+    x = rng.uniform(-1, 1, a.ndof)
+    assert rel(a.matvec_free(x), o.matvec(x)) < TOL
+
+
 @pytest.mark.parametrize("n,p", [(16, 2), (24, 4), (16, 8)])
 def test_matvec_heterogeneous_vs_oracle(P, n, p):
     Kg = specs.hetero_K(n, seed=n + p)

@@ -27,7 +27,7 @@ for (n, p) in [(37, 4), (40, 1), (33, 8), (35, 2)]:
     ref = lay.sum_owners(np.einsum("ij,ej->ei", S, lay.gather(x) * np.repeat(lay.side_mask(), p + 1, axis=1)))
     errs.append(float(np.abs(s.matvec_free(x) - ref).max() / np.abs(ref).max()))
 out["parity_max_rel_err"] = max(errs)
-cases = [(1024, 4, False), (512, 4, True), (1024, 1, False), (768, 8, False), (384, 8, True)]
+cases = [tuple(c) for c in json.loads(os.environ.get("TUNE_CASES", "null"))] if os.environ.get("TUNE_CASES") else [(1024, 4, False), (512, 4, True), (1024, 1, False), (768, 8, False), (384, 8, True)]
 for (n, p, stored) in cases:
     s = TraceSystem(build_cartesian(n, n), p, constant_problem(0.0, 1.0))
     if stored:
