@@ -39,7 +39,7 @@ namespace hdg {
 #define HDG_F_MAXN1 13     // cap on the two-facets-per-thread rule (tuning knob)
 #endif
 #ifndef HDG_F3_MAXN1
-#define HDG_F3_MAXN1 0     // shared mode: three facets per thread up to this n1 (tuning knob)
+#define HDG_F3_MAXN1 5     // shared mode: HDG_F_SHARED facets per thread up to this n1 (measured: p<=4)
 #endif
 #ifndef HDG_F_MAXN1_SHARED
 #define HDG_F_MAXN1_SHARED 9
@@ -386,6 +386,13 @@ __device__ __forceinline__ void apply_shared_sym(const double* const (&nb)[FF][7
   constexpr int H = Y::H, L = Y::L, KE = Y::KE, KO = Y::KO;
   const double* Ge = G;
   const double* Go = G + H * KE;
+#ifdef HDG_EXP_NOCOMPUTE
+#pragma unroll
+  for (int f = 0; f < FF; ++f)
+#pragma unroll
+    for (int k = 0; k < N1; ++k) acc[f][k] = nb[f][1][k] + nb[f][4][k];
+  return;
+#endif
   double ze[FF][KE], zo[FF][KO > 0 ? KO : 1];
 #pragma unroll
   for (int f = 0; f < FF; ++f) {

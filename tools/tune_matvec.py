@@ -34,17 +34,18 @@ for (n, p, stored) in cases:
         E = n * n
         s = TraceSystem.from_blocks(build_cartesian(n, n), p, np.repeat(s.operator.S_cls, E, axis=0), np.arange(E))
     h = s.operator.handle
-    xs = [torch.rand(s.ndof, dtype=torch.float64, device="cuda") for _ in range(4)]
-    ys = [torch.empty_like(xs[0]) for _ in range(4)]
+    NR = int(os.environ.get("TUNE_ROT", "4"))
+    xs = [torch.rand(s.ndof, dtype=torch.float64, device="cuda") for _ in range(NR)]
+    ys = [torch.empty_like(xs[0]) for _ in range(NR)]
     st = torch.cuda.current_stream().cuda_stream
     for k in range(20):
-        L.check(L.lib.hdg_matvec(h, xs[k %% 4].data_ptr(), ys[k %% 4].data_ptr(), st))
+        L.check(L.lib.hdg_matvec(h, xs[k %% NR].data_ptr(), ys[k %% NR].data_ptr(), st))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     R = 200
     e0.record()
     for k in range(R):
-        L.check(L.lib.hdg_matvec(h, xs[k %% 4].data_ptr(), ys[k %% 4].data_ptr(), st))
+        L.check(L.lib.hdg_matvec(h, xs[k %% NR].data_ptr(), ys[k %% NR].data_ptr(), st))
     e1.record(); torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / R
     byts = 16 * s.ndof + (s.operator.operator_bytes() if stored else 0)
