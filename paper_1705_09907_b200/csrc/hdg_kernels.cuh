@@ -38,6 +38,9 @@ namespace hdg {
 #ifndef HDG_F_MAXN1
 #define HDG_F_MAXN1 13     // cap on the two-facets-per-thread rule (tuning knob)
 #endif
+#ifndef HDG_F_SHARED
+#define HDG_F_SHARED 3     // facet rows per thread in shared mode for n1 <= HDG_F3_MAXN1
+#endif
 #ifndef HDG_F3_MAXN1
 #define HDG_F3_MAXN1 5     // shared mode: HDG_F_SHARED facets per thread up to this n1 (measured: p<=4)
 #endif
@@ -77,7 +80,7 @@ template <int N1, bool ST = false> struct Cfg {
   // facets per thread per orientation (measured: 2 pays up to p=8 when W is in the constant
   // bank, up to p=4 when W streams from HBM)
   static constexpr int F = (N1 <= (ST ? 5 : HDG_F_MAXN1_SHARED)) && (N1 <= HDG_F_MAXN1)
-                               ? ((!ST && N1 <= HDG_F3_MAXN1) ? 3 : 2) : 1;
+                               ? ((!ST && N1 <= HDG_F3_MAXN1) ? HDG_F_SHARED : 2) : 1;
   static constexpr int TY = NWARP * F;              // tile height in elements
   static constexpr int WSZ = 7 * N1 * N1;           // merged facet operator entries
   static constexpr int DSZ = N1 * N1;               // block-Jacobi inverse entries
