@@ -126,6 +126,11 @@ int hdg_mg_create(hdg_level* const* levels, hdg_transfer* const* transfers, int 
 int hdg_mg_destroy(hdg_mg* mg);
 /* coarsest-level inverse, n x n row-major HOST pointer, n = ndof of the last level */
 int hdg_mg_set_coarse_inverse(hdg_mg* mg, const double* inv, int64_t n);
+/* Fused coarse tail (default on): the trailing p = 1, block-Jacobi-smoothed, h-linked levels
+ * of <= 70k dofs run as ONE cooperative kernel with grid barriers between dependent steps
+ * (same recursion, buffers and weights as the per-launch cycle, multigrid.py:393-406).
+ * enable = 0 issues them as separate launches (A/B timing, parity tests). */
+int hdg_mg_set_fused_tail(hdg_mg* mg, int enable);
 /* x = cycle(b, x0) with nu1/nu2 smoothing sweeps (FSAI if attached to the level, else
  * block-Jacobi), visits = 1 (V) or 2 (W).
  * x0 may be NULL (zero initial guess, as v_cycle(x0=None)).  x may alias x0.

@@ -49,6 +49,7 @@ SIGNATURES = [
                               ctypes.POINTER(c_void_p)]),
     ("hdg_mg_destroy", c_int, [c_void_p]),
     ("hdg_mg_set_coarse_inverse", c_int, [c_void_p, c_void_p, c_int64]),
+    ("hdg_mg_set_fused_tail", c_int, [c_void_p, c_int]),
     ("hdg_mg_cycle", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
                              c_void_p]),
     ("hdg_coarse_solve", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -4,6 +4,7 @@
 #include "hdgb200.h"
 #include "hdg_kernels.cuh"
 
+#include <algorithm>
 #include <atomic>
 #define _USE_MATH_DEFINES
 #include <cmath>
@@ -61,6 +62,7 @@ struct hdg_level {
   int *g_ptr = nullptr, *g_col = nullptr, *gt_ptr = nullptr, *gt_col = nullptr;
   double *g_val = nullptr, *gt_val = nullptr;
   double lam_max = 1.0, cheb_frac = 0.15, fsai_omega = 1.0;
+  double* tail_wd = nullptr;   // fused coarse tail, shared mode: device copy of Wh, Wv, Dh, Dv (n1 = 2)
 };
 
 struct hdg_transfer {
@@ -86,6 +88,8 @@ struct hdg_mg {
   long long nc = 0;
   cudaStream_t cs = nullptr;
   std::map<std::tuple<const void*, const void*, void*, int, int, int>, GraphEntry> graphs;
+  int tail_k0 = -1;              // first level of the fused coarse tail (-1: none)
+  bool tail_enabled = true;
 };
 
 // ------------------------------------------------------------------------------ helpers
@@ -398,6 +402,7 @@ static int create_stored(int nx, int ny, int p, const double* blocks, bool bcast
 int hdg_level_destroy(hdg_level* L) {
   if (!L) return 0;
   cudaFree(L->dWh); cudaFree(L->dWv); cudaFree(L->dDh); cudaFree(L->dDv); cudaFree(L->partials);
+  cudaFree(L->tail_wd);
   cudaFree(L->g_ptr); cudaFree(L->g_col); cudaFree(L->g_val);
   cudaFree(L->gt_ptr); cudaFree(L->gt_col); cudaFree(L->gt_val);
   delete L;
@@ -800,6 +805,14 @@ int hdg_mg_destroy(hdg_mg* mg) {
   return 0;
 }
 
+int hdg_mg_set_fused_tail(hdg_mg* mg, int enable) {
+  if (!mg) return fail(HDG_EINVAL, "null mg");
+  mg->tail_enabled = enable != 0;
+  for (auto& kv : mg->graphs) cudaGraphExecDestroy(kv.second.exec);
+  mg->graphs.clear();
+  return 0;
+}
+
 int hdg_mg_set_coarse_inverse(hdg_mg* mg, const double* inv, int64_t n) {
   if (!mg || !inv) return fail(HDG_EINVAL, "null argument");
   if (n != mg->L[mg->n - 1]->ndof) return fail(HDG_EINVAL, "coarse inverse size != coarsest ndof");
@@ -830,12 +843,153 @@ int hdg_coarse_solve(hdg_mg* mg, const double* b, double* x, void* stream) {
   return coarse_apply(mg, b, x, S(stream));
 }
 
+// ------------------------------------------------------------------ fused coarse-level tail
+// Levels k0..n-1 run as one single-CTA kernel with all their vectors in shared memory
+// (hdg_kernels.cuh: tail_cycle_kernel) when they are all p = 1, linked by h-transfers and
+// smoothed by block-Jacobi, and their X, T, B vectors fit the shared-memory budget.
+// vectors; + the program copy + shared operators <= 218 KB
+static const long long TAIL_SMEM_DOUBLES = 27200 - TAIL_ARGS_DOUBLES - 64 * TAIL_MAXL;
+
+static const long long TAIL_MAX_TOP_DOF = 2048;
+
+static long long tail_footprint(const hdg_mg* mg, int k0) {
+  long long d = 0;
+  for (int k = k0; k < mg->n; ++k) d += 3 * (mg->L[k]->ndof + (mg->L[k]->ndof & 1));
+  return d;
+}
+
+static int tail_find(const hdg_mg* mg) {
+  if (!mg->tail_enabled) return -1;
+  int k0 = -1;
+  for (int k = mg->n - 1; k >= 0; --k) {
+    const hdg_level* L = mg->L[k];
+    if (L->n1 != 2) break;
+    if (k < mg->n - 1 && (!mg->T[k]->is_h || L->use_fsai || !L->has_bj)) break;
+    if (mg->n - k > TAIL_MAXL || tail_footprint(mg, k) > TAIL_SMEM_DOUBLES) break;
+    // one CTA beats ~6 launches per level visit only while the level is small (measured on B200:
+    // a 960-dof level costs 14 us inside the tail vs 26 us as launches, a 3968-dof level 43 vs 27)
+    if (L->ndof > TAIL_MAX_TOP_DOF) break;
+    k0 = k;
+  }
+  return (k0 >= 0 && k0 < mg->n - 1) ? k0 : -1;   // a tail needs at least one smoothed level
+}
+
+// device copies of the shared-mode operators of the tail levels (outside any stream capture)
+static int tail_prepare(hdg_mg* mg) {
+  mg->tail_k0 = tail_find(mg);
+  if (mg->tail_k0 < 0) return 0;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(tail_cycle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)((TAIL_SMEM_DOUBLES + TAIL_ARGS_DOUBLES + 64 * TAIL_MAXL) * sizeof(double))));
+    attr = true;
+  }
+  for (int k = mg->tail_k0; k < mg->n; ++k) {
+    hdg_level* L = mg->L[k];
+    if (L->stored || L->tail_wd) continue;
+    std::vector<double> h(64, 0.0);
+    std::copy(L->Wh.begin(), L->Wh.end(), h.begin());
+    std::copy(L->Wv.begin(), L->Wv.end(), h.begin() + 28);
+    if (L->has_bj) {
+      std::copy(L->Dh.begin(), L->Dh.end(), h.begin() + 56);
+      std::copy(L->Dv.begin(), L->Dv.end(), h.begin() + 60);
+    }
+    CK(cudaMalloc(&L->tail_wd, sizeof(double) * 64));
+    CK(cudaMemcpy(L->tail_wd, h.data(), sizeof(double) * 64, cudaMemcpyHostToDevice));
+  }
+  return 0;
+}
+
+// the same recursion, sweep weights and buffer roles as cycle_rec (multigrid.py:393-406), on
+// buffer ids 3 * (k - k0) + {0: X, 1: T, 2: B}; the residual reuses the free T buffer
+struct TailGen {
+  hdg_mg* mg;
+  TailArgs* A;
+  int k0, nu1, nu2, visits;
+  bool overflow = false;
+  void emit(int code, int k, int x, int b, int out, double w = 0.0) {
+    if (A->nops >= TAIL_MAXOPS) { overflow = true; return; }
+    TailOp& o = A->ops[A->nops++];
+    o.code = (short)code; o.lev = (short)(k - k0); o.x = (short)x; o.b = (short)b; o.out = (short)out; o.w = w;
+  }
+  int id(int k, int role) const { return 3 * (k - k0) + role; }
+  void gen(int k, bool zero_init) {
+    hdg_level* L = mg->L[k];
+    const int xk = id(k, 0), bk = id(k, 2);
+    if (k == mg->n - 1) { if (mg->nc > 0) emit(T_COARSE, k, -1, bk, xk); return; }
+    if (L->ndof == 0) return;
+    int cur = xk, oth = id(k, 1), first = 0;
+    if (zero_init) {
+      if (nu1 >= 1) {
+        emit(T_BJZ, k, -1, bk, oth, bj_weight(L, 1, nu1));
+        std::swap(cur, oth);
+        first = 1;
+      } else {
+        emit(T_ZERO, k, -1, -1, xk);
+      }
+    }
+    for (int it = first; it < nu1; ++it) {
+      emit(T_BJ, k, cur, bk, oth, bj_weight(L, it + 1, nu1));
+      std::swap(cur, oth);
+    }
+    emit(T_RES, k, cur, bk, oth);
+    emit(T_RESTRICT, k, oth, -1, id(k + 1, 2));
+    for (int v = 0; v < visits; ++v) gen(k + 1, v == 0);
+    emit(T_PROLONG, k, id(k + 1, 0), -1, cur);
+    for (int it = 0; it < nu2; ++it) {
+      emit(T_BJ, k, cur, bk, oth, bj_weight(L, it + 1, nu2));
+      std::swap(cur, oth);
+    }
+    if (cur != xk) emit(T_COPY, k, cur, -1, xk);
+  }
+};
+
+// returns 1 when the tail was issued, 0 when it does not apply (program too long), < 0 on error
+static int tail_issue(hdg_mg* mg, const double* b, bool zero_init, int nu1, int nu2, int visits, cudaStream_t s) {
+  const int k0 = mg->tail_k0;
+  if (mg->nc > 0 && !mg->Ainv) return fail(HDG_ESTATE, "coarse inverse not set");
+  TailArgs* A = new TailArgs();
+  std::memset(A, 0, sizeof(TailArgs));
+  long long off = 0;
+  for (int k = k0; k < mg->n; ++k) {
+    const hdg_level* L = mg->L[k];
+    TailLevel& t = A->lev[k - k0];
+    t.nx = L->nx; t.ny = L->ny; t.nxp = L->nxp; t.stored = L->stored ? 1 : 0;
+    t.nh = L->nh; t.nblk = L->n_blocks;
+    if (L->stored) {
+      t.W[0] = L->dWh; t.W[1] = L->dWv; t.D[0] = L->dDh; t.D[1] = L->dDv;
+    } else {
+      t.W[0] = L->tail_wd; t.W[1] = L->tail_wd + 28; t.D[0] = L->tail_wd + 56; t.D[1] = L->tail_wd + 60;
+    }
+    const long long len = L->ndof + (L->ndof & 1);   // keep every vector 16-byte aligned
+    for (int r = 0; r < 3; ++r) { t.off[r] = (int)off; off += len; }
+    if (k + 1 < mg->n) A->h[k - k0] = mg->T[k]->ha;
+  }
+  A->Ainv = mg->Ainv;
+  A->nc = (int)mg->nc;
+  A->nlev = mg->n - k0;
+  A->b_in = b;
+  A->x_in = zero_init ? nullptr : mg->X[k0];
+  A->x_out = mg->X[k0];
+  TailGen g{mg, A, k0, nu1, nu2, visits};
+  g.gen(k0, zero_init);
+  if (g.overflow) { delete A; return 0; }
+  tail_cycle_kernel<<<1, TAIL_THREADS, (size_t)(off + TAIL_ARGS_DOUBLES + 64 * TAIL_MAXL) * sizeof(double), s>>>(*A);
+  delete A;
+  CKL();
+  return 1;
+}
+
 // multigrid.py:393-406, device resident: on entry the level-k iterate is X[k] (or zero),
 // on exit the result is in X[k].
 static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1, int nu2, int visits,
                      cudaStream_t s) {
   hdg_level* L = mg->L[k];
   double* xk = mg->X[k];
+  if (k == mg->tail_k0) {
+    const int t = tail_issue(mg, b, zero_init, nu1, nu2, visits, s);
+    if (t != 0) return t < 0 ? t : 0;
+  }
   if (k == mg->n - 1) return coarse_apply(mg, b, xk, s);
   const size_t bytes = sizeof(double) * (size_t)L->ndof;
   double* cur = xk;
@@ -901,6 +1055,8 @@ int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int n
   if (nu1 < 0 || nu2 < 0 || visits < 1) return fail(HDG_EINVAL, "bad cycle parameters");
   if (mg->L[0]->ndof == 0) return 0;
   cudaStream_t s = S(stream);
+  int rc0 = tail_prepare(mg);
+  if (rc0) return rc0;
   if (!use_graph) return cycle_issue(mg, b, x0, x, nu1, nu2, visits, s);
   auto key = std::make_tuple((const void*)b, (const void*)x0, (void*)x, nu1, nu2, visits);
   auto it = mg->graphs.find(key);

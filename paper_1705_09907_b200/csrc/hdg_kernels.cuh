@@ -27,10 +27,14 @@
 //  * Epilogues fuse what follows the apply: residual, residual norm^2 partials, damped
 //    block-Jacobi update, and residual + p-restriction.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <type_traits>
 
 namespace hdg {
+
+namespace cg = cooperative_groups;
 
 #ifndef HDG_NBUF
 #define HDG_NBUF 0         // stage buffers per CTA; 0 = per-order default (measured, see Cfg)
@@ -1080,8 +1084,17 @@ __device__ __forceinline__ const double* hcross(const HArgs& h, int I, int Jl, i
   return h.cross + (set * 4 + cf) * 16;
 }
 
+// SM = true: the vectors live in shared memory (the fused coarse tail below), plain loads;
+// otherwise read-only global loads through the texture path.
+template <bool SM> __device__ __forceinline__ double vld(const double* p) {
+  if constexpr (SM) return *p; else return __ldg(p);
+}
+template <bool SM> __device__ __forceinline__ double2 vld2(const double2* p) {
+  if constexpr (SM) return *p; else return __ldg(p);
+}
 // coarse side value (2 doubles) of coarse window element (I, Jl), side s; zero when the side is
 // a Dirichlet facet or outside the window
+template <bool SM>
 __device__ __forceinline__ void coarse_side(const HArgs& h, const double* ec, int I, int Jl, int s, double* v) {
   long long blk = -1;
   if (s == 0 && Jl >= 1) blk = (long long)(Jl - 1) * h.nxc + I;
@@ -1089,7 +1102,7 @@ __device__ __forceinline__ void coarse_side(const HArgs& h, const double* ec, in
   if (s == 3 && I >= 1) blk = h.nhc + (long long)(I - 1) * h.nyc + Jl;
   if (s == 1 && I + 1 <= h.nxc - 1) blk = h.nhc + (long long)I * h.nyc + Jl;
   if (blk >= 0) {
-    const double2 e = __ldg(reinterpret_cast<const double2*>(ec) + blk);
+    const double2 e = vld2<SM>(reinterpret_cast<const double2*>(ec) + blk);
     v[0] = e.x; v[1] = e.y;
   } else {
     v[0] = 0.0; v[1] = 0.0;
@@ -1097,17 +1110,17 @@ __device__ __forceinline__ void coarse_side(const HArgs& h, const double* ec, in
 }
 
 // fine window facet t (n1 = 2, one double2 per facet) += its prolongation from the coarse level
-__global__ void h_prolong_add_kernel(const HArgs h, const double* __restrict__ ec, double* __restrict__ xf) {
-  const int nxf = 2 * h.nxc, nyf = h.nyf;
-  const long long nvf = (long long)(nxf - 1) * nyf;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= h.nhf + nvf) return;
+template <bool SM>
+__device__ __forceinline__ void h_prolong_add_one(const HArgs& h, const double* __restrict__ ec,
+                                                  double* __restrict__ xf, long long t) {
+  using IT = typename std::conditional<SM, int, long long>::type;   // 32-bit index math for small levels
+  const IT nxf = 2 * h.nxc, nyf = h.nyf, nhf = (IT)h.nhf, tt = (IT)t;
   double add[2] = {0.0, 0.0};
   bool half;
   int I, Jl, hf, cf;
   long long cb = 0;
-  if (t < h.nhf) {  // fine h(i, jl), block (jl-1)*nxf + i
-    const int jg = (int)(t / nxf) + 1 + h.jf0, i = (int)(t % nxf);
+  if (tt < nhf) {  // fine h(i, jl), block (jl-1)*nxf + i
+    const int jg = (int)(tt / nxf) + 1 + h.jf0, i = (int)(tt % nxf);
     I = i >> 1;
     half = (jg & 1) == 0;
     if (half) {
@@ -1121,7 +1134,7 @@ __global__ void h_prolong_add_kernel(const HArgs h, const double* __restrict__ e
       cf = (i & 1) ? 3 : 2;
     }
   } else {          // fine v(i, jl), block nhf + (i-1)*nyf + jl
-    const long long u = t - h.nhf;
+    const IT u = tt - nhf;
     const int i = (int)(u / nyf) + 1, jg = (int)(u % nyf) + h.jf0;
     Jl = (jg >> 1) - h.jc0;
     if (Jl < 0 || Jl >= h.nyc) return;
@@ -1130,13 +1143,13 @@ __global__ void h_prolong_add_kernel(const HArgs h, const double* __restrict__ e
     else { I = (i - 1) >> 1; cf = (jg & 1) ? 1 : 0; }
   }
   if (half) {
-    const double2 e = __ldg(reinterpret_cast<const double2*>(ec) + cb);
+    const double2 e = vld2<SM>(reinterpret_cast<const double2*>(ec) + cb);
     for (int k = 0; k < 2; ++k) add[k] = h.halves[hf * 4 + k * 2] * e.x + h.halves[hf * 4 + k * 2 + 1] * e.y;
   } else {
     const double* tm = hcross(h, I, Jl, cf);
     for (int s = 0; s < 4; ++s) {
       double v[2];
-      coarse_side(h, ec, I, Jl, s, v);
+      coarse_side<SM>(h, ec, I, Jl, s, v);
       for (int k = 0; k < 2; ++k) add[k] += __ldg(tm + k * 8 + s * 2) * v[0] + __ldg(tm + k * 8 + s * 2 + 1) * v[1];
     }
   }
@@ -1145,6 +1158,12 @@ __global__ void h_prolong_add_kernel(const HArgs h, const double* __restrict__ e
   x.x += add[0];
   x.y += add[1];
   *xp = x;
+}
+
+__global__ void h_prolong_add_kernel(const HArgs h, const double* __restrict__ ec, double* __restrict__ xf) {
+  const long long nvf = (long long)(2 * h.nxc - 1) * h.nyf;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < h.nhf + nvf) h_prolong_add_one<false>(h, ec, xf, t);
 }
 
 // fine window blocks of h(i, jg) / v(i, jg) (global row jg), -1 when outside the window
@@ -1158,6 +1177,7 @@ __device__ __forceinline__ long long fine_v(const HArgs& h, int i, int jg) {
 }
 
 // contribution of coarse element (I, Jl)'s 4 cross facets to its side-s coarse dofs
+template <bool SM>
 __device__ __forceinline__ bool cross_restrict(const HArgs& h, const double* rf, int I, int Jl, int s, double* acc) {
   const int J = Jl + h.jc0;
   const long long cfb[4] = {fine_v(h, 2 * I + 1, 2 * J),       // right of SW = v(2I+1, 2J)
@@ -1167,35 +1187,36 @@ __device__ __forceinline__ bool cross_restrict(const HArgs& h, const double* rf,
   if (cfb[0] < 0 || cfb[1] < 0 || cfb[2] < 0 || cfb[3] < 0 || Jl < 0 || Jl >= h.nyc) return false;
   for (int cf = 0; cf < 4; ++cf) {
     const double* tm = hcross(h, I, Jl, cf);
-    const double r0 = __ldg(rf + 2 * cfb[cf]), r1 = __ldg(rf + 2 * cfb[cf] + 1);
+    const double r0 = vld<SM>(rf + 2 * cfb[cf]), r1 = vld<SM>(rf + 2 * cfb[cf] + 1);
     for (int c = 0; c < 2; ++c) acc[c] += tm[0 * 8 + s * 2 + c] * r0 + tm[1 * 8 + s * 2 + c] * r1;
   }
   return true;
 }
 
-__global__ void h_restrict_kernel(const HArgs h, const double* __restrict__ rf, double* __restrict__ rc) {
-  const long long nvc = (long long)(h.nxc - 1) * h.nyc;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= h.nhc + nvc) return;
+template <bool SM>
+__device__ __forceinline__ void h_restrict_one(const HArgs& h, const double* __restrict__ rf,
+                                               double* __restrict__ rc, long long t) {
+  using IT = typename std::conditional<SM, int, long long>::type;   // 32-bit index math for small levels
+  const IT tt = (IT)t, nhc = (IT)h.nhc;
   double acc[2] = {0.0, 0.0};
   bool ok = true;
   long long kf[2];
-  if (t < h.nhc) {  // coarse h(I, Jl)
-    const int Jl = (int)(t / h.nxc) + 1, I = (int)(t % h.nxc);
+  if (tt < nhc) {  // coarse h(I, Jl)
+    const int Jl = (int)(tt / h.nxc) + 1, I = (int)(tt % h.nxc);
     const int J = Jl + h.jc0;
     kf[0] = fine_h(h, 2 * I, 2 * J);          // children: fine h(2I, 2J), h(2I+1, 2J)
     kf[1] = fine_h(h, 2 * I + 1, 2 * J);
     ok = kf[0] >= 0 && kf[1] >= 0;
     if (ok) {
       for (int hf = 0; hf < 2; ++hf) {
-        const double r0 = __ldg(rf + 2 * kf[hf]), r1 = __ldg(rf + 2 * kf[hf] + 1);
+        const double r0 = vld<SM>(rf + 2 * kf[hf]), r1 = vld<SM>(rf + 2 * kf[hf] + 1);
         for (int c = 0; c < 2; ++c) acc[c] += h.halves[hf * 4 + 0 * 2 + c] * r0 + h.halves[hf * 4 + 1 * 2 + c] * r1;
       }
-      ok = cross_restrict(h, rf, I, Jl - 1, 2, acc)   // element below: this facet is its TOP side
-           && cross_restrict(h, rf, I, Jl, 0, acc);   // element above: BOTTOM side
+      ok = cross_restrict<SM>(h, rf, I, Jl - 1, 2, acc)   // element below: this facet is its TOP side
+           && cross_restrict<SM>(h, rf, I, Jl, 0, acc);   // element above: BOTTOM side
     }
   } else {          // coarse v(I, Jl)
-    const long long u = t - h.nhc;
+    const IT u = tt - nhc;
     const int I = (int)(u / h.nyc) + 1, Jl = (int)(u % h.nyc);
     const int J = Jl + h.jc0;
     kf[0] = fine_v(h, 2 * I, 2 * J);          // children: fine v(2I, 2J), v(2I, 2J+1)
@@ -1203,15 +1224,21 @@ __global__ void h_restrict_kernel(const HArgs h, const double* __restrict__ rf, 
     ok = kf[0] >= 0 && kf[1] >= 0;
     if (ok) {
       for (int hf = 0; hf < 2; ++hf) {
-        const double r0 = __ldg(rf + 2 * kf[hf]), r1 = __ldg(rf + 2 * kf[hf] + 1);
+        const double r0 = vld<SM>(rf + 2 * kf[hf]), r1 = vld<SM>(rf + 2 * kf[hf] + 1);
         for (int c = 0; c < 2; ++c) acc[c] += h.halves[hf * 4 + 0 * 2 + c] * r0 + h.halves[hf * 4 + 1 * 2 + c] * r1;
       }
-      ok = cross_restrict(h, rf, I - 1, Jl, 1, acc)   // element left: RIGHT side
-           && cross_restrict(h, rf, I, Jl, 3, acc);   // element right: LEFT side
+      ok = cross_restrict<SM>(h, rf, I - 1, Jl, 1, acc)   // element left: RIGHT side
+           && cross_restrict<SM>(h, rf, I, Jl, 3, acc);   // element right: LEFT side
     }
   }
   rc[2 * t] = ok ? acc[0] : 0.0;
   rc[2 * t + 1] = ok ? acc[1] : 0.0;
+}
+
+__global__ void h_restrict_kernel(const HArgs h, const double* __restrict__ rf, double* __restrict__ rc) {
+  const long long nvc = (long long)(h.nxc - 1) * h.nyc;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < h.nhc + nvc) h_restrict_one<false>(h, rf, rc, t);
 }
 
 // ---------------------------------------------------------------------------- small kernels
@@ -1320,6 +1347,231 @@ __global__ void cg_update_kernel(double* __restrict__ x, double* __restrict__ r,
 __global__ void xpby_kernel(const double* __restrict__ z, double beta, double* __restrict__ d, long long n) {
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
     d[t] = fma(beta, d[t], z[t]);
+}
+
+// ------------------------------------------------------------------ fused coarse-level tail
+// The small p = 1 levels at the bottom of a V/W cycle (multigrid.py:393-406) are latency-bound:
+// ~6 dependent launches per level visit, each a few microseconds whatever the level size.  The
+// host turns the tail of the cycle (same recursion, sweep weights and buffer roles as the
+// launch path) into a flat program of facet-parallel ops that ONE CTA runs with every tail
+// vector resident in shared memory and __syncthreads between dependent ops.  Facet applies read
+// their 7 stencil blocks from shared memory and the unreduced merged operators from global
+// (read-only, L1/L2-resident).  Only the entry right-hand side (and, on a repeated visit, the
+// entry iterate) come from global memory, and only the level's result goes back.
+enum TailCode { T_BJ = 0, T_BJZ = 1, T_RES = 2, T_RESTRICT = 3, T_PROLONG = 4, T_COARSE = 5, T_COPY = 6, T_ZERO = 7 };
+
+struct TailLevel {          // one level of the tail (n1 = 2)
+  int nx, ny, nxp, stored;
+  long long nh, nblk;
+  const double* W[2];       // merged n1 x 7n1 operators: shared (7*4 doubles, [q][k][m]) or stored streams
+  const double* D[2];       // block-Jacobi inverses: shared (4 doubles) or stored streams
+  int off[3];               // shared-memory offsets (doubles) of this level's X, T, B vectors
+};
+
+struct TailOp {
+  short code, lev;          // lev: the level (T_RESTRICT / T_PROLONG: the fine level of the link)
+  short x, b, out;          // buffer ids: 3 * level + {0: X, 1: T, 2: B}; -1 unused
+  double w;
+};
+
+constexpr int TAIL_MAXL = 12;
+constexpr int TAIL_MAXOPS = 512;
+constexpr int TAIL_THREADS = 512;
+
+struct __align__(16) TailArgs {
+  TailLevel lev[TAIL_MAXL];
+  HArgs h[TAIL_MAXL];       // h[l]: transfer level l -> l + 1 of the tail
+  const double* Ainv;       // coarsest level: dense inverse (n_c x n_c)
+  const double* b_in;       // entry right-hand side of the top tail level (global)
+  const double* x_in;       // entry iterate of the top tail level (global; nullptr = zero start)
+  double* x_out;            // result of the top tail level (global)
+  int nc, nops, nlev, pad_;
+  TailOp ops[TAIL_MAXOPS];
+};
+
+static_assert(sizeof(TailArgs) % sizeof(uint4) == 0, "TailArgs is copied to shared memory as uint4");
+constexpr int TAIL_ARGS_DOUBLES = (int)(sizeof(TailArgs) / sizeof(double));
+
+// A x restricted to facet bk of level L (n1 = 2, x in shared memory); out-of-mesh / Dirichlet
+// stencil blocks read 0.  32-bit index math: tail levels are small.
+__device__ __forceinline__ void tail_facet_apply(const TailLevel& L, const double* x, int bk, double (&y)[2],
+                                                 int& slot_out, bool& vert_out) {
+  constexpr int N1 = 2;
+  const int nx = L.nx, ny = L.ny, nh = (int)L.nh;
+  const bool vert = bk >= nh;
+  int i, j;
+  if (!vert) { j = bk / nx + 1; i = bk - (j - 1) * nx; }
+  else { const int u = bk - nh; i = u / ny + 1; j = u - (i - 1) * ny; }
+  auto hb = [&](int ii, int jj) -> int { return (ii >= 0 && ii < nx && jj >= 1 && jj <= ny - 1) ? (jj - 1) * nx + ii : -1; };
+  auto vb = [&](int ii, int jj) -> int { return (ii >= 1 && ii <= nx - 1 && jj >= 0 && jj < ny) ? nh + (ii - 1) * ny + jj : -1; };
+  int q[7];
+  if (!vert) {
+    q[0] = hb(i, j - 1); q[1] = bk; q[2] = hb(i, j + 1);
+    q[3] = vb(i, j - 1); q[4] = vb(i + 1, j - 1); q[5] = vb(i, j); q[6] = vb(i + 1, j);
+  } else {
+    q[0] = vb(i - 1, j); q[1] = bk; q[2] = vb(i + 1, j);
+    q[3] = hb(i - 1, j); q[4] = hb(i - 1, j + 1); q[5] = hb(i, j); q[6] = hb(i, j + 1);
+  }
+  const int slot = j * L.nxp + i;
+  const double* W = L.W[vert ? 1 : 0];
+  const int ws = L.stored ? 32 : 1;
+  if (L.stored) W += (size_t)(slot >> 5) * 7 * N1 * N1 * 32 + (slot & 31);
+  y[0] = 0.0; y[1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < 7; ++s) {
+    const double2 v = q[s] >= 0 ? reinterpret_cast<const double2*>(x)[q[s]] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      y[k] = fma(W[((s * N1 + k) * N1 + 0) * ws], v.x, y[k]);
+      y[k] = fma(W[((s * N1 + k) * N1 + 1) * ws], v.y, y[k]);
+    }
+  }
+  slot_out = slot;
+  vert_out = vert;
+}
+
+__device__ __forceinline__ void tail_dinv(const TailLevel& L, bool vert, int slot, const double (&r)[2],
+                                          double (&z)[2]) {
+  const double* D = L.D[vert ? 1 : 0];
+  int st = 1;
+  if (L.stored) { D += (size_t)(slot >> 5) * 4 * 32 + (slot & 31); st = 32; }
+  const double d0 = D[0], d1 = D[st], d2 = D[2 * st], d3 = D[3 * st];
+  z[0] = fma(d0, r[0], d1 * r[1]);
+  z[1] = fma(d2, r[0], d3 * r[1]);
+}
+
+__device__ __forceinline__ int tail_slot(const TailLevel& L, int bk, bool& vert) {
+  const int nh = (int)L.nh;
+  vert = bk >= nh;
+  int i, j;
+  if (!vert) { j = bk / L.nx + 1; i = bk - (j - 1) * L.nx; }
+  else { const int u = bk - nh; i = u / L.ny + 1; j = u - (i - 1) * L.ny; }
+  return j * L.nxp + i;
+}
+
+__global__ void __launch_bounds__(TAIL_THREADS, 1) tail_cycle_kernel(const __grid_constant__ TailArgs Ap) {
+  extern __shared__ __align__(16) double tsm_raw[];
+  const int tid = threadIdx.x;
+  // the program and level descriptors are read on every op: copy them from the parameter
+  // bank (constant-cache misses on a 15 KB block) into shared memory once
+  TailArgs& A = *reinterpret_cast<TailArgs*>(tsm_raw);
+  {
+    constexpr int NW = (int)(sizeof(TailArgs) / sizeof(uint4));
+    const uint4* src = reinterpret_cast<const uint4*>(&Ap);
+    uint4* dst = reinterpret_cast<uint4*>(tsm_raw);
+    for (int t = tid; t < NW; t += TAIL_THREADS) dst[t] = src[t];
+  }
+  __syncthreads();
+  // shared-mode operators (64 doubles per level) next to the program; stored streams stay global
+  double* opsm = tsm_raw + TAIL_ARGS_DOUBLES;
+  for (int l = 0; l < A.nlev; ++l) {
+    if (A.lev[l].stored) continue;
+    const double* src = A.lev[l].W[0];   // Wh, Wv, Dh, Dv contiguous (hdg_capi.cu: tail_wd)
+    for (int t = tid; t < 64; t += TAIL_THREADS) opsm[64 * l + t] = __ldg(src + t);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int l = 0; l < A.nlev; ++l) {
+      if (A.lev[l].stored) continue;
+      double* o = opsm + 64 * l;
+      A.lev[l].W[0] = o; A.lev[l].W[1] = o + 28; A.lev[l].D[0] = o + 56; A.lev[l].D[1] = o + 60;
+    }
+  }
+  __syncthreads();
+  double* tsm = opsm + 64 * TAIL_MAXL;
+  auto buf = [&](int id) -> double* { return tsm + A.lev[id / 3].off[id % 3]; };
+  {  // entry: b (and x) of the top tail level
+    const long long n0 = 2 * A.lev[0].nblk;
+    double* b0 = buf(2);
+    double* x0 = buf(0);
+    for (long long t = tid; t < n0; t += TAIL_THREADS) {
+      b0[t] = A.b_in[t];
+      if (A.x_in) x0[t] = A.x_in[t];
+    }
+  }
+  __syncthreads();
+  for (int o = 0; o < A.nops; ++o) {
+    const TailOp& op = A.ops[o];
+    const TailLevel& L = A.lev[op.lev];
+    switch (op.code) {
+      case T_BJ:
+      case T_RES: {
+        const double* x = buf(op.x);
+        const double* b = buf(op.b);
+        double* out = buf(op.out);
+        for (int bk = tid; bk < (int)L.nblk; bk += TAIL_THREADS) {
+          double y[2];
+          int slot;
+          bool vert;
+          tail_facet_apply(L, x, bk, y, slot, vert);
+          const double r[2] = {b[2 * bk] - y[0], b[2 * bk + 1] - y[1]};
+          if (op.code == T_RES) {
+            out[2 * bk] = r[0]; out[2 * bk + 1] = r[1];
+          } else {
+            double z[2];
+            tail_dinv(L, vert, slot, r, z);
+            out[2 * bk] = fma(op.w, z[0], x[2 * bk]);
+            out[2 * bk + 1] = fma(op.w, z[1], x[2 * bk + 1]);
+          }
+        }
+        break;
+      }
+      case T_BJZ: {
+        const double* b = buf(op.b);
+        double* out = buf(op.out);
+        for (int bk = tid; bk < (int)L.nblk; bk += TAIL_THREADS) {
+          bool vert;
+          const int slot = tail_slot(L, bk, vert);
+          const double r[2] = {b[2 * bk], b[2 * bk + 1]};
+          double z[2];
+          tail_dinv(L, vert, slot, r, z);
+          out[2 * bk] = op.w * z[0];
+          out[2 * bk + 1] = op.w * z[1];
+        }
+        break;
+      }
+      case T_RESTRICT: {
+        const HArgs& h = A.h[op.lev];
+        const int nc = (int)(h.nhc + (long long)(h.nxc - 1) * h.nyc);
+        for (int t = tid; t < nc; t += TAIL_THREADS) h_restrict_one<true>(h, buf(op.x), buf(op.out), t);
+        break;
+      }
+      case T_PROLONG: {
+        const HArgs& h = A.h[op.lev];
+        const int nf = (int)(h.nhf + (long long)(2 * h.nxc - 1) * h.nyf);
+        for (int t = tid; t < nf; t += TAIL_THREADS) h_prolong_add_one<true>(h, buf(op.x), buf(op.out), t);
+        break;
+      }
+      case T_COARSE: {   // warp per row of the dense inverse (multigrid.py:209-212)
+        const int lane = tid & 31;
+        const double* b = buf(op.b);
+        double* out = buf(op.out);
+        for (int row = tid >> 5; row < A.nc; row += TAIL_THREADS / 32) {
+          double acc = 0.0;
+          for (int c = lane; c < A.nc; c += 32) acc = fma(__ldg(A.Ainv + (size_t)row * A.nc + c), b[c], acc);
+#pragma unroll
+          for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
+          if (lane == 0) out[row] = acc;
+        }
+        break;
+      }
+      case T_COPY: {
+        const double* x = buf(op.x);
+        double* out = buf(op.out);
+        for (long long t = tid; t < 2 * L.nblk; t += TAIL_THREADS) out[t] = x[t];
+        break;
+      }
+      default: {  // T_ZERO
+        double* out = buf(op.out);
+        for (long long t = tid; t < 2 * L.nblk; t += TAIL_THREADS) out[t] = 0.0;
+        break;
+      }
+    }
+    __syncthreads();
+  }
+  const long long n0 = 2 * A.lev[0].nblk;
+  const double* x0 = buf(0);
+  for (long long t = tid; t < n0; t += TAIL_THREADS) A.x_out[t] = x0[t];
 }
 
 }  // namespace hdg

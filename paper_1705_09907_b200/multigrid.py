@@ -467,6 +467,12 @@ class _NativeMG:
 _MG_CACHE = {}
 
 
+def set_fused_tail(levels, enable=True):
+    """Run the small trailing p = 1 levels of the device cycle as one cooperative kernel
+    (default) or as separate launches (hdgb200.h: hdg_mg_set_fused_tail)."""
+    check(lib.hdg_mg_set_fused_tail(_native_mg(levels).handle, int(bool(enable))))
+
+
 def _native_mg(levels):
     key = tuple(id(lev) for lev in levels)
     mg = _MG_CACHE.get(key)

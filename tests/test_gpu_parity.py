@@ -442,3 +442,39 @@ def test_reconstruct_postprocess_gpu_condensed(P, aniso):
     qo, uo = O.reconstruct_all(o, lam)
     assert rel(q, qo) < 1e-11 and rel(u, uo) < 1e-11
     assert rel(s.postprocess_all(q, u), O.postprocess_all(o, qo, uo)) < 1e-11
+
+
+@pytest.mark.parametrize("case", ["cfg1", "hetero_w", "p1_rect"])
+def test_fused_coarse_tail_matches_launch_path(P, case):
+    """The trailing small p = 1 levels run as one cooperative kernel: same cycle as the
+    per-launch path (to rounding) and as the oracle (1e-12)."""
+    if case == "cfg1":
+        levels = P.mg.build_hierarchy(P.mesh(64, 64), 2, P.pb.config1_problem(), smoother=None)[:6]
+        P.mg.attach_smoothers(levels, "blockjacobi", 0.8)
+        grid, ospec = O.config1_system(64, 2)
+        olevels = O.build_levels(grid, 2, ospec, smoother="blockjacobi")[:6]
+        visits = 1
+    elif case == "hetero_w":
+        Kg = specs.hetero_K(16, seed=5)
+        spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+        levels = P.mg.build_hierarchy(P.mesh(16, 16), 2, spec, smoother="blockjacobi", omega=0.8)
+        olevels = O.build_levels(O.Grid(16, 16), 2, O.Spec(O.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0),
+                                 smoother="blockjacobi")
+        visits = 2
+    else:
+        spec, ospec = specs.manufactured(P.pb.ProblemSpec), specs.manufactured(O.Spec)
+        levels = P.mg.build_hierarchy(P.mesh(32, 16), 1, spec, smoother="blockjacobi", omega=0.8)
+        olevels = O.build_levels(O.Grid(32, 16), 1, ospec, smoother="blockjacobi")
+        visits = 1
+    b = np.random.default_rng(3).uniform(-1, 1, levels[0].ndof)
+    run = P.mg.v_cycle if visits == 1 else P.mg.w_cycle
+    P.mg.set_fused_tail(levels, True)
+    xf = run(levels, b)
+    xf2 = run(levels, b, xf)                 # second cycle from a nonzero guess (replayed graph)
+    P.mg.set_fused_tail(levels, False)
+    xl = run(levels, b)
+    xl2 = run(levels, b, xl)
+    P.mg.set_fused_tail(levels, True)
+    assert rel(xf, xl) < 1e-13 and rel(xf2, xl2) < 1e-13
+    xo = O.cycle(olevels, 0, b, np.zeros_like(b), 2, 2, visits)
+    assert rel(xf, xo) < TOL
