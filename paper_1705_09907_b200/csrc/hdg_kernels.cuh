@@ -199,7 +199,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   }
   __trap();
 }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+#ifndef HDG_EXP_NOFENCE
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+#endif
+}
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
@@ -309,7 +313,24 @@ __device__ __forceinline__ void stage_tile(const MvArgs& a, double* buf, int i0,
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)));
   return;
 #endif
+#ifdef HDG_EXP_BIGH
+  // experiment: the same H bytes as ONE contiguous bulk copy (wrong data; measures per-copy cost)
+  if (threadIdx.x == 0) {
+    const unsigned hb = (unsigned)((C::HROWS * C::HCOLS * N1 * 8) & ~15);
+    const long long tiles = (long long)((a.nx + TX - 1) / TX) * ((a.ny + C::TY - 1) / C::TY);
+    const long long t = (long long)(j0 / C::TY) * ((a.nx + TX - 1) / TX) + i0 / TX;
+    const long long maxoff = ((long long)a.nh * N1 * 8 - hb) & ~15LL;
+    const long long off = (maxoff * t / (tiles > 1 ? tiles - 1 : 1)) & ~15LL;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(bar, hb);
+    tma_load_1d(buf, reinterpret_cast<const char*>(a.x) + off, hb, bar);
+  } else if (lane == 0) {
+    mbar_arrive_expect_tx(bar, 0);
+  }
+  if (false) {
+#else
   if (lane == 0) {
+#endif
     unsigned bytes = 0;
 #ifndef HDG_EXP_NOH
     for (int r = warp; r < C::HROWS; r += NWARP) bytes += run_bytes(h_run<N1, ST>(a, i0, j0, r));
@@ -616,6 +637,9 @@ template <int N1, int NO>
 __device__ __forceinline__ void store_h_row(const MvArgs& a, double* scr, int i0, int j, const double (&o)[N1],
                                             int lane) {
   if (a.out == nullptr || j < 1 || j > a.ny - 1) return;  // warp-uniform
+#ifdef HDG_EXP_NOHSTORE
+  if (a.nx > 0) return;
+#endif
 #pragma unroll
   for (int k = 0; k < NO; ++k) scr[lane * NO + k] = o[k];
   __syncwarp();
