@@ -63,6 +63,9 @@ namespace cg = cooperative_groups;
 #ifndef HDG_NWARP
 #define HDG_NWARP 8
 #endif
+#ifndef HDG_HDIRECT
+#define HDG_HDIRECT 0      // shared mode h-facet outputs: 1 = direct stores, 0 = warp transpose
+#endif
 #ifndef HDG_SHARED_SYM
 #define HDG_SHARED_SYM 1   // shared mode: mirror-reduced stencil (apply_shared_sym); 0 = full n1 x 7n1
 #endif
@@ -639,6 +642,15 @@ __device__ __forceinline__ void store_h_row(const MvArgs& a, double* scr, int i0
   if (a.out == nullptr || j < 1 || j > a.ny - 1) return;  // warp-uniform
 #ifdef HDG_EXP_NOHSTORE
   if (a.nx > 0) return;
+#endif
+#if HDG_HDIRECT
+  // direct stride-n1 stores from registers (no shared-memory transpose)
+  if (i0 + lane < a.nx) {
+    double* d = a.out + (hblk(a.nx, i0, j) + lane) * NO;
+#pragma unroll
+    for (int k = 0; k < NO; ++k) d[k] = o[k];
+  }
+  return;
 #endif
 #pragma unroll
   for (int k = 0; k < NO; ++k) scr[lane * NO + k] = o[k];
