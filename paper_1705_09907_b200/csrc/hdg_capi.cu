@@ -2,6 +2,10 @@
 // the device-resident multigrid cycle and its CUDA-graph cache.
 // Reference interfaces replaced: see include/hdgb200.h (each entry cites trace.py / multigrid.py).
 #include "hdgb200.h"
+#ifndef HDG_WS
+#define HDG_WS 0
+#endif
+#define HDG_WS_KERNEL HDG_WS
 #include "hdg_kernels.cuh"
 
 #include <algorithm>
@@ -109,9 +113,7 @@ static void host_invert(std::vector<double>& a, int n) {  // SPD Gauss-Jordan, n
   }
 }
 
-#ifndef HDG_WS
-#define HDG_WS 0
-#endif
+
 // warp-specialized (producer warp + compute warps) or uniform kernel
 template <int N1, bool STORED, int EPI>
 static auto kernel_ptr() {
@@ -122,7 +124,7 @@ static constexpr int kThreads = HDG_WS ? NT + 32 : NT;
 
 template <int N1, bool STORED, int EPI>
 static int set_attr() {
-  const size_t smem = Cfg<N1, STORED>::smem_doubles(STORED) * sizeof(double);
+  const size_t smem = Cfg<N1, STORED>::template smem_doubles_epi<EPI>() * sizeof(double);
   CK(cudaFuncSetAttribute(kernel_ptr<N1, STORED, EPI>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   return 0;
 }
@@ -153,7 +155,7 @@ static int grid_for(const hdg_level* L) {
   using C = Cfg<N1, STORED>;
   static int occ = -1;
   if (occ < 0) {
-    const size_t smem = C::smem_doubles(STORED) * sizeof(double);
+    const size_t smem = C::template smem_doubles_epi<EPI>() * sizeof(double);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel_ptr<N1, STORED, EPI>(), kThreads, smem) !=
             cudaSuccess || occ < 1)
       occ = 1;
@@ -167,7 +169,7 @@ static int grid_for(const hdg_level* L) {
 template <int N1, bool STORED, int EPI>
 static int apply_t(const hdg_level* L, MvArgs& a, cudaStream_t s) {
   using C = Cfg<N1, STORED>;
-  const size_t smem = C::smem_doubles(STORED) * sizeof(double);
+  const size_t smem = C::template smem_doubles_epi<EPI>() * sizeof(double);
   const int grid = grid_for<N1, STORED, EPI>(L);
   SharedOp<(STORED ? 1 : N1)> op;
   if constexpr (!STORED) {

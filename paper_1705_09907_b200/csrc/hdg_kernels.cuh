@@ -66,6 +66,9 @@ namespace cg = cooperative_groups;
 #ifndef HDG_HDIRECT
 #define HDG_HDIRECT 0      // shared mode h-facet outputs: 1 = direct stores, 0 = warp transpose
 #endif
+#ifndef HDG_WS_KERNEL
+#define HDG_WS_KERNEL 0    // set by hdg_capi.cu when the warp-specialised kernel is selected (HDG_WS)
+#endif
 #ifndef HDG_SHARED_SYM
 #define HDG_SHARED_SYM 1   // shared mode: mirror-reduced stencil (apply_shared_sym); 0 = full n1 x 7n1
 #endif
@@ -115,7 +118,21 @@ template <int N1, bool ST = false> struct Cfg {
   static constexpr int KS = (7 * N1 + 3) / 4;                             // DMMA k-steps (K = 7 n1)
   static constexpr int WSCR = DMMA ? 32 * 9 : 32 * NOUT;                  // per-warp output transpose
   // shared mode adds the per-warp transpose scratch; stored mode stages h outputs in BUF
-  static constexpr int smem_doubles(bool stored) { return NBUF * BUF + (stored ? 0 : (NWARP + 1) * WSCR); }
+  // Residual / Jacobi / restriction epilogues need b of the tile's own facets.  h-facet rows are
+  // contiguous runs (loaded coalesced through the warp scratch); the v-facet columns would be
+  // one scattered 40-byte piece per lane, so they are staged with the tile, transposed like x
+  // ([row][column], odd block stride), when two CTAs per SM still fit.
+  static constexpr int SB = (N1 & 1) ? N1 : N1 + 1;
+  static constexpr int BSZ = ((TY * TX * SB) + 1) & ~1;
+  __host__ __device__ static constexpr int base_doubles(bool stored) { return NBUF * BUF + (stored ? 0 : (NWARP + 1) * WSCR); }
+  template <int EPI> __host__ __device__ static constexpr bool stage_b() {
+    return EPI != 0 && !HDG_WS_KERNEL && (base_doubles(ST) + NBUF * BSZ) * 8 <= 113 * 1024;
+  }
+  template <int EPI> __host__ __device__ static constexpr int bufs() { return BUF + (stage_b<EPI>() ? BSZ : 0); }   // stage stride
+  template <int EPI> __host__ __device__ static constexpr int smem_doubles_epi() {
+    return NBUF * bufs<EPI>() + (ST ? 0 : (NWARP + 1) * WSCR);
+  }
+  static constexpr int smem_doubles(bool stored) { return base_doubles(stored); }
 };
 
 // Shared-mode operator: both merged facet matrices + block-Jacobi inverses, passed by value
@@ -306,7 +323,30 @@ __device__ __forceinline__ void stage_v_columns(const MvArgs& a, double* Vs, int
 // most two 8-byte LDGSTS for a misaligned head/tail.  Completion: `bar` (2 arrivals per warp).
 //   H region: h(i, j), i in [i0-1, i0+TX), j in [j0-1, j0+TY]      ((TY+2) x (TX+1) blocks)
 //   V region: v(i, j), i in [i0-1, i0+TX], j in [j0-1, j0+TY)      ((TX+2) x (TY+1) blocks)
+// b of the tile's own v facets v(i0 + c, j0 .. j0 + TY - 1), c < TX: one contiguous run per
+// column, copied by coalesced 8-byte LDGSTS and transposed into [row][column] (stride SB, odd)
 template <int N1, bool ST>
+__device__ __forceinline__ void stage_b_columns(const MvArgs& a, double* Bs, int i0, int j0, int warp, int lane) {
+  using C = Cfg<N1, ST>;
+  constexpr int LEN = C::TY * N1;
+  constexpr int NQ = (LEN + 31) / 32;
+  const int ehi = min(C::TY, a.ny - j0) * N1;
+  for (int c = warp; c < TX; c += NWARP) {
+    const int i = i0 + c;
+    if (i < 1 || i > a.nx - 1) continue;   // warp-uniform; never read for these columns
+    const double* src = a.b + (long long)vblk(a.nh, a.ny, i, j0) * N1;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int e = lane + 32 * q;
+      if (e < ehi) {
+        const int r = e / N1, m = e - r * N1;
+        cp_async8(Bs + (r * TX + c) * C::SB + m, src + e, true);
+      }
+    }
+  }
+}
+
+template <int N1, bool ST, bool SBV = false>
 __device__ __forceinline__ void stage_tile(const MvArgs& a, double* buf, int i0, int j0, uint64_t* bar) {
   using C = Cfg<N1, ST>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -352,6 +392,7 @@ __device__ __forceinline__ void stage_tile(const MvArgs& a, double* buf, int i0,
 #ifndef HDG_EXP_NOV
   stage_v_columns<N1, ST>(a, buf + C::HSZ, i0, j0, warp, NWARP, lane);
 #endif
+  if constexpr (SBV) stage_b_columns<N1, ST>(a, buf + C::BUF, i0, j0, warp, lane);
   cp_async_mbar_arrive(bar);           // every thread: one arrival when its LDGSTS land
 }
 
@@ -762,7 +803,9 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
       for (int f = 0; f < F; ++f) {
         const int j = j0 + F * w + f;
         if (i >= 1 && i <= a.nx - 1 && j < a.ny)
-          facet_epilogue<N1, false, EPI>(a, vblk(a.nh, a.ny, i, j), nb[f][1], op.Dv, nullptr, acc[f], ov[f], nrm);
+          facet_epilogue<N1, false, EPI>(a, vblk(a.nh, a.ny, i, j), nb[f][1], op.Dv, nullptr, acc[f], ov[f], nrm,
+                                         C::template stage_b<EPI>() ? buf + C::BUF + ((F * w + f) * TX + tx) * C::SB
+                                                                    : nullptr);
       }
     } else {
 #pragma unroll
@@ -774,7 +817,9 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
           apply_stored<N1>(nb[f], a.Wv + (size_t)grp * C::WSZ * 32 + tx, acc);
           if (i >= 1 && i <= a.nx - 1)
             facet_epilogue<N1, true, EPI>(a, vblk(a.nh, a.ny, i, j), nb[f][1], nullptr,
-                                          a.Dv + (size_t)grp * C::DSZ * 32 + tx, acc, ov[f], nrm);
+                                          a.Dv + (size_t)grp * C::DSZ * 32 + tx, acc, ov[f], nrm,
+                                          C::template stage_b<EPI>() ? buf + C::BUF + ((F * w + f) * TX + tx) * C::SB
+                                                                     : nullptr);
         }
       }
     }
@@ -840,6 +885,8 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
   const int tiles_x = (a.nx + TX - 1) / TX;
   const int ntiles = tiles_x * ((a.ny + C::TY - 1) / C::TY);
   constexpr int NB = C::NBUF;
+  constexpr bool SBV = C::template stage_b<EPI>();
+  constexpr int BS = C::template bufs<EPI>();
   __shared__ __align__(8) uint64_t bars[NB];
   double nrm = 0.0;
   if (threadIdx.x == 0) {
@@ -852,7 +899,8 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
 #pragma unroll
   for (int q = 0; q < NB - 1; ++q) {
     const int t = blockIdx.x + q * gridDim.x;
-    if (t < ntiles) stage_tile<N1, STORED>(a, smem + q * C::BUF, (t % tiles_x) * TX, (t / tiles_x) * C::TY, &bars[q]);
+    if (t < ntiles)
+      stage_tile<N1, STORED, SBV>(a, smem + q * BS, (t % tiles_x) * TX, (t / tiles_x) * C::TY, &bars[q]);
   }
   int slot = 0;
   unsigned phase = 0;
@@ -860,11 +908,11 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
     const int pre = tile + (NB - 1) * gridDim.x;
     if (pre < ntiles) {
       const int ps = (slot + NB - 1) % NB;
-      stage_tile<N1, STORED>(a, smem + ps * C::BUF, (pre % tiles_x) * TX, (pre / tiles_x) * C::TY, &bars[ps]);
+      stage_tile<N1, STORED, SBV>(a, smem + ps * BS, (pre % tiles_x) * TX, (pre / tiles_x) * C::TY, &bars[ps]);
     }
     mbar_wait(&bars[slot], phase);
     __syncthreads();
-    compute_tile<N1, STORED, EPI>(a, op, smem + slot * C::BUF, smem + NB * C::BUF + (threadIdx.x >> 5) * C::WSCR,
+    compute_tile<N1, STORED, EPI>(a, op, smem + slot * BS, smem + NB * BS + (threadIdx.x >> 5) * C::WSCR,
                                   (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
     __syncthreads();
     if (++slot == NB) { slot = 0; phase ^= 1u; }
