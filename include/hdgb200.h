@@ -126,10 +126,12 @@ int hdg_mg_create(hdg_level* const* levels, hdg_transfer* const* transfers, int 
 int hdg_mg_destroy(hdg_mg* mg);
 /* coarsest-level inverse, n x n row-major HOST pointer, n = ndof of the last level */
 int hdg_mg_set_coarse_inverse(hdg_mg* mg, const double* inv, int64_t n);
-/* Fused coarse tail (default on): the trailing p = 1, block-Jacobi-smoothed, h-linked levels
- * of <= 70k dofs run as ONE cooperative kernel with grid barriers between dependent steps
- * (same recursion, buffers and weights as the per-launch cycle, multigrid.py:393-406).
- * enable = 0 issues them as separate launches (A/B timing, parity tests). */
+/* Cycle fusions (default on): (1) the trailing p = 1, block-Jacobi-smoothed, h-linked levels
+ * whose top level has <= 2048 dofs run as ONE single-CTA shared-memory kernel; (2) on
+ * constant-coefficient levels the first two Jacobi steps from x = 0 run as one trace kernel
+ * (x1 = w1 D^-1 b formed on the staged tile).  Same recursion, buffers and weights as the
+ * per-launch cycle (multigrid.py:393-406).  enable = 0 issues everything as separate launches
+ * (A/B timing, parity tests). */
 int hdg_mg_set_fused_tail(hdg_mg* mg, int enable);
 /* x = cycle(b, x0) with nu1/nu2 smoothing sweeps (FSAI if attached to the level, else
  * block-Jacobi), visits = 1 (V) or 2 (W).

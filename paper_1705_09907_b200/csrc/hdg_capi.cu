@@ -94,6 +94,7 @@ struct hdg_mg {
   std::map<std::tuple<const void*, const void*, void*, int, int, int>, GraphEntry> graphs;
   int tail_k0 = -1;              // first level of the fused coarse tail (-1: none)
   bool tail_enabled = true;
+  bool fuse_first = true;        // first two Jacobi steps from x = 0 in one kernel (shared levels)
 };
 
 // ------------------------------------------------------------------------------ helpers
@@ -810,6 +811,7 @@ int hdg_mg_destroy(hdg_mg* mg) {
 int hdg_mg_set_fused_tail(hdg_mg* mg, int enable) {
   if (!mg) return fail(HDG_EINVAL, "null mg");
   mg->tail_enabled = enable != 0;
+  mg->fuse_first = enable != 0;
   for (auto& kv : mg->graphs) cudaGraphExecDestroy(kv.second.exec);
   mg->graphs.clear();
   return 0;
@@ -1000,7 +1002,15 @@ static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1
   const bool fsai = L->use_fsai;   // the smoother attached last (FSAI or block-Jacobi)
   int first = 0;
   if (zero_init && L->ndof > 0) {
-    if (!fsai && nu1 >= 1) {
+    if (!fsai && nu1 >= 2 && !L->stored && mg->fuse_first) {
+      // x = 0: x_1 = w1 D^-1 b is formed on the staged tile of b inside the second sweep's
+      // kernel (one pass instead of bj_zero + sweep)
+      MvArgs a{};
+      a.x = b; a.b = b; a.out = oth; a.w_first = bj_weight(L, 1, nu1);
+      if ((rc = apply(L, EPI_BJ, a, s, bj_weight(L, 2, nu1)))) return rc;
+      std::swap(cur, oth);
+      first = 2;
+    } else if (!fsai && nu1 >= 1) {
       // x = 0: the first Jacobi step needs no operator apply (x_1 = w D^-1 b)
       if ((rc = bj_sweep_zero(L, b, oth, bj_weight(L, 1, nu1), s))) return rc;
       std::swap(cur, oth);

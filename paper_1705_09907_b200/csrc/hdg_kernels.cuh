@@ -155,6 +155,7 @@ struct MvArgs {
   const double* Dh;         // stored mode: interleaved D^-1 [grp][idx][lane]
   const double* Dv;
   double omega;
+  double w_first;           // EPI_BJ, shared mode: staged x holds b; x1 = w_first D^-1 b first (0: off)
   double* partials;         // per-CTA norm^2 partials (RES) or nullptr
   double V[MAXN1 * (MAXN1 - 1)];  // RESPR: fine x coarse p-transfer matrix, row-major
 };
@@ -718,6 +719,34 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
   const int hpar0 = h_run_start<N1>(a, i0, j0, 0), hstep = a.nx * N1;
   auto H = [&](int r, int c) { return Hs + r * C::RS + ((hpar0 + r * hstep) & 1) + c * C::S; };
   auto V = [&](int c, int r) { return Vs + (r * C::VCOLS + c) * C::SV; };
+  if constexpr (!STORED && EPI == EPI_BJ) {
+    if (a.w_first != 0.0) {
+      // Two Jacobi steps from x = 0 in one pass (multigrid.py:400 then the first sweep): the
+      // tile was staged from b, so every staged block becomes x1 = w1 D^-1 b in place
+      // (Dirichlet / outside blocks are 0 and stay 0), then the sweep below runs on x1.
+      auto dmul = [&](double* blk, const double* D) {
+        double r[N1];
+#pragma unroll
+        for (int k = 0; k < N1; ++k) r[k] = blk[k];
+#pragma unroll
+        for (int k = 0; k < N1; ++k) {
+          double s = 0.0;
+#pragma unroll
+          for (int m = 0; m < N1; ++m) s = fma(D[k * N1 + m], r[m], s);
+          blk[k] = a.w_first * s;
+        }
+      };
+      for (int t = threadIdx.x; t < C::HROWS * C::HCOLS; t += NT) {
+        const int r = t / C::HCOLS, c = t - r * C::HCOLS;
+        dmul(const_cast<double*>(H(r, c)), op.Dh);
+      }
+      for (int t = threadIdx.x; t < C::VROWS * C::VCOLS; t += NT) {
+        const int r = t / C::VCOLS, c = t - r * C::VCOLS;
+        dmul(const_cast<double*>(V(c, r)), op.Dv);
+      }
+      consumer_sync();
+    }
+  }
   double ov[F][N1];
   double ohs[STORED ? F : 1][N1];   // stored mode: h outputs wait for the CTA-staged write
   // ---- horizontal facets: owners (i, j-1) [TOP rows] and (i, j) [BOTTOM rows]
