@@ -1039,11 +1039,23 @@ static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1
   }
   for (int v = 0; v < visits; ++v)
     if ((rc = cycle_rec(mg, k + 1, mg->B[k + 1], v == 0, nu1, nu2, visits, s))) return rc;
-  if ((rc = hdg_prolong_add(T, mg->X[k + 1], cur, s))) return rc;
+  int post0 = 0;
+  if (!T->is_h && !fsai && nu2 >= 1 && mg->fuse_first) {
+    // p-prolongation fused into the first post-smoothing sweep: x + V e_c is formed on the
+    // staged tile and never stored
+    MvArgs a{};
+    a.x = cur; a.b = b; a.out = oth; a.pec = mg->X[k + 1];
+    std::memcpy(a.V, T->pa.V, sizeof(a.V));
+    if ((rc = apply(L, EPI_BJ, a, s, bj_weight(L, 1, nu2)))) return rc;
+    std::swap(cur, oth);
+    post0 = 1;
+  } else if ((rc = hdg_prolong_add(T, mg->X[k + 1], cur, s))) {
+    return rc;
+  }
   if (fsai) {
     if ((rc = fsai_sweeps(L, b, cur, mg->R[k], oth, nu2, s))) return rc;
   } else {
-    for (int it = 0; it < nu2; ++it) {
+    for (int it = post0; it < nu2; ++it) {
       if ((rc = bj_sweep_w(L, b, cur, oth, bj_weight(L, it + 1, nu2), s))) return rc;
       std::swap(cur, oth);
     }

@@ -156,6 +156,7 @@ struct MvArgs {
   const double* Dv;
   double omega;
   double w_first;           // EPI_BJ, shared mode: staged x holds b; x1 = w_first D^-1 b first (0: off)
+  const double* pec;        // EPI_BJ: coarse p-level vector; staged x becomes x + V ec first (null: off)
   double* partials;         // per-CTA norm^2 partials (RES) or nullptr
   double V[MAXN1 * (MAXN1 - 1)];  // RESPR: fine x coarse p-transfer matrix, row-major
 };
@@ -743,6 +744,37 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
       for (int t = threadIdx.x; t < C::VROWS * C::VCOLS; t += NT) {
         const int r = t / C::VCOLS, c = t - r * C::VCOLS;
         dmul(const_cast<double*>(V(c, r)), op.Dv);
+      }
+      consumer_sync();
+    }
+  }
+  if constexpr (EPI == EPI_BJ && N1 >= 2) {
+    if (a.pec != nullptr) {
+      // Prolongation fused into the first post-smoothing sweep (multigrid.py:403 then 405):
+      // every staged real facet block becomes x + V ec (p-transfer, facet-local), so the
+      // prolonged iterate is never written to memory.  Dirichlet / outside blocks stay 0.
+      constexpr int NC = N1 - 1;
+      auto padd = [&](double* blk, long long cb) {
+        double e[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) e[c] = __ldg(a.pec + cb * NC + c);
+#pragma unroll
+        for (int k = 0; k < N1; ++k) {
+          double s = blk[k];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) s = fma(a.V[k * NC + c], e[c], s);
+          blk[k] = s;
+        }
+      };
+      for (int t = threadIdx.x; t < C::HROWS * C::HCOLS; t += NT) {
+        const int r = t / C::HCOLS, c = t - r * C::HCOLS;
+        const int ig = i0 - 1 + c, jg = j0 - 1 + r;
+        if (ig >= 0 && ig < a.nx && jg >= 1 && jg <= a.ny - 1) padd(const_cast<double*>(H(r, c)), hblk(a.nx, ig, jg));
+      }
+      for (int t = threadIdx.x; t < C::VROWS * C::VCOLS; t += NT) {
+        const int c = t / C::VROWS, r = t - c * C::VROWS;   // consecutive threads walk a column
+        const int ig = i0 - 1 + c, jg = j0 - 1 + r;
+        if (ig >= 1 && ig <= a.nx - 1 && jg >= 0 && jg < a.ny) padd(const_cast<double*>(V(c, r)), vblk(a.nh, a.ny, ig, jg));
       }
       consumer_sync();
     }
