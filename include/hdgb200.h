@@ -87,6 +87,15 @@ int hdg_level_set_fsai(hdg_level* lev, int64_t n, const int32_t* g_rowptr, const
                        const double* g_vals, int64_t nnz, const int32_t* gt_rowptr,
                        const int32_t* gt_cols, const double* gt_vals, double lam_max,
                        double cheb_fraction, double omega);
+/* fsai_build's row solves (multigrid.py:133-152) on the device: for every row i of the
+ * lower-triangular pattern (g_ptr/g_col, sorted, diagonal last; DEVICE arrays) solve
+ * A[P_i, P_i] g = e_last by Cholesky and write g / sqrt(g_last) into g_val.  A in CSR on the
+ * device (int32, sorted).  max_len >= the longest pattern row (<= 96).  *bad_row = the first
+ * row whose principal block is not SPD (NotSPDError, multigrid.py:34), else -1.  Synchronises
+ * the stream. */
+int hdg_fsai_rows(int64_t n, const int32_t* a_ptr, const int32_t* a_col, const double* a_val,
+                  const int32_t* g_ptr, const int32_t* g_col, double* g_val, int32_t max_len,
+                  int64_t* bad_row, void* stream);
 /* z = G'(G r)  (multigrid.py:72-74) */
 int hdg_fsai_apply(const hdg_level* lev, const double* r, double* z, void* stream);
 /* `steps` Chebyshev-weighted sweeps x <- x + w_k G'G(b - A x) in place (multigrid.py:83-88);

@@ -46,3 +46,7 @@ def empty(n):
 
 def zeros(n):
     return torch.zeros(int(n), dtype=torch.float64, device="cuda")
+
+
+def cuda_available():
+    return torch.cuda.is_available()

@@ -16,6 +16,7 @@ c_double_p = ctypes.POINTER(ctypes.c_double)
 c_void_p = ctypes.c_void_p
 c_int = ctypes.c_int
 c_int64 = ctypes.c_int64
+c_int32 = ctypes.c_int32
 
 # (name, restype, argtypes) - mirrors include/hdgb200.h exactly
 SIGNATURES = [
@@ -50,6 +51,8 @@ SIGNATURES = [
     ("hdg_mg_destroy", c_int, [c_void_p]),
     ("hdg_mg_set_coarse_inverse", c_int, [c_void_p, c_void_p, c_int64]),
     ("hdg_mg_set_fused_tail", c_int, [c_void_p, c_int]),
+    ("hdg_fsai_rows", c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
+                              ctypes.POINTER(c_int64), c_void_p]),
     ("hdg_mg_cycle", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
                              c_void_p]),
     ("hdg_coarse_solve", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -9,6 +9,7 @@
 #include "hdg_kernels.cuh"
 
 #include <algorithm>
+#include <climits>
 #include <atomic>
 #define _USE_MATH_DEFINES
 #include <cmath>
@@ -576,6 +577,38 @@ static int upload(T** dst, const T* src, size_t n) {
   return 0;
 }
 extern "C" {
+
+int hdg_fsai_rows(int64_t n, const int32_t* a_ptr, const int32_t* a_col, const double* a_val, const int32_t* g_ptr,
+                  const int32_t* g_col, double* g_val, int32_t max_len, int64_t* bad_row, void* stream) {
+  if (n < 0 || !bad_row) return fail(HDG_EINVAL, "bad arguments");
+  if (n == 0) { *bad_row = -1; return 0; }
+  long long* dbad = nullptr;
+  CK(cudaMalloc(&dbad, sizeof(long long)));
+  const long long init = LLONG_MAX;
+  CK(cudaMemcpyAsync(dbad, &init, sizeof(long long), cudaMemcpyHostToDevice, S(stream)));
+  const int bs = 128;
+  const unsigned grid = (unsigned)((n + bs - 1) / bs);
+  int rc = 0;
+  if (max_len <= 24) fsai_rows_kernel<24><<<grid, bs, 0, S(stream)>>>(n, a_ptr, a_col, a_val, g_ptr, g_col, g_val, dbad);
+  else if (max_len <= 40) fsai_rows_kernel<40><<<grid, bs, 0, S(stream)>>>(n, a_ptr, a_col, a_val, g_ptr, g_col, g_val, dbad);
+  else if (max_len <= 64) fsai_rows_kernel<64><<<grid, bs, 0, S(stream)>>>(n, a_ptr, a_col, a_val, g_ptr, g_col, g_val, dbad);
+  else if (max_len <= 96) fsai_rows_kernel<96><<<grid, bs, 0, S(stream)>>>(n, a_ptr, a_col, a_val, g_ptr, g_col, g_val, dbad);
+  else rc = fail(HDG_EINVAL, "FSAI pattern rows longer than 96 entries");
+  if (!rc) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = fail(HDG_ECUDA, std::string("fsai rows: ") + cudaGetErrorString(e));
+  }
+  long long hb = LLONG_MAX;
+  if (!rc) {
+    cudaError_t e = cudaMemcpyAsync(&hb, dbad, sizeof(long long), cudaMemcpyDeviceToHost, S(stream));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+    if (e != cudaSuccess) rc = fail(HDG_ECUDA, std::string("fsai rows: ") + cudaGetErrorString(e));
+  }
+  cudaFree(dbad);
+  *bad_row = (hb == LLONG_MAX) ? -1 : hb;
+  return rc;
+}
 
 int hdg_level_set_fsai(hdg_level* L, int64_t n, const int32_t* g_ptr, const int32_t* g_col, const double* g_val,
                        int64_t nnz, const int32_t* gt_ptr, const int32_t* gt_col, const double* gt_val,

@@ -1760,4 +1760,59 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_cycle_kernel(const __gri
   for (long long t = tid; t < n0; t += TAIL_THREADS) A.x_out[t] = x0[t];
 }
 
+// ------------------------------------------------------------------- FSAI setup (rows)
+// fsai_build's per-row solve (multigrid.py:133-152) for every row at once, one thread per row:
+// gather the principal block A[P_i, P_i] of the row's pattern (sorted columns, the diagonal
+// last) from A's CSR by binary search, Cholesky-factor it (the block is SPD for an SPD A; a
+// non-positive pivot flags the row), solve A_P g = e_last and scale g by 1/sqrt(g_last).
+// With A_P = L L^T:  L^-1 e_last = e_last / l_LL, so g = L^-T e_last / l_LL and the scaled row
+// is l_LL * g = L^-T e_last.
+__device__ __forceinline__ double csr_at(const int* __restrict__ ptr, const int* __restrict__ col,
+                                         const double* __restrict__ val, int r, int c) {
+  int lo = __ldg(ptr + r), hi = __ldg(ptr + r + 1) - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int cm = __ldg(col + mid);
+    if (cm == c) return __ldg(val + mid);
+    if (cm < c) lo = mid + 1; else hi = mid - 1;
+  }
+  return 0.0;
+}
+
+template <int MAXL>
+__global__ void fsai_rows_kernel(long long n, const int* __restrict__ a_ptr, const int* __restrict__ a_col,
+                                 const double* __restrict__ a_val, const int* __restrict__ g_ptr,
+                                 const int* __restrict__ g_col, double* __restrict__ g_val,
+                                 long long* __restrict__ bad) {
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= n) return;
+  const int s = __ldg(g_ptr + row), L = __ldg(g_ptr + row + 1) - s;
+  if (L < 1 || L > MAXL) { atomicMin(reinterpret_cast<unsigned long long*>(bad), (unsigned long long)row); return; }
+  double M[MAXL * (MAXL + 1) / 2];   // packed lower triangle, M(a, b) at a (a + 1) / 2 + b
+  int cols[MAXL];
+  for (int a = 0; a < L; ++a) cols[a] = __ldg(g_col + s + a);
+  for (int a = 0; a < L; ++a)
+    for (int b = 0; b <= a; ++b) M[a * (a + 1) / 2 + b] = csr_at(a_ptr, a_col, a_val, cols[a], cols[b]);
+  for (int j = 0; j < L; ++j) {       // Cholesky, column by column
+    double d = M[j * (j + 1) / 2 + j];
+    for (int k = 0; k < j; ++k) d -= M[j * (j + 1) / 2 + k] * M[j * (j + 1) / 2 + k];
+    if (!(d > 0.0)) { atomicMin(reinterpret_cast<unsigned long long*>(bad), (unsigned long long)row); return; }
+    d = sqrt(d);
+    M[j * (j + 1) / 2 + j] = d;
+    for (int i = j + 1; i < L; ++i) {
+      double v = M[i * (i + 1) / 2 + j];
+      for (int k = 0; k < j; ++k) v -= M[i * (i + 1) / 2 + k] * M[j * (j + 1) / 2 + k];
+      M[i * (i + 1) / 2 + j] = v / d;
+    }
+  }
+  // back substitution L^T g = e_last (in place of the solution vector, written straight out)
+  double g[MAXL];
+  for (int a = L - 1; a >= 0; --a) {
+    double v = (a == L - 1) ? 1.0 : 0.0;
+    for (int i = a + 1; i < L; ++i) v -= M[i * (i + 1) / 2 + a] * g[i];
+    g[a] = v / M[a * (a + 1) / 2 + a];
+  }
+  for (int a = 0; a < L; ++a) g_val[s + a] = g[a];
+}
+
 }  // namespace hdg

@@ -87,6 +87,29 @@ def _rows_solve(A, pattern):
     return out
 
 
+def _rows_solve_device(A, pattern):
+    """_rows_solve on the GPU (hdg_fsai_rows: one thread per row, Cholesky of the gathered
+    principal block); A and the pattern go up once as int32 CSR, G's values come back."""
+    import torch
+    n = A.shape[0]
+    counts = np.diff(pattern.indptr)
+    max_len = int(counts.max()) if n else 0
+    if max_len > 96 or A.nnz >= 2 ** 31 or pattern.nnz >= 2 ** 31:
+        return _rows_solve(A, pattern)
+    Acsr = A.tocsr()
+    Acsr.sort_indices()
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).cuda()
+    a_ptr, a_col, a_val = t(Acsr.indptr, np.int32), t(Acsr.indices, np.int32), t(Acsr.data, np.float64)
+    g_ptr, g_col = t(pattern.indptr, np.int32), t(pattern.indices, np.int32)
+    g_val = torch.empty(pattern.nnz, dtype=torch.float64, device="cuda")
+    bad = ctypes.c_int64(-1)
+    check(lib.hdg_fsai_rows(n, a_ptr.data_ptr(), a_col.data_ptr(), a_val.data_ptr(), g_ptr.data_ptr(),
+                            g_col.data_ptr(), g_val.data_ptr(), max_len, ctypes.byref(bad), dev.stream()))
+    if bad.value >= 0:
+        raise NotSPDError(f"non-SPD principal submatrix in FSAI row {bad.value}")
+    return g_val.cpu().numpy()
+
+
 class FSAISmoother:
     """multigrid.py:47-88 with device application.  Host attributes match the reference
     (G, Gt scipy CSR; omega, aggressiveness, complexity, lam_max, cheb_fraction)."""
@@ -156,8 +179,10 @@ def _estimate_lam_max(A, G, iters=20, seed=1234):
     return lam
 
 
-def fsai_build(A, aggressiveness=1, omega=1.0, max_complexity=2.85):
-    """multigrid.py:123-159."""
+def fsai_build(A, aggressiveness=1, omega=1.0, max_complexity=2.85, device=None):
+    """multigrid.py:123-159.  The per-row SPD solves run on the GPU (hdg_fsai_rows) when one is
+    present (device=None) — the host restatement is ~34 us/row (baseline) to ~250 us/row
+    (aggressive), minutes at configs[1] sizes."""
     A = sp.csr_matrix(A)
     A.sort_indices()
     n = A.shape[0]
@@ -166,7 +191,14 @@ def fsai_build(A, aggressiveness=1, omega=1.0, max_complexity=2.85):
     else:
         pattern = _aggressive_pattern(A, aggressiveness, max_complexity)
     pattern.sort_indices()
-    data = _rows_solve(A, pattern) if n else np.zeros(0)
+    if device is None:
+        device = dev.cuda_available()
+    if not n:
+        data = np.zeros(0)
+    elif device:
+        data = _rows_solve_device(A, pattern)
+    else:
+        data = _rows_solve(A, pattern)
     G = sp.csr_matrix((data, pattern.indices.astype(np.int64), pattern.indptr.astype(np.int64)), shape=(n, n))
     complexity = (2 * G.nnz - n) / A.nnz if A.nnz else 1.0
     lam_max = _estimate_lam_max(A, G) if n else 1.0

@@ -478,3 +478,20 @@ def test_fused_coarse_tail_matches_launch_path(P, case):
     assert rel(xf, xl) < 1e-13 and rel(xf2, xl2) < 1e-13
     xo = O.cycle(olevels, 0, b, np.zeros_like(b), 2, 2, visits)
     assert rel(xf, xo) < TOL
+
+
+@pytest.mark.parametrize("power", [1, 2])
+def test_fsai_rows_on_device_match_host(P, power):
+    """fsai_build's per-row SPD solves on the GPU (hdg_fsai_rows, Cholesky) against the host
+    restatement (LU, multigrid.py:133-152) on a K = I p=3 level and a heterogeneous p=2 level."""
+    from paper_1705_09907_b200.fsai import fsai_build
+    for spec, n, p in [(specs.constant(P.pb.ProblemSpec), 16, 3),
+                       (P.pb.ProblemSpec(P.pb.piecewise_coefficient(specs.hetero_K(12, seed=3)), specs.zero,
+                                         specs.zero, 1.0), 12, 2)]:
+        lev = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother=None)[0]
+        A = lev.operator.tocsr()
+        gd = fsai_build(A, power, device=True)
+        gh = fsai_build(A, power, device=False)
+        assert (gd.G.indptr == gh.G.indptr).all() and (gd.G.indices == gh.G.indices).all()
+        assert rel(gd.G.data, gh.G.data) < 1e-12
+        assert abs(gd.lam_max - gh.lam_max) <= 1e-12 * gh.lam_max
