@@ -179,6 +179,33 @@ def _estimate_lam_max(A, G, iters=20, seed=1234):
     return lam
 
 
+def _estimate_lam_max_device(A, G, iters=20, seed=1234):
+    """_estimate_lam_max with the three sparse products per step on the GPU (setup only; the same
+    seed-1234 start vector as multigrid.py:162-173)."""
+    import torch
+
+    import warnings
+
+    def csr(M):
+        M = M.tocsr()
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)   # torch marks sparse CSR as beta
+            return torch.sparse_csr_tensor(torch.from_numpy(M.indptr.astype(np.int64)),
+                                           torch.from_numpy(M.indices.astype(np.int64)),
+                                           torch.from_numpy(np.ascontiguousarray(M.data, dtype=np.float64)),
+                                           size=M.shape).cuda()
+    Ad, Gd, Gtd = csr(A), csr(G), csr(G.T)
+    v = torch.from_numpy(np.random.default_rng(seed).standard_normal(A.shape[0])).cuda()
+    lam = 1.0
+    for _ in range(iters):
+        w = Gtd @ (Gd @ (Ad @ v))
+        lam = float(torch.linalg.vector_norm(w))
+        if lam == 0.0:
+            return 1.0
+        v = w / lam
+    return lam
+
+
 def fsai_build(A, aggressiveness=1, omega=1.0, max_complexity=2.85, device=None):
     """multigrid.py:123-159.  The per-row SPD solves run on the GPU (hdg_fsai_rows) when one is
     present (device=None) — the host restatement is ~34 us/row (baseline) to ~250 us/row
@@ -201,6 +228,11 @@ def fsai_build(A, aggressiveness=1, omega=1.0, max_complexity=2.85, device=None)
         data = _rows_solve(A, pattern)
     G = sp.csr_matrix((data, pattern.indices.astype(np.int64), pattern.indptr.astype(np.int64)), shape=(n, n))
     complexity = (2 * G.nnz - n) / A.nnz if A.nnz else 1.0
-    lam_max = _estimate_lam_max(A, G) if n else 1.0
+    if not n:
+        lam_max = 1.0
+    elif device:
+        lam_max = _estimate_lam_max_device(A, G)
+    else:
+        lam_max = _estimate_lam_max(A, G)
     frac = CHEB_LOWER_FRACTION if aggressiveness == 1 else CHEB_LOWER_FRACTION_AGGRESSIVE
     return FSAISmoother(G, omega, aggressiveness, complexity, lam_max, frac)
