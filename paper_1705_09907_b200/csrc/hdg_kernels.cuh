@@ -119,7 +119,7 @@ template <int N1, bool ST = false> struct Cfg {
   static constexpr int NBUF = HDG_NBUF ? HDG_NBUF : (N1 <= 3 ? 2 : 1);
   static constexpr bool DMMA = HDG_DMMA && N1 <= 8;
   static constexpr int KS = (7 * N1 + 3) / 4;                             // DMMA k-steps (K = 7 n1)
-  static constexpr int WSCR = DMMA ? 32 * 9 : 32 * NOUT + 2;              // per-warp output transpose (+ parity slack)
+  static constexpr int WSCR = DMMA ? 32 * 9 : 32 * NOUT + (HDG_HBULK ? 2 : 0);   // per-warp output transpose (+ bulk-store parity slack)
   // shared mode adds the per-warp transpose scratch; stored mode stages h outputs in BUF
   // Residual / Jacobi / restriction epilogues need b of the tile's own facets.  h-facet rows are
   // contiguous runs (loaded coalesced through the warp scratch); the v-facet columns would be
