@@ -495,3 +495,35 @@ def test_fsai_rows_on_device_match_host(P, power):
         assert (gd.G.indptr == gh.G.indptr).all() and (gd.G.indices == gh.G.indices).all()
         assert rel(gd.G.data, gh.G.data) < 1e-12
         assert abs(gd.lam_max - gh.lam_max) <= 1e-12 * gh.lam_max
+
+
+def test_heterogeneous_full_size_properties(P):
+    """configs[2]'s coefficient law (log-uniform K in [1e-2, 1e2], seed 2) at 1024^2, p=4
+    (1M elements condensed on the GPU, stored facet streams): sampled element blocks against the
+    oracle's full local LU (SURVEY 8c recipe 7), then size-independent properties of the
+    operator: symmetry, linearity, determinism (test_trace.py:51-66)."""
+    import torch
+    n, p = 1024, 4
+    Kg = specs.hetero_K(n, seed=2)
+    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+    s = P.tr.TraceSystem(P.mesh(n, n), p, spec)
+    assert s.piecewise is not None and not s.operator.shared
+    ospec = O.Spec(O.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+    core = O.ElementCore(O.Grid(n, n), p)
+    rng = np.random.default_rng(7)
+    elems = rng.choice(np.arange(n + 1, n * n - n - 1), 48, replace=False)
+    elems = elems[(elems % n != 0) & (elems % n != n - 1)]          # interior: no Dirichlet sides
+    S = s.operator.S_cls
+    got = (S[torch.as_tensor(elems, device=S.device)] if isinstance(S, torch.Tensor) else S[elems])
+    got = got.cpu().numpy() if isinstance(got, torch.Tensor) else np.asarray(got)
+    for k, e in enumerate(elems):
+        assert rel(got[k], O.Local(core, int(e), ospec).schur) < 1e-11
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand(s.ndof, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    y = torch.rand(s.ndof, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    Ax, Ay = s.matvec_free(x), s.matvec_free(y)
+    lhs, rhs_ = float(Ax @ y), float(x @ Ay)
+    assert abs(lhs - rhs_) <= 1e-11 * max(1.0, abs(lhs))
+    A2 = s.matvec_free(2.0 * x - 3.0 * y)
+    assert float((A2 - (2.0 * Ax - 3.0 * Ay)).abs().max()) <= 1e-12 * float(A2.abs().max())
+    assert torch.equal(Ax, s.matvec_free(x))
