@@ -497,18 +497,26 @@ def test_fsai_rows_on_device_match_host(P, power):
         assert abs(gd.lam_max - gh.lam_max) <= 1e-12 * gh.lam_max
 
 
-def test_heterogeneous_full_size_properties(P):
-    """configs[2]'s coefficient law (log-uniform K in [1e-2, 1e2], seed 2) at 1024^2, p=4
+@pytest.mark.parametrize("aniso", [False, True])
+def test_heterogeneous_full_size_properties(P, aniso):
+    """configs[2]'s coefficient law (log-uniform K in [1e-2, 1e2], seed 2) and configs[4]'s
+    anisotropic diagonal law (Kxx, Kyy log-uniform in [1e-1, 1e1], seed 3) at 1024^2, p=4
     (1M elements condensed on the GPU, stored facet streams): sampled element blocks against the
     oracle's full local LU (SURVEY 8c recipe 7), then size-independent properties of the
     operator: symmetry, linearity, determinism (test_trace.py:51-66)."""
     import torch
     n, p = 1024, 4
-    Kg = specs.hetero_K(n, seed=2)
-    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+    if aniso:
+        rng3 = np.random.default_rng(3)
+        Kx, Ky = np.exp(rng3.uniform(np.log(0.1), np.log(10.0), (2, n, n)))
+        spec = P.pb.ProblemSpec(P.pb.piecewise_anisotropic(Kx, Ky), specs.zero, specs.zero, 1.0)
+        ospec = O.Spec(O.piecewise_anisotropic(Kx, Ky), specs.zero, specs.zero, 1.0)
+    else:
+        Kg = specs.hetero_K(n, seed=2)
+        spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+        ospec = O.Spec(O.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
     s = P.tr.TraceSystem(P.mesh(n, n), p, spec)
     assert s.piecewise is not None and not s.operator.shared
-    ospec = O.Spec(O.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
     core = O.ElementCore(O.Grid(n, n), p)
     rng = np.random.default_rng(7)
     elems = rng.choice(np.arange(n + 1, n * n - n - 1), 48, replace=False)
