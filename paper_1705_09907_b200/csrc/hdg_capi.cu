@@ -711,6 +711,7 @@ int hdg_transfer_create_h_window(const hdg_level* fine, const hdg_level* coarse,
   CK(cudaMemcpy(t->dcross, cross, bytes, cudaMemcpyHostToDevice));
   t->ha.cross = t->dcross;
   t->ha.shared_cross = (nsets == 1) ? 1 : 0;
+  if (nsets == 1) std::memcpy(t->ha.cross_c, cross, sizeof(t->ha.cross_c));
   *out = t;
   return 0;
 }

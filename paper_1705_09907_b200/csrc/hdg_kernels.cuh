@@ -1263,10 +1263,13 @@ struct HArgs {
   double halves[8];
   const double* cross;    // device, (nsets, 4, 2, 8)
   int shared_cross;       // 1 => one set for every coarse element (else one per window element)
+  double cross_c[64];     // shared_cross: the one set, read as kernel-parameter constants
 };
 
+template <bool SC>
 __device__ __forceinline__ const double* hcross(const HArgs& h, int I, int Jl, int cf) {
-  const long long set = h.shared_cross ? 0 : ((long long)Jl * h.nxc + I);
+  if constexpr (SC) return h.cross_c + cf * 16;
+  const long long set = (long long)Jl * h.nxc + I;
   return h.cross + (set * 4 + cf) * 16;
 }
 
@@ -1296,7 +1299,7 @@ __device__ __forceinline__ void coarse_side(const HArgs& h, const double* ec, in
 }
 
 // fine window facet t (n1 = 2, one double2 per facet) += its prolongation from the coarse level
-template <bool SM>
+template <bool SM, bool SC>
 __device__ __forceinline__ void h_prolong_add_one(const HArgs& h, const double* __restrict__ ec,
                                                   double* __restrict__ xf, long long t) {
   using IT = typename std::conditional<SM, int, long long>::type;   // 32-bit index math for small levels
@@ -1332,11 +1335,16 @@ __device__ __forceinline__ void h_prolong_add_one(const HArgs& h, const double* 
     const double2 e = vld2<SM>(reinterpret_cast<const double2*>(ec) + cb);
     for (int k = 0; k < 2; ++k) add[k] = h.halves[hf * 4 + k * 2] * e.x + h.halves[hf * 4 + k * 2 + 1] * e.y;
   } else {
-    const double* tm = hcross(h, I, Jl, cf);
+    const double* tm = hcross<SC>(h, I, Jl, cf);
+#pragma unroll
     for (int s = 0; s < 4; ++s) {
       double v[2];
       coarse_side<SM>(h, ec, I, Jl, s, v);
-      for (int k = 0; k < 2; ++k) add[k] += __ldg(tm + k * 8 + s * 2) * v[0] + __ldg(tm + k * 8 + s * 2 + 1) * v[1];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if constexpr (SC) add[k] += tm[k * 8 + s * 2] * v[0] + tm[k * 8 + s * 2 + 1] * v[1];
+        else add[k] += __ldg(tm + k * 8 + s * 2) * v[0] + __ldg(tm + k * 8 + s * 2 + 1) * v[1];
+      }
     }
   }
   double2* xp = reinterpret_cast<double2*>(xf) + t;
@@ -1346,10 +1354,13 @@ __device__ __forceinline__ void h_prolong_add_one(const HArgs& h, const double* 
   *xp = x;
 }
 
-__global__ void h_prolong_add_kernel(const HArgs h, const double* __restrict__ ec, double* __restrict__ xf) {
+__global__ void h_prolong_add_kernel(const __grid_constant__ HArgs h, const double* __restrict__ ec,
+                                     double* __restrict__ xf) {
   const long long nvf = (long long)(2 * h.nxc - 1) * h.nyf;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < h.nhf + nvf) h_prolong_add_one<false>(h, ec, xf, t);
+  if (t >= h.nhf + nvf) return;
+  if (h.shared_cross) h_prolong_add_one<false, true>(h, ec, xf, t);
+  else h_prolong_add_one<false, false>(h, ec, xf, t);
 }
 
 // fine window blocks of h(i, jg) / v(i, jg) (global row jg), -1 when outside the window
@@ -1363,7 +1374,7 @@ __device__ __forceinline__ long long fine_v(const HArgs& h, int i, int jg) {
 }
 
 // contribution of coarse element (I, Jl)'s 4 cross facets to its side-s coarse dofs
-template <bool SM>
+template <bool SM, bool SC>
 __device__ __forceinline__ bool cross_restrict(const HArgs& h, const double* rf, int I, int Jl, int s, double* acc) {
   const int J = Jl + h.jc0;
   const long long cfb[4] = {fine_v(h, 2 * I + 1, 2 * J),       // right of SW = v(2I+1, 2J)
@@ -1371,15 +1382,16 @@ __device__ __forceinline__ bool cross_restrict(const HArgs& h, const double* rf,
                             fine_h(h, 2 * I, 2 * J + 1),       // top of SW   = h(2I, 2J+1)
                             fine_h(h, 2 * I + 1, 2 * J + 1)};  // top of SE   = h(2I+1, 2J+1)
   if (cfb[0] < 0 || cfb[1] < 0 || cfb[2] < 0 || cfb[3] < 0 || Jl < 0 || Jl >= h.nyc) return false;
+#pragma unroll
   for (int cf = 0; cf < 4; ++cf) {
-    const double* tm = hcross(h, I, Jl, cf);
+    const double* tm = hcross<SC>(h, I, Jl, cf);
     const double r0 = vld<SM>(rf + 2 * cfb[cf]), r1 = vld<SM>(rf + 2 * cfb[cf] + 1);
     for (int c = 0; c < 2; ++c) acc[c] += tm[0 * 8 + s * 2 + c] * r0 + tm[1 * 8 + s * 2 + c] * r1;
   }
   return true;
 }
 
-template <bool SM>
+template <bool SM, bool SC>
 __device__ __forceinline__ void h_restrict_one(const HArgs& h, const double* __restrict__ rf,
                                                double* __restrict__ rc, long long t) {
   using IT = typename std::conditional<SM, int, long long>::type;   // 32-bit index math for small levels
@@ -1398,8 +1410,8 @@ __device__ __forceinline__ void h_restrict_one(const HArgs& h, const double* __r
         const double r0 = vld<SM>(rf + 2 * kf[hf]), r1 = vld<SM>(rf + 2 * kf[hf] + 1);
         for (int c = 0; c < 2; ++c) acc[c] += h.halves[hf * 4 + 0 * 2 + c] * r0 + h.halves[hf * 4 + 1 * 2 + c] * r1;
       }
-      ok = cross_restrict<SM>(h, rf, I, Jl - 1, 2, acc)   // element below: this facet is its TOP side
-           && cross_restrict<SM>(h, rf, I, Jl, 0, acc);   // element above: BOTTOM side
+      ok = cross_restrict<SM, SC>(h, rf, I, Jl - 1, 2, acc)   // element below: this facet is its TOP side
+           && cross_restrict<SM, SC>(h, rf, I, Jl, 0, acc);   // element above: BOTTOM side
     }
   } else {          // coarse v(I, Jl)
     const IT u = tt - nhc;
@@ -1413,18 +1425,21 @@ __device__ __forceinline__ void h_restrict_one(const HArgs& h, const double* __r
         const double r0 = vld<SM>(rf + 2 * kf[hf]), r1 = vld<SM>(rf + 2 * kf[hf] + 1);
         for (int c = 0; c < 2; ++c) acc[c] += h.halves[hf * 4 + 0 * 2 + c] * r0 + h.halves[hf * 4 + 1 * 2 + c] * r1;
       }
-      ok = cross_restrict<SM>(h, rf, I - 1, Jl, 1, acc)   // element left: RIGHT side
-           && cross_restrict<SM>(h, rf, I, Jl, 3, acc);   // element right: LEFT side
+      ok = cross_restrict<SM, SC>(h, rf, I - 1, Jl, 1, acc)   // element left: RIGHT side
+           && cross_restrict<SM, SC>(h, rf, I, Jl, 3, acc);   // element right: LEFT side
     }
   }
   rc[2 * t] = ok ? acc[0] : 0.0;
   rc[2 * t + 1] = ok ? acc[1] : 0.0;
 }
 
-__global__ void h_restrict_kernel(const HArgs h, const double* __restrict__ rf, double* __restrict__ rc) {
+__global__ void h_restrict_kernel(const __grid_constant__ HArgs h, const double* __restrict__ rf,
+                                  double* __restrict__ rc) {
   const long long nvc = (long long)(h.nxc - 1) * h.nyc;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < h.nhc + nvc) h_restrict_one<false>(h, rf, rc, t);
+  if (t >= h.nhc + nvc) return;
+  if (h.shared_cross) h_restrict_one<false, true>(h, rf, rc, t);
+  else h_restrict_one<false, false>(h, rf, rc, t);
 }
 
 // ---------------------------------------------------------------------------- small kernels
@@ -1719,13 +1734,19 @@ __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_cycle_kernel(const __gri
       case T_RESTRICT: {
         const HArgs& h = A.h[op.lev];
         const int nc = (int)(h.nhc + (long long)(h.nxc - 1) * h.nyc);
-        for (int t = tid; t < nc; t += TAIL_THREADS) h_restrict_one<true>(h, buf(op.x), buf(op.out), t);
+        if (h.shared_cross)
+          for (int t = tid; t < nc; t += TAIL_THREADS) h_restrict_one<true, true>(h, buf(op.x), buf(op.out), t);
+        else
+          for (int t = tid; t < nc; t += TAIL_THREADS) h_restrict_one<true, false>(h, buf(op.x), buf(op.out), t);
         break;
       }
       case T_PROLONG: {
         const HArgs& h = A.h[op.lev];
         const int nf = (int)(h.nhf + (long long)(2 * h.nxc - 1) * h.nyf);
-        for (int t = tid; t < nf; t += TAIL_THREADS) h_prolong_add_one<true>(h, buf(op.x), buf(op.out), t);
+        if (h.shared_cross)
+          for (int t = tid; t < nf; t += TAIL_THREADS) h_prolong_add_one<true, true>(h, buf(op.x), buf(op.out), t);
+        else
+          for (int t = tid; t < nf; t += TAIL_THREADS) h_prolong_add_one<true, false>(h, buf(op.x), buf(op.out), t);
         break;
       }
       case T_COARSE: {   // warp per row of the dense inverse (multigrid.py:209-212)
