@@ -239,7 +239,7 @@ static int init_level(hdg_level* L, int nx, int ny, int p) {
   if (nx < 1 || ny < 1) return fail(HDG_EINVAL, "mesh element counts must be positive");
   if (p < 1 || p > MAXN1 - 1) return fail(HDG_EINVAL, "order p must be in [1, 12]");
   L->nx = nx; L->ny = ny; L->p = p; L->n1 = p + 1;
-  L->nxp = ((nx + 31) / 32) * 32;
+  L->nxp = ((nx + 1 + 31) / 32) * 32;   // >= nx + 1: the half-stored stream reads slot (j, i + 1)
   L->nh = (long long)nx * (ny - 1);
   L->n_blocks = L->nh + (long long)(nx - 1) * ny;
   L->ndof = L->n_blocks * L->n1;
@@ -373,7 +373,7 @@ static int create_stored(int nx, int ny, int p, const double* blocks, bool bcast
   if (rc) { delete L; return rc; }
   const int n1 = L->n1;
   const long long nslots = (long long)ny * L->nxp;
-  const size_t wbytes = sizeof(double) * (size_t)nslots * 7 * n1 * n1;
+  const size_t wbytes = sizeof(double) * (size_t)nslots * (HDG_SYMSTORE ? 4 : 7) * n1 * n1;
   L->op_bytes = 0;
   if (L->ndof > 0) {
     if (!blocks) { hdg_level_destroy(L); return fail(HDG_EINVAL, "null blocks"); }
@@ -381,7 +381,29 @@ static int create_stored(int nx, int ny, int p, const double* blocks, bool bcast
       hdg_level_destroy(L);
       return fail(HDG_ENOMEM, "cannot allocate stored operator streams");
     }
-    const long long nthr = nslots * 7 * n1 * n1;
+    if (HDG_SYMSTORE && !bcast) {
+      // each coupling block is stored once and read transposed by its partner: the element
+      // blocks must be symmetric (the condensed operator is, local.py:223-237)
+      unsigned long long* dchk = nullptr;
+      CK(cudaMalloc(&dchk, 2 * sizeof(unsigned long long)));
+      CK(cudaMemset(dchk, 0, 2 * sizeof(unsigned long long)));
+      const long long E = (long long)nx * ny, tot = E * 16 * n1 * n1;
+#define ASYM_CASE(N) { block_asym_kernel<N><<<(unsigned)((tot + 255) / 256), 256>>>(blocks, E, dchk); CKL(); break; }
+      HDG_N1_SWITCH(n1, ASYM_CASE)
+#undef ASYM_CASE
+      unsigned long long hchk[2];
+      CK(cudaMemcpy(hchk, dchk, sizeof(hchk), cudaMemcpyDeviceToHost));
+      cudaFree(dchk);
+      double asym, mag;
+      std::memcpy(&asym, &hchk[0], sizeof(double));
+      std::memcpy(&mag, &hchk[1], sizeof(double));
+      if (!(asym <= 1e-10 * mag)) {
+        hdg_level_destroy(L);
+        return fail(HDG_EINVAL, "stored element blocks are not symmetric (max |S - S^T| = " + std::to_string(asym) +
+                                    ", max |S| = " + std::to_string(mag) + ")");
+      }
+    }
+    const long long nthr = nslots * (HDG_SYMSTORE ? 4 : 7) * n1 * n1;
     const int bs = 256;
     const long long nbk = (nthr + bs - 1) / bs;
 #define RELAYOUT_CASE(N)                                                                         \
@@ -396,7 +418,7 @@ static int create_stored(int nx, int ny, int p, const double* blocks, bool bcast
 #undef RELAYOUT_CASE
     CK(cudaDeviceSynchronize());
     // algorithmic operator bytes: the facets' merged matrices (boundary padding excluded)
-    L->op_bytes = (long long)L->n_blocks * 7 * n1 * n1 * 8;
+    L->op_bytes = (long long)L->n_blocks * (HDG_SYMSTORE ? 4 : 7) * n1 * n1 * 8;
   }
   if ((rc = prepare(n1, true))) { hdg_level_destroy(L); return rc; }
   *out = L;
@@ -438,7 +460,7 @@ int hdg_level_set_blockjacobi(hdg_level* L, double omega) {
     for (int vert = 0; vert < 2; ++vert) {                                                \
       const double* W = vert ? L->dWv : L->dWh;                                           \
       double* D = vert ? L->dDv : L->dDh;                                                 \
-      CK(cudaMemcpy2D(D, sizeof(double) * 32 * DSZ, W + (size_t)DSZ * 32,                 \
+      CK(cudaMemcpy2D(D, sizeof(double) * 32 * DSZ, W + (size_t)(HDG_SYMSTORE ? 0 : DSZ) * 32, \
                       sizeof(double) * 32 * WSZ, sizeof(double) * 32 * DSZ, nslots / 32,  \
                       cudaMemcpyDeviceToDevice));                                         \
       invert_kernel<N><<<(unsigned)((nslots + bs - 1) / bs), bs>>>(D, nslots);            \

@@ -72,6 +72,12 @@ namespace cg = cooperative_groups;
 #ifndef HDG_WS_KERNEL
 #define HDG_WS_KERNEL 0    // set by hdg_capi.cu when the warp-specialised kernel is selected (HDG_WS)
 #endif
+#ifndef HDG_SYMSTORE
+#define HDG_SYMSTORE 1     // stored mode: each facet-pair coupling block stored once (4 of 7 blocks per facet)
+#endif
+#ifndef HDG_SYMSTORE_EF_MIN_N1
+#define HDG_SYMSTORE_EF_MIN_N1 7   // half-stored stream: evict-first hint on the owner's read from this n1
+#endif                             // (measured: p=8 192 vs 207 us, p=4 118 vs 105 us, p=1 69 vs 62 us)
 #ifndef HDG_SHARED_SYM
 #define HDG_SHARED_SYM 1   // shared mode: mirror-reduced stencil (apply_shared_sym); 0 = full n1 x 7n1
 #endif
@@ -95,7 +101,10 @@ template <int N1, bool ST = false> struct Cfg {
   static constexpr int F = (N1 <= (ST ? 5 : HDG_F_MAXN1_SHARED)) && (N1 <= HDG_F_MAXN1)
                                ? ((!ST && N1 <= HDG_F3_MAXN1) ? HDG_F_SHARED : 2) : 1;
   static constexpr int TY = NWARP * F;              // tile height in elements
-  static constexpr int WSZ = 7 * N1 * N1;           // merged facet operator entries
+  // stored stream entries per facet: the merged n1 x 7n1 row (7 blocks), or with HDG_SYMSTORE
+  // only the blocks this facet owns (diagonal + 3 couplings); the other 3 are read transposed from
+  // the neighbour that owns the pair (the operator is symmetric)
+  static constexpr int WSZ = (HDG_SYMSTORE ? 4 : 7) * N1 * N1;
   static constexpr int DSZ = N1 * N1;               // block-Jacobi inverse entries
   static constexpr int QUNROLL = (N1 <= 8) ? 7 : 1; // keep registers bounded at high order
   static constexpr int HROWS = TY + 2, HCOLS = TX + 1;
@@ -625,6 +634,56 @@ __device__ __forceinline__ void apply_stored(const double* const (&nb)[7], const
   }
 }
 
+// Stored mode with each coupling block stored once (HDG_SYMSTORE).  Owned blocks per facet, in
+// stream order:  h(i,j): q1 (diagonal), q2 = h(i,j+1), q5 = v(i,j), q6 = v(i+1,j)
+//                v(i,j): q1, q2 = v(i+1,j), q4 = h(i-1,j+1), q6 = h(i,j+1)
+// and the other three come transposed from their owners:
+//   h(i,j): q0 <- h(i,j-1).q2,  q3 <- v(i,j-1).q6,  q4 <- v(i+1,j-1).q4
+//   v(i,j): q0 <- v(i-1,j).q2,  q3 <- h(i-1,j).q6,  q5 <- h(i,j).q5
+// (same lane or the neighbouring lane of the interleaved stream, so the reads stay coalesced;
+// the owner's copy is read in the same tile, so the second read is an L2 hit).
+template <int N1> __device__ __forceinline__ const double* wslot(const double* W, long long slot) {
+  return W + (size_t)(slot >> 5) * Cfg<N1>::WSZ * 32 + (slot & 31);
+}
+
+template <int N1, bool VERT>
+__device__ __forceinline__ void apply_stored_half(const double* const (&nb)[7], const double* own, const double* t0,
+                                                  const double* t1, const double* t2, double (&acc)[N1]) {
+  const uint64_t pol = evict_first_policy();
+  constexpr int B = N1 * N1 * 32;   // one block of the interleaved stream
+  constexpr int QO[4] = {1, 2, VERT ? 4 : 5, 6};
+  constexpr int QT[3] = {0, 3, VERT ? 5 : 4};
+#pragma unroll
+  for (int k = 0; k < N1; ++k) acc[k] = 0.0;
+#pragma unroll
+  for (int qs = 0; qs < 4; ++qs) {
+    double xv[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) xv[m] = nb[QO[qs]][m];
+    const double* Wq = own + qs * B;
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        // the partner reads this block again (transposed) within the same tile: keep it in L2
+        const double w = (N1 >= HDG_SYMSTORE_EF_MIN_N1) ? ld_stream(Wq + (k * N1 + m) * 32, pol)
+                                                          : __ldg(Wq + (k * N1 + m) * 32);
+        acc[k] = fma(w, xv[m], acc[k]);
+      }
+  }
+  const double* tp[3] = {t0, t1, t2};
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    double xv[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) xv[m] = nb[QT[t]][m];
+#pragma unroll
+    for (int mm = 0; mm < N1; ++mm)       // owner's row mm = our input mm; its column k = our output k
+#pragma unroll
+      for (int k = 0; k < N1; ++k) acc[k] = fma(__ldg(tp[t] + (mm * N1 + k) * 32), xv[mm], acc[k]);
+  }
+}
+
 template <int EPI, int N1> struct NOutOf { static constexpr int v = (EPI == EPI_RESPR) ? N1 - 1 : N1; };
 
 // Per-facet epilogue: the facet's output values (y | r | x_out | r_coarse) into `o`.
@@ -818,6 +877,7 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
   }
   double ov[F][N1];
   double ohs[STORED ? F : 1][N1];   // stored mode: h outputs wait for the CTA-staged write
+  {
   // ---- horizontal facets: owners (i, j-1) [TOP rows] and (i, j) [BOTTOM rows]
   {
     const double* nb[F][7];
@@ -870,7 +930,14 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
         if (j >= 1 && j <= a.ny - 1) {  // warp-uniform; lanes i >= nx read zero padding slots
           const long long grp = ((long long)j * a.nxp + i0) >> 5;
           double acc[N1];
-          apply_stored<N1>(nb[f], a.Wh + (size_t)grp * C::WSZ * 32 + tx, acc);
+          if constexpr (HDG_SYMSTORE) {
+            constexpr int B = N1 * N1 * 32;
+            const long long sl = (long long)j * a.nxp + i, sd = sl - a.nxp;   // row j-1
+            apply_stored_half<N1, false>(nb[f], wslot<N1>(a.Wh, sl), wslot<N1>(a.Wh, sd) + 1 * B,
+                                         wslot<N1>(a.Wv, sd) + 3 * B, wslot<N1>(a.Wv, sd + 1) + 2 * B, acc);
+          } else {
+            apply_stored<N1>(nb[f], a.Wh + (size_t)grp * C::WSZ * 32 + tx, acc);
+          }
           if (i < a.nx)
             facet_epilogue<N1, true, EPI>(a, hblk(a.nx, i, j), nb[f][1], nullptr,
                                           a.Dh + (size_t)grp * C::DSZ * 32 + tx, acc, ohs[f], nrm);
@@ -913,7 +980,14 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
         if (j < a.ny) {
           const long long grp = ((long long)j * a.nxp + i0) >> 5;
           double acc[N1];
-          apply_stored<N1>(nb[f], a.Wv + (size_t)grp * C::WSZ * 32 + tx, acc);
+          if constexpr (HDG_SYMSTORE) {
+            constexpr int B = N1 * N1 * 32;
+            const long long sl = (long long)j * a.nxp + i, sw = sl > 0 ? sl - 1 : 0;   // column i-1
+            apply_stored_half<N1, true>(nb[f], wslot<N1>(a.Wv, sl), wslot<N1>(a.Wv, sw) + 1 * B,
+                                        wslot<N1>(a.Wh, sw) + 3 * B, wslot<N1>(a.Wh, sl) + 2 * B, acc);
+          } else {
+            apply_stored<N1>(nb[f], a.Wv + (size_t)grp * C::WSZ * 32 + tx, acc);
+          }
           if (i >= 1 && i <= a.nx - 1)
             facet_epilogue<N1, true, EPI>(a, vblk(a.nh, a.ny, i, j), nb[f][1], nullptr,
                                           a.Dv + (size_t)grp * C::DSZ * 32 + tx, acc, ov[f], nrm,
@@ -922,6 +996,7 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
         }
       }
     }
+  }
   }
   // ---- outputs -> shared (x buffer is consumed) -> contiguous global runs
   consumer_sync();
@@ -1167,7 +1242,9 @@ __global__ void relayout_kernel(const double* __restrict__ S, int nx, int ny, in
     if (bcast) e1 = e2 = 0;   // one block for every element (asymmetric constant operator)
   }
   const int L = 4 * N1;
-  const int q = idx / (N1 * N1), k = (idx / N1) % N1, m = idx % N1;
+  int q = idx / (N1 * N1);
+  const int k = (idx / N1) % N1, m = idx % N1;
+  if (HDG_SYMSTORE) q = (q == 0) ? 1 : (q == 1) ? 2 : (q == 2) ? (vert ? 4 : 5) : 6;   // owned blocks
   double v = 0.0;
   if (valid) {
     int w1, r1, c1, w2, r2, c2;
@@ -1176,6 +1253,31 @@ __global__ void relayout_kernel(const double* __restrict__ S, int nx, int ny, in
     if (w2 >= 0) v += S[((w2 ? e2 : e1) * L + r2) * L + c2];
   }
   W[(grp * C::WSZ + idx) * 32 + lane] = v;
+}
+
+// max |S - S^T| and max |S| over all element blocks (atomicMax on the bit patterns of
+// non-negative doubles): the half-stored stream requires a symmetric operator
+template <int N1>
+__global__ void block_asym_kernel(const double* __restrict__ S, long long E, unsigned long long* out) {
+  constexpr int L = 4 * N1;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double asym = 0.0, mag = 0.0;
+  if (tid < E * L * L) {
+    const long long e = tid / (L * L);
+    const int r = (int)((tid / L) % L), c = (int)(tid % L);
+    const double a = S[(e * L + r) * L + c], b = S[(e * L + c) * L + r];
+    asym = fabs(a - b);
+    mag = fabs(a);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    asym = fmax(asym, __shfl_xor_sync(0xffffffffu, asym, o));
+    mag = fmax(mag, __shfl_xor_sync(0xffffffffu, mag, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, (unsigned long long)__double_as_longlong(asym));
+    atomicMax(out + 1, (unsigned long long)__double_as_longlong(mag));
+  }
 }
 
 // In-place inverse of SPD n1 x n1 blocks held in the interleaved layout (Gauss-Jordan, no
@@ -1614,17 +1716,54 @@ __device__ __forceinline__ void tail_facet_apply(const TailLevel& L, const doubl
     q[3] = hb(i - 1, j); q[4] = hb(i - 1, j + 1); q[5] = hb(i, j); q[6] = hb(i, j + 1);
   }
   const int slot = j * L.nxp + i;
-  const double* W = L.W[vert ? 1 : 0];
-  const int ws = L.stored ? 32 : 1;
-  if (L.stored) W += (size_t)(slot >> 5) * 7 * N1 * N1 * 32 + (slot & 31);
   y[0] = 0.0; y[1] = 0.0;
+  if (L.stored && HDG_SYMSTORE) {
+    // half-stored stream: own blocks + 3 transposed from their owners (apply_stored_half)
+    constexpr int B = N1 * N1 * 32;
+    const int QO[4] = {1, 2, vert ? 4 : 5, 6};
+    const double* own = wslot<N1>(L.W[vert ? 1 : 0], slot);
+    const double* tp[3];
+    const int QT[3] = {0, 3, vert ? 5 : 4};
+    if (!vert) {
+      const int sd = slot - L.nxp;
+      tp[0] = wslot<N1>(L.W[0], sd) + B; tp[1] = wslot<N1>(L.W[1], sd) + 3 * B; tp[2] = wslot<N1>(L.W[1], sd + 1) + 2 * B;
+    } else {
+      const int sw = slot - 1;
+      tp[0] = wslot<N1>(L.W[1], sw) + B; tp[1] = wslot<N1>(L.W[0], sw) + 3 * B; tp[2] = wslot<N1>(L.W[0], slot) + 2 * B;
+    }
 #pragma unroll
-  for (int s = 0; s < 7; ++s) {
-    const double2 v = q[s] >= 0 ? reinterpret_cast<const double2*>(x)[q[s]] : make_double2(0.0, 0.0);
+    for (int t = 0; t < 4; ++t) {
+      const int s = QO[t];
+      const double2 v = q[s] >= 0 ? reinterpret_cast<const double2*>(x)[q[s]] : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      y[k] = fma(W[((s * N1 + k) * N1 + 0) * ws], v.x, y[k]);
-      y[k] = fma(W[((s * N1 + k) * N1 + 1) * ws], v.y, y[k]);
+      for (int k = 0; k < N1; ++k) {
+        y[k] = fma(own[t * B + (k * N1 + 0) * 32], v.x, y[k]);
+        y[k] = fma(own[t * B + (k * N1 + 1) * 32], v.y, y[k]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const int s = QT[t];
+      if (q[s] < 0) continue;
+      const double2 v = reinterpret_cast<const double2*>(x)[q[s]];
+#pragma unroll
+      for (int k = 0; k < N1; ++k) {
+        y[k] = fma(tp[t][(0 * N1 + k) * 32], v.x, y[k]);
+        y[k] = fma(tp[t][(1 * N1 + k) * 32], v.y, y[k]);
+      }
+    }
+  } else {
+    const double* W = L.W[vert ? 1 : 0];
+    const int ws = L.stored ? 32 : 1;
+    if (L.stored) W += (size_t)(slot >> 5) * 7 * N1 * N1 * 32 + (slot & 31);
+#pragma unroll
+    for (int s = 0; s < 7; ++s) {
+      const double2 v = q[s] >= 0 ? reinterpret_cast<const double2*>(x)[q[s]] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < N1; ++k) {
+        y[k] = fma(W[((s * N1 + k) * N1 + 0) * ws], v.x, y[k]);
+        y[k] = fma(W[((s * N1 + k) * N1 + 1) * ws], v.y, y[k]);
+      }
     }
   }
   slot_out = slot;
