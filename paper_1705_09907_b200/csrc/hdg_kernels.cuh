@@ -48,6 +48,10 @@ namespace cg = cooperative_groups;
 #ifndef HDG_F3_MAXN1
 #define HDG_F3_MAXN1 5     // shared mode: HDG_F_SHARED facets per thread up to this n1 (measured: p<=4)
 #endif
+#ifndef HDG_F_MAXN1_STORED
+#define HDG_F_MAXN1_STORED 2   // stored mode: two facet rows per thread up to this n1 (smaller tiles keep the
+                               // half-stored partner reads in L2: p=4 105 -> 90 us; p=1 prefers 2 rows)
+#endif
 #ifndef HDG_F_MAXN1_SHARED
 #define HDG_F_MAXN1_SHARED 9
 #endif
@@ -98,7 +102,7 @@ template <int N1, bool ST = false> struct Cfg {
   static constexpr int S = N1;                      // facet blocks contiguous in a staged run
   // facets per thread per orientation (measured: 2 pays up to p=8 when W is in the constant
   // bank, up to p=4 when W streams from HBM)
-  static constexpr int F = (N1 <= (ST ? 5 : HDG_F_MAXN1_SHARED)) && (N1 <= HDG_F_MAXN1)
+  static constexpr int F = (N1 <= (ST ? HDG_F_MAXN1_STORED : HDG_F_MAXN1_SHARED)) && (N1 <= HDG_F_MAXN1)
                                ? ((!ST && N1 <= HDG_F3_MAXN1) ? HDG_F_SHARED : 2) : 1;
   static constexpr int TY = NWARP * F;              // tile height in elements
   // stored stream entries per facet: the merged n1 x 7n1 row (7 blocks), or with HDG_SYMSTORE
