@@ -67,12 +67,6 @@ namespace cg = cooperative_groups;
 #ifndef HDG_NWARP
 #define HDG_NWARP 8
 #endif
-#ifndef HDG_HBULK
-#define HDG_HBULK 0        // shared mode h-facet outputs by bulk (TMA) stores from the warp scratch
-#endif
-#ifndef HDG_HDIRECT
-#define HDG_HDIRECT 0      // shared mode h-facet outputs: 1 = direct stores, 0 = warp transpose
-#endif
 #ifndef HDG_WS_KERNEL
 #define HDG_WS_KERNEL 0    // set by hdg_capi.cu when the warp-specialised kernel is selected (HDG_WS)
 #endif
@@ -132,7 +126,7 @@ template <int N1, bool ST = false> struct Cfg {
   static constexpr int NBUF = HDG_NBUF ? HDG_NBUF : (N1 <= 3 ? 2 : 1);
   static constexpr bool DMMA = HDG_DMMA && N1 <= 8;
   static constexpr int KS = (7 * N1 + 3) / 4;                             // DMMA k-steps (K = 7 n1)
-  static constexpr int WSCR = DMMA ? 32 * 9 : 32 * NOUT + (HDG_HBULK ? 2 : 0);   // per-warp output transpose (+ bulk-store parity slack)
+  static constexpr int WSCR = DMMA ? 32 * 9 : 32 * NOUT;                  // per-warp output transpose
   // shared mode adds the per-warp transpose scratch; stored mode stages h outputs in BUF
   // Residual / Jacobi / restriction epilogues need b of the tile's own facets.  h-facet rows are
   // contiguous runs (loaded coalesced through the warp scratch); the v-facet columns would be
@@ -745,55 +739,12 @@ __device__ __forceinline__ void facet_epilogue(const MvArgs& a, int blk, const d
 // shared memory (the consumed x buffer) and written back as contiguous runs.
 // h-facet outputs of one warp row (32 consecutive facets = one contiguous run in HBM):
 // transposed through the warp's private scratch and stored coalesced, right after compute
-// the warp scratch may still be the source of an in-flight bulk store: wait until it was read
-__device__ __forceinline__ void scr_acquire(int lane) {
-#if HDG_HBULK
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-  __syncwarp();
-#endif
-}
-
 template <int N1, int NO>
 __device__ __forceinline__ void store_h_row(const MvArgs& a, double* scr, int i0, int j, const double (&o)[N1],
                                             int lane) {
   if (a.out == nullptr || j < 1 || j > a.ny - 1) return;  // warp-uniform
 #ifdef HDG_EXP_NOHSTORE
   if (a.nx > 0) return;
-#endif
-#if HDG_HDIRECT
-  // direct stride-n1 stores from registers (no shared-memory transpose)
-  if (i0 + lane < a.nx) {
-    double* d = a.out + (hblk(a.nx, i0, j) + lane) * NO;
-#pragma unroll
-    for (int k = 0; k < NO; ++k) d[k] = o[k];
-  }
-  return;
-#endif
-#if HDG_HBULK
-  {
-    // bulk (TMA) store of the row's aligned body; the smem copy keeps the global 16-byte parity
-    const long long g0 = (long long)hblk(a.nx, i0, j) * NO;
-    const int shift = (int)(g0 & 1);
-    const int count = min(TX, a.nx - i0) * NO;
-    scr_acquire(lane);
-#pragma unroll
-    for (int k = 0; k < NO; ++k) scr[shift + lane * NO + k] = o[k];
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) {
-      long long gs = g0 + shift, ge = (g0 + count) & ~1LL;
-      double* dst = a.out;
-      if (shift) dst[g0] = scr[shift];
-      if (((g0 + count) & 1) && g0 + count - 1 >= gs) dst[g0 + count - 1] = scr[shift + count - 1];
-      if (ge > gs) {
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
-                     ::"l"(dst + gs), "r"(smem_u32(scr + shift + (gs - g0))), "r"((unsigned)((ge - gs) * 8))
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-      }
-    }
-    return;
-  }
 #endif
 #pragma unroll
   for (int k = 0; k < NO; ++k) scr[lane * NO + k] = o[k];
@@ -914,7 +865,6 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
           if (rowok) {
             const int count = min(TX, a.nx - i0) * N1;
             const double* src = a.b + hblk(a.nx, i0, j) * N1;
-            scr_acquire(tx);
 #pragma unroll
             for (int q = 0; q < N1; ++q)
               if (tx + 32 * q < count) scr[tx + 32 * q] = __ldg(src + tx + 32 * q);
@@ -1095,9 +1045,6 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
     __syncthreads();
     if (++slot == NB) { slot = 0; phase ^= 1u; }
   }
-#if HDG_HBULK
-  if ((threadIdx.x & 31) == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-#endif
   if constexpr (EPI == EPI_RES) {
     if (a.partials != nullptr) {
       __shared__ double red[NWARP];
