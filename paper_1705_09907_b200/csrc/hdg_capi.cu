@@ -2,10 +2,6 @@
 // the device-resident multigrid cycle and its CUDA-graph cache.
 // Reference interfaces replaced: see include/hdgb200.h (each entry cites trace.py / multigrid.py).
 #include "hdgb200.h"
-#ifndef HDG_WS
-#define HDG_WS 0
-#endif
-#define HDG_WS_KERNEL HDG_WS
 #include "hdg_kernels.cuh"
 
 #include <algorithm>
@@ -116,13 +112,10 @@ static void host_invert(std::vector<double>& a, int n) {  // SPD Gauss-Jordan, n
 }
 
 
-// warp-specialized (producer warp + compute warps) or uniform kernel
 template <int N1, bool STORED, int EPI>
 static auto kernel_ptr() {
-  if constexpr (HDG_WS) return trace_apply_ws_kernel<N1, STORED, EPI>;
-  else return trace_apply_kernel<N1, STORED, EPI>;
+  return trace_apply_kernel<N1, STORED, EPI>;
 }
-static constexpr int kThreads = HDG_WS ? NT + 32 : NT;
 
 template <int N1, bool STORED, int EPI>
 static int set_attr() {
@@ -158,7 +151,7 @@ static int grid_for(const hdg_level* L) {
   static int occ = -1;
   if (occ < 0) {
     const size_t smem = C::template smem_doubles_epi<EPI>() * sizeof(double);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel_ptr<N1, STORED, EPI>(), kThreads, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel_ptr<N1, STORED, EPI>(), C::NTH, smem) !=
             cudaSuccess || occ < 1)
       occ = 1;
     if (occ > MAX_CTAS_PER_SM) occ = MAX_CTAS_PER_SM;
@@ -194,7 +187,7 @@ static int apply_t(const hdg_level* L, MvArgs& a, cudaStream_t s) {
   } else {
     std::memset(&op, 0, sizeof(op));
   }
-  kernel_ptr<N1, STORED, EPI>()<<<grid, kThreads, smem, s>>>(a, op);
+  kernel_ptr<N1, STORED, EPI>()<<<grid, C::NTH, smem, s>>>(a, op);
   CKL();
   return 0;
 }

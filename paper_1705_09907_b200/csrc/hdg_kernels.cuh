@@ -58,17 +58,11 @@ namespace cg = cooperative_groups;
 #ifndef HDG_MINB
 #define HDG_MINB 2         // __launch_bounds__ min blocks per SM for the trace kernel
 #endif
-#ifndef HDG_WS_MINB
-#define HDG_WS_MINB 2      // warp-specialized kernel: CTAs per SM the registers must allow
-#endif
 #ifndef HDG_DMMA
 #define HDG_DMMA 0         // shared mode: FP64 tensor-core (DMMA m8n8k4) stencil GEMM for n1 <= 8
 #endif
 #ifndef HDG_NWARP
-#define HDG_NWARP 8
-#endif
-#ifndef HDG_WS_KERNEL
-#define HDG_WS_KERNEL 0    // set by hdg_capi.cu when the warp-specialised kernel is selected (HDG_WS)
+#define HDG_NWARP 0        // warps per CTA; 0 = per-configuration default (Cfg::NW, measured)
 #endif
 #ifndef HDG_SYMSTORE
 #define HDG_SYMSTORE 1     // stored mode: each facet-pair coupling block stored once (4 of 7 blocks per facet)
@@ -85,20 +79,25 @@ namespace cg = cooperative_groups;
 #endif
 
 constexpr int TX = 32;     // tile width in elements (= warp width: lanes walk i)
-constexpr int NWARP = HDG_NWARP;   // warps per CTA
-constexpr int NT = TX * NWARP;
 constexpr int MAXN1 = 13;  // p <= 12
 constexpr int MAX_CTAS_PER_SM = 8;
 
 enum Epi { EPI_Y = 0, EPI_RES = 1, EPI_BJ = 2, EPI_RESPR = 3 };
 
 template <int N1, bool ST = false> struct Cfg {
+  // warps per CTA (measured on B200, tools/tune_matvec.py): 8 for the low-order shared and the
+  // p <= 2 stored kernels; 4-warp CTAs (3 per SM) for high orders and stored p >= 3, where
+  // shorter tiles shorten the stencil/partner reuse distances (shared p=8 59.7 -> 48.2 us,
+  // p=12 53.3 -> 49.2 us, stored p=8 192 -> 182 us; shared p=4 44.5 vs 45.1 us with 4)
+  static constexpr int NW = HDG_NWARP ? HDG_NWARP : ((N1 <= 3 || (!ST && N1 <= 5)) ? 8 : 4);
+  static constexpr int NTH = 32 * NW;
+  static constexpr int MINB = (NW >= 8) ? (ST ? 2 : (N1 <= 9 ? HDG_MINB : 1)) : 3;
   static constexpr int S = N1;                      // facet blocks contiguous in a staged run
   // facets per thread per orientation (measured: 2 pays up to p=8 when W is in the constant
   // bank, up to p=4 when W streams from HBM)
   static constexpr int F = (N1 <= (ST ? HDG_F_MAXN1_STORED : HDG_F_MAXN1_SHARED)) && (N1 <= HDG_F_MAXN1)
                                ? ((!ST && N1 <= HDG_F3_MAXN1) ? HDG_F_SHARED : 2) : 1;
-  static constexpr int TY = NWARP * F;              // tile height in elements
+  static constexpr int TY = NW * F;                 // tile height in elements
   // stored stream entries per facet: the merged n1 x 7n1 row (7 blocks), or with HDG_SYMSTORE
   // only the blocks this facet owns (diagonal + 3 couplings); the other 3 are read transposed from
   // the neighbour that owns the pair (the operator is symmetric)
@@ -134,13 +133,13 @@ template <int N1, bool ST = false> struct Cfg {
   // ([row][column], odd block stride), when two CTAs per SM still fit.
   static constexpr int SB = (N1 & 1) ? N1 : N1 + 1;
   static constexpr int BSZ = ((TY * TX * SB) + 1) & ~1;
-  __host__ __device__ static constexpr int base_doubles(bool stored) { return NBUF * BUF + (stored ? 0 : (NWARP + 1) * WSCR); }
+  __host__ __device__ static constexpr int base_doubles(bool stored) { return NBUF * BUF + (stored ? 0 : (NW + 1) * WSCR); }
   template <int EPI> __host__ __device__ static constexpr bool stage_b() {
-    return EPI != 0 && !HDG_WS_KERNEL && (base_doubles(ST) + NBUF * BSZ) * 8 <= 113 * 1024;
+    return EPI != 0 && (base_doubles(ST) + NBUF * BSZ) * 8 <= 113 * 1024;
   }
   template <int EPI> __host__ __device__ static constexpr int bufs() { return BUF + (stage_b<EPI>() ? BSZ : 0); }   // stage stride
   template <int EPI> __host__ __device__ static constexpr int smem_doubles_epi() {
-    return NBUF * bufs<EPI>() + (ST ? 0 : (NWARP + 1) * WSCR);
+    return NBUF * bufs<EPI>() + (ST ? 0 : (NW + 1) * WSCR);
   }
   static constexpr int smem_doubles(bool stored) { return base_doubles(stored); }
 };
@@ -343,7 +342,7 @@ __device__ __forceinline__ void stage_b_columns(const MvArgs& a, double* Bs, int
   constexpr int LEN = C::TY * N1;
   constexpr int NQ = (LEN + 31) / 32;
   const int ehi = min(C::TY, a.ny - j0) * N1;
-  for (int c = warp; c < TX; c += NWARP) {
+  for (int c = warp; c < TX; c += C::NW) {
     const int i = i0 + c;
     if (i < 1 || i > a.nx - 1) continue;   // warp-uniform; never read for these columns
     const double* src = a.b + (long long)vblk(a.nh, a.ny, i, j0) * N1;
@@ -388,29 +387,30 @@ __device__ __forceinline__ void stage_tile(const MvArgs& a, double* buf, int i0,
 #endif
     unsigned bytes = 0;
 #ifndef HDG_EXP_NOH
-    for (int r = warp; r < C::HROWS; r += NWARP) bytes += run_bytes(h_run<N1, ST>(a, i0, j0, r));
+    for (int r = warp; r < C::HROWS; r += C::NW) bytes += run_bytes(h_run<N1, ST>(a, i0, j0, r));
 #endif
     fence_proxy_async();               // prior generic reads/writes of this buffer -> async proxy
     mbar_arrive_expect_tx(bar, bytes);
 #ifndef HDG_EXP_NOH
-    for (int r = warp; r < C::HROWS; r += NWARP) run_issue(a.x, buf, h_run<N1, ST>(a, i0, j0, r), bar);
+    for (int r = warp; r < C::HROWS; r += C::NW) run_issue(a.x, buf, h_run<N1, ST>(a, i0, j0, r), bar);
 #endif
   }
   if (edge) {  // zero Dirichlet / out-of-mesh parts of H rows (interior tiles skip this)
-    for (int r = warp; r < C::HROWS; r += NWARP) run_zero(buf, h_run<N1, ST>(a, i0, j0, r), lane);
+    for (int r = warp; r < C::HROWS; r += C::NW) run_zero(buf, h_run<N1, ST>(a, i0, j0, r), lane);
   }
   // V columns: coalesced 8-byte LDGSTS from the contiguous run, transposed into [row][col];
   // src-size 0 zero-fills Dirichlet / out-of-mesh blocks
 #ifndef HDG_EXP_NOV
-  stage_v_columns<N1, ST>(a, buf + C::HSZ, i0, j0, warp, NWARP, lane);
+  stage_v_columns<N1, ST>(a, buf + C::HSZ, i0, j0, warp, C::NW, lane);
 #endif
   if constexpr (SBV) stage_b_columns<N1, ST>(a, buf + C::BUF, i0, j0, warp, lane);
   cp_async_mbar_arrive(bar);           // every thread: one arrival when its LDGSTS land
 }
 
-// barrier among the NT compute threads only (named barrier 1; the warp-specialized kernel has
-// an extra producer warp that must not take part)
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory"); }
+// CTA-wide barrier of the NTH compute threads (named barrier 1)
+template <int NTH> __device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(NTH) : "memory");
+}
 
 // acc_f = W . [x of facet f's 7 stencil blocks] for FF facets of one orientation.
 // Shared mode: W is uniform (constant bank), each W value feeds FF facets.
@@ -788,15 +788,15 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
           blk[k] = a.w_first * s;
         }
       };
-      for (int t = threadIdx.x; t < C::HROWS * C::HCOLS; t += NT) {
+      for (int t = threadIdx.x; t < C::HROWS * C::HCOLS; t += C::NTH) {
         const int r = t / C::HCOLS, c = t - r * C::HCOLS;
         dmul(const_cast<double*>(H(r, c)), op.Dh);
       }
-      for (int t = threadIdx.x; t < C::VROWS * C::VCOLS; t += NT) {
+      for (int t = threadIdx.x; t < C::VROWS * C::VCOLS; t += C::NTH) {
         const int r = t / C::VCOLS, c = t - r * C::VCOLS;
         dmul(const_cast<double*>(V(c, r)), op.Dv);
       }
-      consumer_sync();
+      consumer_sync<C::NTH>();
     }
   }
   if constexpr (EPI == EPI_BJ && N1 >= 2) {
@@ -817,17 +817,17 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
           blk[k] = s;
         }
       };
-      for (int t = threadIdx.x; t < C::HROWS * C::HCOLS; t += NT) {
+      for (int t = threadIdx.x; t < C::HROWS * C::HCOLS; t += C::NTH) {
         const int r = t / C::HCOLS, c = t - r * C::HCOLS;
         const int ig = i0 - 1 + c, jg = j0 - 1 + r;
         if (ig >= 0 && ig < a.nx && jg >= 1 && jg <= a.ny - 1) padd(const_cast<double*>(H(r, c)), hblk(a.nx, ig, jg));
       }
-      for (int t = threadIdx.x; t < C::VROWS * C::VCOLS; t += NT) {
+      for (int t = threadIdx.x; t < C::VROWS * C::VCOLS; t += C::NTH) {
         const int c = t / C::VROWS, r = t - c * C::VROWS;   // consecutive threads walk a column
         const int ig = i0 - 1 + c, jg = j0 - 1 + r;
         if (ig >= 1 && ig <= a.nx - 1 && jg >= 0 && jg < a.ny) padd(const_cast<double*>(V(c, r)), vblk(a.nh, a.ny, ig, jg));
       }
-      consumer_sync();
+      consumer_sync<C::NTH>();
     }
   }
   double ov[F][N1];
@@ -953,7 +953,7 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
   }
   }
   // ---- outputs -> shared (x buffer is consumed) -> contiguous global runs
-  consumer_sync();
+  consumer_sync<C::NTH>();
   double* Yv = buf;                       // [col tx][row r][NO], column stride YCS (odd)
   double* Yh = buf + TX * C::YCS;         // stored mode: [row r][tx][NO]
 #pragma unroll
@@ -965,7 +965,7 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
       if constexpr (STORED) Yh[(r * TX + tx) * NO + k] = ohs[f][k];
     }
   }
-  consumer_sync();
+  consumer_sync<C::NTH>();
   if (a.out == nullptr) return;  // norm-only residual
 #ifdef HDG_EXP_NOOUT
   if (a.nx > 0) return;
@@ -975,8 +975,8 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
     // h rows: facets h(i0 .. i0+TX-1, j) -> blocks (j-1)*nx + i, contiguous
     const int hcount = min(TX, a.nx - i0) * NO;
 #pragma unroll
-    for (int rr = 0; rr < C::TY / NWARP; ++rr) {
-      const int r = w + rr * NWARP;
+    for (int rr = 0; rr < C::TY / C::NW; ++rr) {
+      const int r = w + rr * C::NW;
       const int j = j0 + r;
       if (j >= 1 && j <= a.ny - 1) {
         double* dst = a.out + hblk(a.nx, i0, j) * NO + lane;
@@ -990,8 +990,8 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
   // v columns: facets v(i, j0 .. j0+TY-1) -> blocks nh + (i-1)*ny + j, contiguous
   const int vcount = min(C::TY, a.ny - j0) * NO;
 #pragma unroll
-  for (int cc = 0; cc < TX / NWARP; ++cc) {
-    const int c = w + cc * NWARP;
+  for (int cc = 0; cc < TX / C::NW; ++cc) {
+    const int c = w + cc * C::NW;
     const int iv = i0 + c;
     if (iv >= 1 && iv <= a.nx - 1) {
       double* dst = a.out + vblk(a.nh, a.ny, iv, j0) * NO + lane;
@@ -1006,7 +1006,7 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
 // Persistent, double-buffered: CTA c walks tiles c, c + grid, ...; the next tile's stencil
 // values stream into the other shared buffer (cp.async group) while this tile computes.
 template <int N1, bool STORED, int EPI>
-__global__ void __launch_bounds__(NT, STORED ? 2 : (N1 <= 9 ? HDG_MINB : 1))
+__global__ void __launch_bounds__(Cfg<N1, STORED>::NTH, Cfg<N1, STORED>::MINB)
 trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 : N1)> op) {
   using C = Cfg<N1, STORED>;
   extern __shared__ __align__(16) double smem[];
@@ -1019,7 +1019,7 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
   double nrm = 0.0;
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int q = 0; q < NB; ++q) mbar_init(&bars[q], NWARP + NT);  // lane-0 expect_tx + per-thread LDGSTS arrivals
+    for (int q = 0; q < NB; ++q) mbar_init(&bars[q], C::NW + C::NTH);  // lane-0 expect_tx + per-thread LDGSTS arrivals
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -1047,91 +1047,14 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
   }
   if constexpr (EPI == EPI_RES) {
     if (a.partials != nullptr) {
-      __shared__ double red[NWARP];
+      __shared__ double red[C::NW];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
       if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
       __syncthreads();
       if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int q = 0; q < NWARP; ++q) t += red[q];
-        a.partials[blockIdx.x] = t;
-      }
-    }
-  }
-}
-
-// ----------------------------------------------------------------- warp-specialized variant
-// One producer warp (warp NWARP) streams tiles into an NB-slot ring; the NWARP compute warps
-// only compute.  full[slot]: 1 expect_tx arrival (producer lane 0) + 32 LDGSTS arrivals;
-// empty[slot]: NT consumer arrivals.
-template <int N1, bool ST>
-__device__ __forceinline__ void produce_tile(const MvArgs& a, double* buf, int i0, int j0, uint64_t* full) {
-  using C = Cfg<N1, ST>;
-  const int lane = threadIdx.x & 31;
-  const bool edge = (i0 == 0) || (j0 == 0) || (i0 + TX >= a.nx) || (j0 + C::TY >= a.ny);
-  if (edge) {
-    for (int r = 0; r < C::HROWS; ++r) run_zero(buf, h_run<N1, ST>(a, i0, j0, r), lane);
-  }
-  stage_v_columns<N1, ST>(a, buf + C::HSZ, i0, j0, 0, 1, lane);
-  __syncwarp();
-  if (lane == 0) {
-    unsigned bytes = 0;
-    for (int r = 0; r < C::HROWS; ++r) bytes += run_bytes(h_run<N1, ST>(a, i0, j0, r));
-    fence_proxy_async();
-    mbar_arrive_expect_tx(full, bytes);
-    for (int r = 0; r < C::HROWS; ++r) run_issue(a.x, buf, h_run<N1, ST>(a, i0, j0, r), full);
-  }
-  cp_async_mbar_arrive(full);
-}
-
-template <int N1, bool STORED, int EPI>
-__global__ void __launch_bounds__(NT + 32, HDG_WS_MINB)
-trace_apply_ws_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 : N1)> op) {
-  using C = Cfg<N1, STORED>;
-  constexpr int NB = C::NBUF;
-  extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(8) uint64_t full[NB], empty[NB];
-  const int tiles_x = (a.nx + TX - 1) / TX;
-  const int ntiles = tiles_x * ((a.ny + C::TY - 1) / C::TY);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      mbar_init(&full[q], 1 + 32);
-      mbar_init(&empty[q], NT);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  int slot = 0;
-  unsigned phase = 0;
-  if (threadIdx.x >= NT) {  // ---- producer warp
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      mbar_wait(&empty[slot], phase ^ 1u);
-      produce_tile<N1, STORED>(a, smem + slot * C::BUF, (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, &full[slot]);
-      if (++slot == NB) { slot = 0; phase ^= 1u; }
-    }
-    return;
-  }
-  double nrm = 0.0;             // ---- compute warps
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    mbar_wait(&full[slot], phase);
-    compute_tile<N1, STORED, EPI>(a, op, smem + slot * C::BUF, smem + NB * C::BUF + (threadIdx.x >> 5) * C::WSCR,
-                                  (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
-    consumer_sync();
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[slot])) : "memory");
-    if (++slot == NB) { slot = 0; phase ^= 1u; }
-  }
-  if constexpr (EPI == EPI_RES) {
-    if (a.partials != nullptr) {
-      __shared__ double red[NWARP];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
-      consumer_sync();
-      if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int q = 0; q < NWARP; ++q) t += red[q];
+        for (int q = 0; q < C::NW; ++q) t += red[q];
         a.partials[blockIdx.x] = t;
       }
     }
