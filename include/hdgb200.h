@@ -73,6 +73,21 @@ int hdg_bj_sweeps(const hdg_level* lev, const double* b, double* x, double* work
 
 /* y = A x  (trace.py:87-94) */
 int hdg_matvec(const hdg_level* lev, const double* x, double* y, void* stream);
+
+/* Facet-plane device layout (hdg_soa.cuh) for shared-block levels (constant coefficient on a
+ * uniform mesh, p <= 8).  Replaces the same TraceSystem.matvec_free (trace.py:87-94) for callers
+ * that keep their trace vectors resident on the device across many applies: node k of every
+ * facet line is one contiguous run (boundary facets and pad slots stored as zeros), so the apply
+ * streams coalesced rows with no shared-memory staging.
+ *   hdg_soa_length  -> number of doubles of one facet-plane vector (prepares the level)
+ *   hdg_soa_pack    -> reference layout (ndof) -> facet planes (writes every slot)
+ *   hdg_soa_unpack  -> facet planes -> reference layout
+ *   hdg_matvec_soa  -> y = A x in facet planes; writes every slot of y (not in place)
+ * HDG_EINVAL for stored levels or an element block that is not mirror-invariant. */
+int hdg_soa_length(hdg_level* lev, int64_t* n);
+int hdg_soa_pack(hdg_level* lev, const double* x, double* x_soa, void* stream);
+int hdg_soa_unpack(hdg_level* lev, const double* x_soa, double* x, void* stream);
+int hdg_matvec_soa(hdg_level* lev, const double* x_soa, double* y_soa, void* stream);
 /* r = b - A x; if norm2_out != NULL also writes ||b - A x||^2 (one double, device) */
 int hdg_residual(const hdg_level* lev, const double* b, const double* x, double* r,
                  double* norm2_out, void* stream);

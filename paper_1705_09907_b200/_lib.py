@@ -30,6 +30,10 @@ SIGNATURES = [
     ("hdg_level_operator_bytes", c_int64, [c_void_p]),
     ("hdg_level_set_blockjacobi", c_int, [c_void_p, ctypes.c_double]),
     ("hdg_matvec", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("hdg_soa_length", c_int, [c_void_p, ctypes.POINTER(c_int64)]),
+    ("hdg_soa_pack", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("hdg_soa_unpack", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("hdg_matvec_soa", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     ("hdg_residual", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("hdg_bj_sweep", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("hdg_level_set_bj_chebyshev", c_int, [c_void_p, ctypes.c_double, ctypes.c_double]),

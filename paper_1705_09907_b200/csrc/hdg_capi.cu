@@ -3,12 +3,14 @@
 // Reference interfaces replaced: see include/hdgb200.h (each entry cites trace.py / multigrid.py).
 #include "hdgb200.h"
 #include "hdg_kernels.cuh"
+#include "hdg_soa.cuh"
 
 #include <algorithm>
 #include <climits>
 #include <atomic>
 #define _USE_MATH_DEFINES
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -16,6 +18,8 @@
 #include <vector>
 
 using namespace hdg;
+
+static const int SOA_MAXN1 = 9;
 
 static thread_local std::string g_err;
 static std::atomic<long long> g_launches{0};
@@ -64,6 +68,11 @@ struct hdg_level {
   double *g_val = nullptr, *gt_val = nullptr;
   double lam_max = 1.0, cheb_frac = 0.15, fsai_omega = 1.0;
   double* tail_wd = nullptr;   // fused coarse tail, shared mode: device copy of Wh, Wv, Dh, Dv (n1 = 2)
+  // facet-plane (SoA) device layout, shared mode (hdg_soa.cuh): element block + adapted blocks
+  std::vector<double> blk;     // the 4n1 x 4n1 element block (shared mode)
+  int soa_state = 0;           // 0: not prepared, 1: ready, -1: not available for this level
+  std::vector<double> soaM;
+  int soaW = 0, soaJ = 0, soaSeg = 0;
 };
 
 struct hdg_transfer {
@@ -320,6 +329,7 @@ int hdg_level_create_shared(int nx, int ny, int p, const double* block, hdg_leve
   int rc = init_level(L, nx, ny, p);
   if (rc) { delete L; return rc; }
   const int n1 = L->n1, Lw = 4 * n1;
+  L->blk.assign(block, block + (size_t)Lw * Lw);
   L->Wh.assign(7 * n1 * n1, 0.0);
   L->Wv.assign(7 * n1 * n1, 0.0);
   for (int vert = 0; vert < 2; ++vert) {
@@ -1152,6 +1162,184 @@ int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int n
   CK(cudaGraphLaunch(it->second.exec, s));
   g_launches.fetch_add(it->second.nkern);
   return 0;
+}
+
+}  // extern "C"
+
+// ----------------------------------------------------------- facet-plane (SoA) layout
+
+// Symmetry-adapted blocks of the element block (hdg_soa.cuh).  T = forward butterflies (rows
+// orthogonal, T T^T = D), y = T^T M T x with M = D^-1 T S T^T D^-1; M is block diagonal when S
+// commutes with both element mirrors.  Off-block entries above 1e-11 max|M| -> not available.
+template <int N1>
+static bool soa_reduce(const std::vector<double>& S, std::vector<double>& out) {
+  using C = SoaCfg<N1>;
+  constexpr int NT = 4 * N1;
+  std::vector<double> T(NT * NT), TT(NT * NT);
+  for (int j = 0; j < NT; ++j) {                      // columns of T
+    double x[NT] = {}, t[NT];
+    x[j] = 1.0;
+    soa_forward<N1>(x, x + N1, x + 2 * N1, x + 3 * N1, t);
+    for (int i = 0; i < NT; ++i) T[i * NT + j] = t[i];
+  }
+  for (int i = 0; i < NT; ++i) {                      // columns of the backward map must be rows of T
+    double t[NT] = {}, y[NT];
+    t[i] = 1.0;
+    soa_backward<N1>(t, y, y + N1, y + 2 * N1, y + 3 * N1);
+    for (int j = 0; j < NT; ++j)
+      if (y[j] != T[i * NT + j]) return false;
+  }
+  std::vector<double> D(NT, 0.0);
+  for (int i = 0; i < NT; ++i) {
+    for (int j = 0; j < NT; ++j) D[i] += T[i * NT + j] * T[i * NT + j];
+    for (int m = 0; m < NT; ++m)
+      if (m != i) {
+        double dot = 0.0;
+        for (int j = 0; j < NT; ++j) dot += T[i * NT + j] * T[m * NT + j];
+        if (dot != 0.0) return false;
+      }
+  }
+  std::vector<double> A(NT * NT, 0.0), M(NT * NT, 0.0);   // A = S T^T, M = T A / (D_i D_j)
+  for (int r = 0; r < NT; ++r)
+    for (int m = 0; m < NT; ++m) {
+      double acc = 0.0;
+      for (int j = 0; j < NT; ++j) acc += S[r * NT + j] * T[m * NT + j];
+      A[r * NT + m] = acc;
+    }
+  double mx = 0.0;
+  for (int i = 0; i < NT; ++i)
+    for (int m = 0; m < NT; ++m) {
+      double acc = 0.0;
+      for (int r = 0; r < NT; ++r) acc += T[i * NT + r] * A[r * NT + m];
+      M[i * NT + m] = acc / (D[i] * D[m]);
+      mx = std::fmax(mx, std::fabs(M[i * NT + m]));
+    }
+  const int off[5] = {0, C::A0, C::A0 + C::A1, C::A0 + C::A1 + C::A2, NT};
+  auto cls = [&](int i) { int c = 0; while (i >= off[c + 1]) ++c; return c; };
+  double defect = 0.0;
+  for (int i = 0; i < NT; ++i)
+    for (int m = 0; m < NT; ++m)
+      if (cls(i) != cls(m)) defect = std::fmax(defect, std::fabs(M[i * NT + m]));
+  if (!(defect <= 1e-11 * mx)) return false;
+  out.clear();
+  for (int c = 0; c < 4; ++c)
+    for (int i = off[c]; i < off[c + 1]; ++i)
+      for (int m = off[c]; m < off[c + 1]; ++m) out.push_back(M[i * NT + m]);
+  return (int)out.size() == C::MSZ;
+}
+
+template <int N1>
+static int soa_occupancy() {
+  static int occ = -1;
+  if (occ < 0) {
+    cudaFuncSetAttribute(soa_apply_kernel<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, soa_smem_bytes<N1>());
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, soa_apply_kernel<N1>, SoaCfg<N1>::NTH,
+                                                      soa_smem_bytes<N1>()) != cudaSuccess || occ < 1)
+      occ = 1;
+  }
+  return occ;
+}
+
+static int soa_prepare(hdg_level* L) {
+  if (L->soa_state == 1) return 0;
+  if (L->soa_state == -1 || L->stored || L->blk.empty() || L->n1 > SOA_MAXN1)
+    return fail(HDG_EINVAL, "facet-plane layout needs a shared-block (constant coefficient, mirror-symmetric) "
+                            "level with p <= 8");
+  bool ok = false;
+  int occ = 1;
+#define SOA_PREP(N) { ok = soa_reduce<N>(L->blk, L->soaM); occ = soa_occupancy<N>(); break; }
+  switch (L->n1) {
+    case 2: SOA_PREP(2) case 3: SOA_PREP(3) case 4: SOA_PREP(4) case 5: SOA_PREP(5)
+    case 6: SOA_PREP(6) case 7: SOA_PREP(7) case 8: SOA_PREP(8) case 9: SOA_PREP(9)
+    default: break;
+  }
+#undef SOA_PREP
+  if (!ok) {
+    L->soa_state = -1;
+    return fail(HDG_EINVAL, "element block is not invariant under the element mirrors: no facet-plane apply");
+  }
+  L->soaW = std::max(1, (L->nx + 30) / 31);           // owned columns 31w .. 31w+30 cover 0 .. nx-1
+  // one wave of warps, equal row segments (each pays one ghost row)
+  const long long resident = (long long)sm_count() * occ * (SoaCfg<2>::NTH / 32);
+  long long nseg = std::max(1LL, resident / L->soaW);
+  if (nseg > L->ny) nseg = L->ny;
+  int J = (int)((L->ny + nseg - 1) / nseg);
+  if (const char* e = std::getenv("HDG_SOA_J")) J = std::max(1, std::atoi(e));
+  L->soaJ = J;
+  L->soaSeg = (L->ny + J - 1) / J;
+  L->soa_state = 1;
+  return 0;
+}
+
+static long long soa_len(const hdg_level* L) {
+  return (long long)(L->ny + 1) * L->soaW * L->n1 * 66;
+}
+
+template <int N1>
+static int soa_apply_t(const hdg_level* L, const double* xs, double* ys, cudaStream_t s) {
+  SoaArgs<N1> a{};
+  a.x = xs; a.y = ys;
+  a.nx = L->nx; a.ny = L->ny; a.W = L->soaW; a.J = L->soaJ; a.nseg = L->soaSeg;
+  std::memcpy(a.M, L->soaM.data(), sizeof(a.M));
+  const long long warps = (long long)a.W * a.nseg;
+  const int wpb = SoaCfg<N1>::NTH / 32;
+  soa_apply_kernel<N1><<<(unsigned)((warps + wpb - 1) / wpb), SoaCfg<N1>::NTH, soa_smem_bytes<N1>(), s>>>(a);
+  CKL();
+  return 0;
+}
+
+extern "C" {
+
+int hdg_soa_length(hdg_level* L, int64_t* n) {
+  if (!L || !n) return fail(HDG_EINVAL, "null argument");
+  int rc = soa_prepare(L);
+  if (rc) return rc;
+  *n = soa_len(L);
+  return 0;
+}
+
+int hdg_soa_pack(hdg_level* L, const double* x, double* xs, void* stream) {
+  if (!L || (!x && L->ndof) || !xs) return fail(HDG_EINVAL, "null argument");
+  int rc = soa_prepare(L);
+  if (rc) return rc;
+  const long long total = soa_len(L);
+  const unsigned grid = (unsigned)((total + 255) / 256);
+#define SOA_PACK(N) { soa_pack_kernel<N><<<grid, 256, 0, S(stream)>>>(x, xs, L->nx, L->ny, L->soaW, L->nh, total); CKL(); return 0; }
+  switch (L->n1) {
+    case 2: SOA_PACK(2) case 3: SOA_PACK(3) case 4: SOA_PACK(4) case 5: SOA_PACK(5)
+    case 6: SOA_PACK(6) case 7: SOA_PACK(7) case 8: SOA_PACK(8) case 9: SOA_PACK(9)
+    default: return fail(HDG_EINVAL, "facet-plane layout: p <= 8");
+  }
+#undef SOA_PACK
+}
+
+int hdg_soa_unpack(hdg_level* L, const double* xs, double* x, void* stream) {
+  if (!L || !xs || (!x && L->ndof)) return fail(HDG_EINVAL, "null argument");
+  int rc = soa_prepare(L);
+  if (rc) return rc;
+  if (L->ndof == 0) return 0;
+  const unsigned grid = (unsigned)((L->ndof + 255) / 256);
+#define SOA_UNPACK(N) { soa_unpack_kernel<N><<<grid, 256, 0, S(stream)>>>(xs, x, L->nx, L->ny, L->soaW, L->nh, L->ndof); CKL(); return 0; }
+  switch (L->n1) {
+    case 2: SOA_UNPACK(2) case 3: SOA_UNPACK(3) case 4: SOA_UNPACK(4) case 5: SOA_UNPACK(5)
+    case 6: SOA_UNPACK(6) case 7: SOA_UNPACK(7) case 8: SOA_UNPACK(8) case 9: SOA_UNPACK(9)
+    default: return fail(HDG_EINVAL, "facet-plane layout: p <= 8");
+  }
+#undef SOA_UNPACK
+}
+
+int hdg_matvec_soa(hdg_level* L, const double* xs, double* ys, void* stream) {
+  if (!L || !xs || !ys) return fail(HDG_EINVAL, "null argument");
+  if (xs == ys) return fail(HDG_EINVAL, "facet-plane apply cannot run in place");
+  int rc = soa_prepare(L);
+  if (rc) return rc;
+#define SOA_APPLY(N) return soa_apply_t<N>(L, xs, ys, S(stream));
+  switch (L->n1) {
+    case 2: SOA_APPLY(2) case 3: SOA_APPLY(3) case 4: SOA_APPLY(4) case 5: SOA_APPLY(5)
+    case 6: SOA_APPLY(6) case 7: SOA_APPLY(7) case 8: SOA_APPLY(8) case 9: SOA_APPLY(9)
+    default: return fail(HDG_EINVAL, "facet-plane layout: p <= 8");
+  }
+#undef SOA_APPLY
 }
 
 }  // extern "C"

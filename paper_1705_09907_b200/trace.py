@@ -152,6 +152,30 @@ class BlockOperator:
             check(lib.hdg_matvec(self.handle, dev.ptr(xd), dev.ptr(y), dev.stream()))
         return dev.back(y, was_np)
 
+    # -- facet-plane device layout (shared-block levels; hdg_soa.cuh) ------------------------
+    def planes_length(self):
+        n = ctypes.c_int64()
+        check(lib.hdg_soa_length(self.handle, ctypes.byref(n)))
+        return int(n.value)
+
+    def to_planes(self, x, out=None):
+        xd, _ = dev.to_device(x)
+        if xd.numel() != self.ndof:
+            raise ValueError(f"expected {self.ndof} trace values, got {xd.numel()}")
+        xs = dev.empty(self.planes_length()) if out is None else out
+        check(lib.hdg_soa_pack(self.handle, dev.ptr(xd), dev.ptr(xs), dev.stream()))
+        return xs
+
+    def from_planes(self, xs, out=None):
+        y = dev.empty(self.ndof) if out is None else out
+        check(lib.hdg_soa_unpack(self.handle, dev.ptr(xs), dev.ptr(y), dev.stream()))
+        return y
+
+    def apply_planes(self, xs, out=None):
+        ys = dev.empty(self.planes_length()) if out is None else out
+        check(lib.hdg_matvec_soa(self.handle, dev.ptr(xs), dev.ptr(ys), dev.stream()))
+        return ys
+
     def residual_norm(self, b, x):
         """||b - A x|| on the device; one scalar crosses to the host."""
         out = dev.empty(1)
@@ -500,10 +524,21 @@ class TraceSystem:
 
     # -- matrix-free application --------------------------------------------------------------
     def matvec_free(self, x):
-        """y = A x on the GPU (trace.py:87-94).  numpy in -> numpy out; CUDA tensor -> tensor."""
+        """y = A x on the GPU (trace.py:87-94).  numpy in -> numpy out; CUDA tensor -> tensor;
+        FacetPlanes (device-resident facet-plane layout) -> FacetPlanes."""
+        if isinstance(x, FacetPlanes):
+            if x.system is not self:
+                raise ValueError("FacetPlanes belongs to another TraceSystem")
+            return FacetPlanes(self, self.operator.apply_planes(x.data))
         if self.ndof == 0:
             return np.zeros(0) if not hasattr(x, "is_cuda") else x.new_zeros(0)
         return self.operator.apply(x)
+
+    def facet_planes(self, x):
+        """Keep a trace vector resident on the device in the facet-plane layout (node k of every
+        facet line contiguous): repeated matvec_free calls on it stream coalesced rows.  Shared-block
+        (constant coefficient) systems with p <= 8; raises otherwise."""
+        return FacetPlanes(self, self.operator.to_planes(x))
 
     def gather_element(self, x, e):
         """trace.py:81-85 (host view)."""
@@ -593,3 +628,20 @@ def flop_memop_count(system, mode):
     else:
         raise ValueError(f"unknown matvec mode {mode!r}")
     return {"flops": int(flops), "bytes": int(bytes_), "ai": flops / bytes_ if bytes_ else 0.0}
+
+
+class FacetPlanes:
+    """A trace vector of one TraceSystem held on the device in the facet-plane layout
+    (include/hdgb200.h: hdg_soa_*).  matvec_free(FacetPlanes) -> FacetPlanes; .numpy() / .tensor()
+    return the reference layout (trace.py:39-41)."""
+
+    __slots__ = ("system", "data")
+
+    def __init__(self, system, data):
+        self.system, self.data = system, data
+
+    def tensor(self, out=None):
+        return self.system.operator.from_planes(self.data, out)
+
+    def numpy(self):
+        return self.tensor().cpu().numpy()
