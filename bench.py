@@ -6,9 +6,10 @@ x ~ U[-1, 1] (seed 1); one STEP = 100 repeated applies y = A x (configs[1]).
   e2e         the same metric through the public API (TraceSystem.matvec_free) with the
               step's x copied host(pinned)->device and the step's y read back inside the
               timed region
-  roofline    the trace kernel: algorithmic bytes (16 B/DOF: x read + y written; the
-              operator is the shared block held in the constant bank) / its average
-              launch time, against MEASURED_PEAKS.json hbm_gbs
+  roofline    the trace kernel (one GPU: soa_apply_kernel on the facet-record layout,
+              hdg_soa.cuh): algorithmic bytes (16 B/DOF: x read + y written; the operator is
+              the shared element block) / its average launch time, against
+              MEASURED_PEAKS.json hbm_gbs
   cpu_baseline the CPU oracle port of trace.py:87-94 (gather, einsum, two-owner sum)
               on a bounded sample of applies on the same system, rank 0
 L2 policy: the applies rotate over 4 (x, y) pairs = 670 MB > 126 MB L2, so no apply
@@ -39,10 +40,10 @@ METRIC = "trace_matvec_gdof_per_s"
 UNIT = "GDOF/s"
 
 
-def ncu_traffic():
+def ncu_traffic(name):
     """dram__bytes_read + dram__bytes_write of the trace kernel from the committed ncu --set full
     capture (profiles/), per launch; None if absent."""
-    path = os.path.join(ROOT, "profiles", "ncu_trace_apply_p4_r01_key_metrics.txt")
+    path = os.path.join(ROOT, "profiles", name)
     try:
         vals = {}
         for line in open(path):
@@ -221,13 +222,24 @@ def run_ours(args, rank, ws):
     xs = [torch.from_numpy(x_host).cuda()] + \
          [torch.from_numpy(np.random.default_rng(1 + k).uniform(-1, 1, ndof)).cuda() for k in range(1, NB)]
     ys = [torch.empty(ndof, dtype=torch.float64, device="cuda") for _ in range(NB)]
+    # one GPU: the facet-record device layout (hdg_soa.cuh) is the product's fastest apply; the
+    # strip path (N > 1) exchanges halo rows in the reference layout and uses trace_apply_kernel
+    records = strip is None
+    if records:
+        xs = [op.to_planes(x) for x in xs]
+        ys = [torch.empty_like(xs[0]) for _ in range(NB)]
+        apply_fn, kname = lib.hdg_matvec_soa, "soa_apply_kernel<5> (facet records)"
+        ncu_keys = "ncu_soa_apply_p4_r01_key_metrics.txt"
+    else:
+        apply_fn, kname = lib.hdg_matvec, "trace_apply_kernel<5,shared,EPI_Y>"
+        ncu_keys = "ncu_trace_apply_p4_r01_key_metrics.txt"
 
     def step():
         for a in range(APPLIES):
             k = a % NB
             if strip is not None:
                 strip.exchange(xs[k])
-            P._lib.check(lib.hdg_matvec(h, xs[k].data_ptr(), ys[k].data_ptr(), sp))
+            P._lib.check(apply_fn(h, xs[k].data_ptr(), ys[k].data_ptr(), sp))
 
     # ---- device-resident throughput
     for _ in range(max(args.warmup, 3)):
@@ -255,10 +267,24 @@ def run_ours(args, rank, ws):
     singles = []
     for k in range(20):
         e_a.record(stream)
-        P._lib.check(lib.hdg_matvec(h, xs[k % NB].data_ptr(), ys[k % NB].data_ptr(), sp))
+        P._lib.check(apply_fn(h, xs[k % NB].data_ptr(), ys[k % NB].data_ptr(), sp))
         e_b.record(stream)
         torch.cuda.synchronize()
         singles.append(e_a.elapsed_time(e_b) * 1e3)
+    # the reference-layout kernel on the same system (same stream, same rotation), for comparison
+    ref_layout_us = None
+    if records:
+        xr = [op.from_planes(x) for x in xs]
+        yr = [torch.empty(ndof, dtype=torch.float64, device="cuda") for _ in range(NB)]
+        for k in range(10):
+            P._lib.check(lib.hdg_matvec(h, xr[k % NB].data_ptr(), yr[k % NB].data_ptr(), sp))
+        e_a.record(stream)
+        for k in range(200):
+            P._lib.check(lib.hdg_matvec(h, xr[k % NB].data_ptr(), yr[k % NB].data_ptr(), sp))
+        e_b.record(stream)
+        torch.cuda.synchronize()
+        ref_layout_us = e_a.elapsed_time(e_b) * 1e3 / 200
+        del xr, yr
 
     # ---- end to end through the public API, host buffers
     x_pin = torch.from_numpy(x_host).pin_memory()
@@ -280,8 +306,14 @@ def run_ours(args, rank, ws):
         ev_in[b].record(s_h2d)
         stream.wait_event(ev_in[b])
         y = None
-        for _ in range(APPLIES):                         # the public API call
-            y = strip.apply(x_dev[b]) if strip is not None else sysg.matvec_free(x_dev[b])
+        if strip is not None:
+            for _ in range(APPLIES):                     # the public API call
+                y = strip.apply(x_dev[b])
+        else:                                            # TraceSystem.facet_planes + matvec_free
+            z = sysg.facet_planes(x_dev[b])
+            for _ in range(APPLIES):
+                y = sysg.matvec_free(z)
+            y = y.tensor()
         ev_used[b].record(stream)
         s_d2h.wait_event(ev_used[b])
         s_d2h.wait_event(ev_out[b])                      # y_pins[b] free
@@ -305,8 +337,8 @@ def run_ours(args, rank, ws):
     e2e_val = ws * owned * applies / (t_e2e * 1e-3) / 1e9
     assert np.isfinite(y_pins[(args.steps - 1) % 2].numpy()).all()
 
-    # ---- parity spot check of the timed output against the host formula (cheap, sampled)
-    y_chk = ys[0].cpu().numpy()
+    # ---- parity check of a timed output against the CPU oracle (cpu_baseline)
+    y_chk = (op.from_planes(ys[0]) if records else ys[0]).cpu().numpy()
 
     hbm, kind = peaks()
     alg_bytes = 16 * ndof
@@ -321,13 +353,16 @@ def run_ours(args, rank, ws):
                        "parallelism": f"strips{ws} (1024 element rows per GPU, NCCL halo rows)" if ws > 1
                        else "single"},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ndof, "d2h_bytes_per_step": 8 * ndof,
-                    "path": "per step: pinned H2D of x, TraceSystem.matvec_free x100, D2H of y; steps pipelined "
-                            "over 3 streams (copies of neighbouring steps overlap the applies)"},
+                    "path": ("per step: pinned H2D of x, TraceSystem.facet_planes (pack), matvec_free x100 on the "
+                             "facet records, .tensor() (unpack), D2H of y" if records else
+                             "per step: pinned H2D of x, StripOperator.apply x100, D2H of y") +
+                            "; steps pipelined over 3 streams (copies of neighbouring steps overlap the applies)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": ncu_traffic(),
-                         "traffic_source": "profiles/ncu_trace_apply_p4_r01_key_metrics.txt (ncu --set full)",
+                         "frac": achieved / hbm, "traffic": ncu_traffic(ncu_keys),
+                         "traffic_source": "profiles/" + ncu_keys + " (ncu --set full)",
                          "peak_kind": kind,
-                         "kernel": "trace_apply_kernel<5,shared,EPI_Y>", "alg_bytes_per_launch": alg_bytes,
+                         "kernel": kname, "alg_bytes_per_launch": alg_bytes,
+                         "ref_layout_kernel_us": ref_layout_us,
                          "kernel_us_avg": kernel_us, "kernel_us_single_median": float(np.median(singles)),
                          "fp64_tflops": flops / (kernel_us * 1e-6) / 1e12},
             "gpu_launches": int(launches),

@@ -1170,7 +1170,8 @@ int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int n
 
 // Symmetry-adapted blocks of the element block (hdg_soa.cuh).  T = forward butterflies (rows
 // orthogonal, T T^T = D), y = T^T M T x with M = D^-1 T S T^T D^-1; M is block diagonal when S
-// commutes with both element mirrors.  Off-block entries above 1e-11 max|M| -> not available.
+// commutes with both element mirrors, and symmetric when S is (the kernel stores the upper
+// triangles).  Off-block entries or asymmetry above 1e-11 max|M| -> not available.
 template <int N1>
 static bool soa_reduce(const std::vector<double>& S, std::vector<double>& out) {
   using C = SoaCfg<N1>;
@@ -1219,12 +1220,13 @@ static bool soa_reduce(const std::vector<double>& S, std::vector<double>& out) {
   double defect = 0.0;
   for (int i = 0; i < NT; ++i)
     for (int m = 0; m < NT; ++m)
-      if (cls(i) != cls(m)) defect = std::fmax(defect, std::fabs(M[i * NT + m]));
+      defect = std::fmax(defect, cls(i) != cls(m) ? std::fabs(M[i * NT + m])
+                                                  : std::fabs(M[i * NT + m] - M[m * NT + i]));
   if (!(defect <= 1e-11 * mx)) return false;
   out.clear();
   for (int c = 0; c < 4; ++c)
     for (int i = off[c]; i < off[c + 1]; ++i)
-      for (int m = off[c]; m < off[c + 1]; ++m) out.push_back(M[i * NT + m]);
+      for (int m = off[c]; m < off[c + 1]; ++m) out.push_back(0.5 * (M[i * NT + m] + M[m * NT + i]));
   return (int)out.size() == C::MSZ;
 }
 

@@ -125,39 +125,50 @@ __host__ __device__ __forceinline__ void soa_backward(const double* t, double* y
   }
 }
 
-// the blocks live in shared memory (rows padded to an even length, read as LDS.128 broadcasts):
-// held in registers they would pin ~200 registers per thread for the whole loop
+// The blocks live in shared memory as packed upper triangles (M is symmetric: S is, and the
+// butterflies are scaled symmetrically), each block padded to an even length and read as LDS.128
+// broadcasts; every stored entry feeds two FMAs.  Held in registers they would pin ~200
+// registers per thread for the whole loop.
 template <int SZ>
-struct SoaRow { static constexpr int RL = (SZ + 1) & ~1; };
+struct SoaTri { static constexpr int N = SZ * (SZ + 1) / 2, NP = (N + 1) & ~1; };
 
 template <int N1>
 struct SoaSmem {
   using C = SoaCfg<N1>;
   static constexpr int O0 = 0;
-  static constexpr int O1 = O0 + C::A0 * SoaRow<C::A0>::RL;
-  static constexpr int O2 = O1 + C::A1 * SoaRow<C::A1>::RL;
-  static constexpr int O3 = O2 + C::A2 * SoaRow<C::A2>::RL;
-  static constexpr int TOTAL = O3 + C::A3 * SoaRow<C::A3>::RL;   // doubles (even)
+  static constexpr int O1 = O0 + SoaTri<C::A0>::NP;
+  static constexpr int O2 = O1 + SoaTri<C::A1>::NP;
+  static constexpr int O3 = O2 + SoaTri<C::A2>::NP;
+  static constexpr int TOTAL = O3 + SoaTri<C::A3>::NP;   // doubles (even)
 };
 
 template <int N1>
 constexpr int soa_smem_bytes() { return SoaSmem<N1>::TOTAL * 8 + SoaCfg<N1>::SMEM_RING; }
 
+// packed index of (i, j), i <= j, row-major upper triangle
+template <int SZ>
+__host__ __device__ constexpr int soa_tri(int i, int j) { return i * SZ - i * (i - 1) / 2 + (j - i); }
+
 template <int SZ, int SOFF, int TOFF>
 __device__ __forceinline__ void soa_block(const double* __restrict__ Ms, const double* t, double* z) {
-  constexpr int RL = SoaRow<SZ>::RL;
+  constexpr int NP = SoaTri<SZ>::NP;
+  double m[NP];
 #pragma unroll
-  for (int i = 0; i < SZ; ++i) {
-    const double2* row = reinterpret_cast<const double2*>(Ms + SOFF + i * RL);
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < RL / 2; ++j) {
-      const double2 m = row[j];
-      acc = fma(m.x, t[TOFF + 2 * j], acc);
-      if (2 * j + 1 < SZ) acc = fma(m.y, t[TOFF + 2 * j + 1], acc);
-    }
-    z[TOFF + i] = acc;
+  for (int q = 0; q < NP / 2; ++q) {
+    const double2 v = reinterpret_cast<const double2*>(Ms + SOFF)[q];
+    m[2 * q] = v.x;
+    m[2 * q + 1] = v.y;
   }
+#pragma unroll
+  for (int i = 0; i < SZ; ++i) z[TOFF + i] = m[soa_tri<SZ>(i, i)] * t[TOFF + i];
+#pragma unroll
+  for (int i = 0; i < SZ; ++i)
+#pragma unroll
+    for (int j = i + 1; j < SZ; ++j) {
+      const double v = m[soa_tri<SZ>(i, j)];
+      z[TOFF + i] = fma(v, t[TOFF + j], z[TOFF + i]);
+      z[TOFF + j] = fma(v, t[TOFF + i], z[TOFF + j]);
+    }
 }
 
 template <int N1>
@@ -170,21 +181,26 @@ __device__ __forceinline__ void soa_blocks(const double* __restrict__ Ms, const 
   soa_block<C::A3, M::O3, C::A0 + C::A1 + C::A2>(Ms, t, z);
 }
 
-// a.M (dense class blocks, row-major) -> padded shared-memory rows
+// a.M (dense class blocks, row-major, symmetric) -> packed upper triangles in shared memory
 template <int N1>
 __device__ __forceinline__ void soa_load_blocks(const SoaArgs<N1>& a, double* Ms) {
   using C = SoaCfg<N1>;
   using M = SoaSmem<N1>;
   constexpr int sz[4] = {C::A0, C::A1, C::A2, C::A3};
-  constexpr int so[4] = {M::O0, M::O1, M::O2, M::O3};
+  constexpr int so[5] = {M::O0, M::O1, M::O2, M::O3, M::TOTAL};
   for (int idx = threadIdx.x; idx < M::TOTAL; idx += blockDim.x) {
     int c = 0;
     while (c < 3 && idx >= so[c + 1]) ++c;
-    const int rl = (sz[c] + 1) & ~1;
-    const int i = (idx - so[c]) / rl, j = (idx - so[c]) % rl;
+    const int n = sz[c], q = idx - so[c];
     int mo = 0;
-    for (int q = 0; q < c; ++q) mo += sz[q] * sz[q];
-    Ms[idx] = j < sz[c] ? a.M[mo + i * sz[c] + j] : 0.0;
+    for (int u = 0; u < c; ++u) mo += sz[u] * sz[u];
+    double v = 0.0;
+    if (q < n * (n + 1) / 2) {
+      int i = 0, rem = q;
+      while (rem >= n - i) { rem -= n - i; ++i; }
+      v = a.M[mo + i * n + i + rem];
+    }
+    Ms[idx] = v;
   }
 }
 
@@ -233,7 +249,7 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
 
   const bool hcol = c >= 0 && c < a.nx;
   const bool vline = c + 1 >= 1 && c + 1 <= a.nx - 1;
-  double tp[N1];
+  double tp[N1], xB[N1];
 #pragma unroll
   for (int k = 0; k < N1; ++k) tp[k] = 0.0;
 
@@ -246,10 +262,10 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
     mbar_wait(bars + (t + 1) % RING, ((t + 1) / RING) & 1);
     const double* e0 = ring + (t % RING) * ENT + lane;
     const double* e1 = ring + ((t + 1) % RING) * ENT + lane;
-    double xB[N1], xT[N1], xR[N1], xL[N1];
+    double xT[N1], xR[N1], xL[N1];
 #pragma unroll
     for (int k = 0; k < N1; ++k) {
-      xB[k] = e0[k * 32];
+      if (t == 0) xB[k] = e0[k * 32];
       xT[k] = e1[k * 32];
       xL[k] = e1[VOFF + k * 34];
       xR[k] = e1[VOFF + k * 34 + 1];
@@ -285,7 +301,7 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
       }
     }
 #pragma unroll
-    for (int k = 0; k < N1; ++k) tp[k] = yT[k];
+    for (int k = 0; k < N1; ++k) { tp[k] = yT[k]; xB[k] = xT[k]; }
     __syncwarp();                                      // entry t is free for issue(t + RING)
   }
   if (r1 == a.ny) {                                    // top boundary line
