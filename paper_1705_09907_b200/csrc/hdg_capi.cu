@@ -1274,7 +1274,7 @@ static int soa_prepare(hdg_level* L) {
 }
 
 static long long soa_len(const hdg_level* L) {
-  return (long long)(L->ny + 1) * L->soaW * L->n1 * 66;
+  return (long long)(L->ny + 1) * L->soaW * L->n1 * (32 + HDG_SOA_VW);
 }
 
 template <int N1>

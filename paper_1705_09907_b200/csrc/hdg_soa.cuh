@@ -35,6 +35,12 @@
 #ifndef HDG_SOA_EXP
 #define HDG_SOA_EXP 0          // experiment flags (tools/build_variants.sh), 0 in the product
 #endif
+#ifndef HDG_SOA_STCS
+#define HDG_SOA_STCS 0         // experiment: streaming (evict-first) stores of y
+#endif
+#ifndef HDG_SOA_VW
+#define HDG_SOA_VW 34          // V row width of a facet record (36: 32-byte aligned records)
+#endif
 #ifndef HDG_SOA_RING
 #define HDG_SOA_RING 3
 #endif
@@ -52,7 +58,8 @@ struct SoaCfg {
   static constexpr int NTH = 128;
   static constexpr int MINB = N1 <= 3 ? 4 : HDG_SOA_MINB_HI;
   static constexpr int RING = HDG_SOA_RING;              // ring entries per warp (RING-2 rows in flight)
-  static constexpr int ENT = N1 * 66;                    // record: H[N1][32] + V[N1][34] doubles
+  static constexpr int VW = HDG_SOA_VW;                  // V row width (34: slots 0..33)
+  static constexpr int ENT = N1 * (32 + VW);             // record: H[N1][32] + V[N1][VW] doubles
   static constexpr int WSTRIDE = (RING * ENT + RING + 1) & ~1;   // doubles per warp (16-byte multiple)
   static constexpr int SMEM_RING = (NTH / 32) * WSTRIDE * 8;
 };
@@ -208,7 +215,8 @@ template <int N1>
 __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
     soa_apply_kernel(const __grid_constant__ SoaArgs<N1> a) {
   constexpr int NT = 4 * N1, RING = SoaCfg<N1>::RING, D = RING - 1;
-  constexpr int ENT = SoaCfg<N1>::ENT;                 // doubles per record: H[N1][32] | V[N1][34]
+  constexpr int ENT = SoaCfg<N1>::ENT;                 // doubles per record: H[N1][32] | V[N1][VW]
+  constexpr int VW = SoaCfg<N1>::VW;
   constexpr int VOFF = N1 * 32;
   extern __shared__ __align__(16) double smem_soa[];
   double* Ms = smem_soa;
@@ -267,8 +275,8 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
     for (int k = 0; k < N1; ++k) {
       if (t == 0) xB[k] = e0[k * 32];
       xT[k] = e1[k * 32];
-      xL[k] = e1[VOFF + k * 34];
-      xR[k] = e1[VOFF + k * 34 + 1];
+      xL[k] = e1[VOFF + k * VW];
+      xR[k] = e1[VOFF + k * VW + 1];
     }
     double yB[N1], yR[N1], yT[N1], yL[N1];
 #if HDG_SOA_EXP == 1   // experiment: no element product (memory path only)
@@ -292,12 +300,20 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
         const double fromR = __shfl_down_sync(0xffffffffu, yL[k], 1);
         const double hv = hint ? tp[k] + yB[k] : 0.0;
         const double vv = (vline && lane != 31) ? yR[k] + fromR : 0.0;
+#if HDG_SOA_STCS
+        __stcs(hrec + k * 32 + lane, hv);
+        __stcs(vrec + k * VW + lane + 1 + (lane == 31), vv);
+#else
         hrec[k * 32 + lane] = hv;                      // lane 0 duplicates the left tile's slot 31
-        vrec[k * 34 + lane + 1 + (lane == 31)] = vv;   // slots 1..31; lane 31 zeroes pad slot 33
-        if (lane == 30 && w + 1 < W) vrec[ENT + k * 34] = vv;         // duplicate: right tile slot 0
-        if (lane == 0 && w > 0) vrec[-ENT + k * 34 + 32] = vv;        // duplicate: left tile slot 32
-        if (lane == 0 && w == 0) vrec[k * 34] = 0.0;                  // line -1 (pad)
-        if (lane == 31 && w + 1 == W) vrec[k * 34 + 32] = 0.0;        // line 31 W >= nx (pad)
+        vrec[k * VW + lane + 1 + (lane == 31)] = vv;   // slots 1..31; lane 31 zeroes pad slot 33
+#endif
+        if (VW > 34 && lane == 31)
+#pragma unroll
+          for (int q = 34; q < VW; ++q) vrec[k * VW + q] = 0.0;
+        if (lane == 30 && w + 1 < W) vrec[ENT + k * VW] = vv;         // duplicate: right tile slot 0
+        if (lane == 0 && w > 0) vrec[-ENT + k * VW + 32] = vv;        // duplicate: left tile slot 32
+        if (lane == 0 && w == 0) vrec[k * VW] = 0.0;                  // line -1 (pad)
+        if (lane == 31 && w + 1 == W) vrec[k * VW + 32] = 0.0;        // line 31 W >= nx (pad)
       }
     }
 #pragma unroll
@@ -313,8 +329,8 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
     double* vrec = Y + rec(0, w) + VOFF;
 #pragma unroll
     for (int k = 0; k < N1; ++k) {
-      vrec[k * 34 + lane] = 0.0;
-      if (lane < 2) vrec[k * 34 + 32 + lane] = 0.0;
+      vrec[k * VW + lane] = 0.0;
+      if (lane < VW - 32) vrec[k * VW + 32 + lane] = 0.0;
     }
   }
 }
@@ -335,7 +351,8 @@ __global__ void soa_pack_kernel(const double* __restrict__ x, double* __restrict
     const int k = o / 32, col = 31 * w - 1 + o % 32;
     if (R >= 1 && R <= ny - 1 && col >= 0 && col < nx) v = x[((long long)(R - 1) * nx + col) * N1 + k];
   } else {
-    const int k = (o - VOFF) / 34, j = (o - VOFF) % 34, line = 31 * w - 1 + j, r = R - 1;
+    constexpr int VW = SoaCfg<N1>::VW;
+    const int k = (o - VOFF) / VW, j = (o - VOFF) % VW, line = 31 * w - 1 + j, r = R - 1;
     if (j < 33 && r >= 0 && line >= 1 && line <= nx - 1) v = x[(nh + (long long)(line - 1) * ny + r) * N1 + k];
   }
   xs[t] = v;
@@ -356,7 +373,7 @@ __global__ void soa_unpack_kernel(const double* __restrict__ xs, double* __restr
   } else {
     const long long b = blk - nh;
     const int line = (int)(b / ny) + 1, r = (int)(b % ny), w = line / 31;
-    src = ((long long)(r + 1) * W + w) * ENT + VOFF + k * 34 + (line - 31 * w + 1);
+    src = ((long long)(r + 1) * W + w) * ENT + VOFF + k * SoaCfg<N1>::VW + (line - 31 * w + 1);
   }
   x[u] = xs[src];
 }
