@@ -349,7 +349,7 @@ def run_ours(args, rank, ws):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"configs[1]: {N_MESH}x{N_MESH} quad mesh, p={P_ORDER}, K=I (shared block), "
                                    f"fp64, {APPLIES} applies/step, x~U[-1,1] seed 1",
-                       "ndof": ndof, "l2": "rotating 4 (x,y) pairs = %.0f MB > 126 MB L2" % (NB * 16 * ndof / 1e6),
+                       "ndof": ndof, "l2": "rotating %d (x,y) pairs = %.0f MB > 126 MB L2" % (NB, NB * 16 * xs[0].numel() / 1e6),
                        "parallelism": f"strips{ws} (1024 element rows per GPU, NCCL halo rows)" if ws > 1
                        else "single"},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ndof, "d2h_bytes_per_step": 8 * ndof,
