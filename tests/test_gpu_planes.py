@@ -99,6 +99,20 @@ def test_planes_config2_full_size(P):
     assert abs(lhs - rhs_) <= 1e-11 * max(1.0, abs(lhs))
 
 
+@pytest.mark.parametrize("shape", [(1, 1), (1, 5), (5, 1), (2, 2), (1, 40), (40, 1)])
+def test_planes_degenerate_meshes(P, shape):
+    """Empty and one-element-wide meshes (trace.py:90-91: ndof may be 0)."""
+    nx, ny = shape
+    s = P.tr.TraceSystem(P.mesh(nx, ny), 3, specs.constant(P.pb.ProblemSpec))
+    x = np.random.default_rng(nx * 7 + ny).uniform(-1, 1, s.ndof)
+    z = s.facet_planes(x)
+    y = s.matvec_free(z).numpy()
+    assert y.shape == (s.ndof,)
+    if s.ndof:
+        assert rel(y, oracle_for(s, nx, ny, 3).matvec(x)) < TOL
+    np.testing.assert_array_equal(z.numpy(), x)
+
+
 def test_planes_refuses_stored_levels(P):
     s = P.tr.TraceSystem(P.mesh(8, 8), 2, specs.manufactured(P.pb.ProblemSpec))
     assert not s.operator.shared
