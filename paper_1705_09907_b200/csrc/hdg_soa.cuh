@@ -35,6 +35,9 @@
 #ifndef HDG_SOA_EXP
 #define HDG_SOA_EXP 0          // experiment flags (tools/build_variants.sh), 0 in the product
 #endif
+#ifndef HDG_SOA_ALT
+#define HDG_SOA_ALT 0          // experiment: alternate the walk direction of neighbouring segments
+#endif
 #ifndef HDG_SOA_STCS
 #define HDG_SOA_STCS 0         // experiment: streaming (evict-first) stores of y
 #endif
@@ -232,6 +235,9 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
   const int r1 = min(r0 + a.J, a.ny);
   const int rs = r0 > 0 ? r0 - 1 : 0;                  // ghost row feeds the first owned line
   const int nrows = r1 - rs;                           // element rows walked; records rs .. r1
+  // odd segments walk down: both rows a segment shares with a neighbour (its ghost row and the
+  // neighbour's ghost) are then read by the two warps at the same time (L2 hits, not DRAM)
+  const bool down = HDG_SOA_ALT && (seg & 1);
   const double* __restrict__ X = a.x;
   double* __restrict__ Y = a.y;
   const long long W = a.W;
@@ -250,31 +256,39 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
     if (t > nrows || lane != 0) return;
     uint64_t* bar = bars + (t % RING);
     mbar_arrive_expect_tx(bar, ENT * 8u);
-    tma_load_1d(ring + (t % RING) * ENT, X + rec(rs + t, w), ENT * 8u, bar);
+    tma_load_1d(ring + (t % RING) * ENT, X + rec(down ? r1 - t : rs + t, w), ENT * 8u, bar);
   };
 #pragma unroll
   for (int t = 0; t < D; ++t) issue(t);
 
   const bool hcol = c >= 0 && c < a.nx;
   const bool vline = c + 1 >= 1 && c + 1 <= a.nx - 1;
-  double tp[N1], xB[N1];
+  // tp: the facet-sum partner carried between rows (walking up: T of the row below; down: B of
+  // the row above); xC: the shared H line carried (up: next bottom; down: next top)
+  double tp[N1], xC[N1];
 #pragma unroll
   for (int k = 0; k < N1; ++k) tp[k] = 0.0;
 
 #pragma unroll 1
   for (int t = 0; t < nrows; ++t) {
-    const int r = rs + t;
+    const int r = down ? r1 - 1 - t : rs + t;
     fence_proxy_async();                               // generic reads of entry t-1 before its async refill
     issue(t + D);                                      // entry t+D (slot of entry t-1: read last iteration)
     if (t == 0) mbar_wait(bars, 0);
     mbar_wait(bars + (t + 1) % RING, ((t + 1) / RING) & 1);
-    const double* e0 = ring + (t % RING) * ENT + lane;
-    const double* e1 = ring + ((t + 1) % RING) * ENT + lane;
-    double xT[N1], xR[N1], xL[N1];
+    // lower entry = record r (H line r), upper entry = record r + 1 (H line r+1, V of row r)
+    const double* e0 = ring + ((down ? t + 1 : t) % RING) * ENT + lane;
+    const double* e1 = ring + ((down ? t : t + 1) % RING) * ENT + lane;
+    double xB[N1], xT[N1], xR[N1], xL[N1];
 #pragma unroll
     for (int k = 0; k < N1; ++k) {
-      if (t == 0) xB[k] = e0[k * 32];
-      xT[k] = e1[k * 32];
+      if (down) {
+        xT[k] = t == 0 ? e1[k * 32] : xC[k];
+        xB[k] = e0[k * 32];
+      } else {
+        xB[k] = t == 0 ? e0[k * 32] : xC[k];
+        xT[k] = e1[k * 32];
+      }
       xL[k] = e1[VOFF + k * VW];
       xR[k] = e1[VOFF + k * VW + 1];
     }
@@ -291,20 +305,32 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
 #if HDG_SOA_EXP == 2   // experiment: no stores unless the result is NaN (compute + loads only)
     if (yB[0] != yB[0] || yR[N1 - 1] != yR[N1 - 1])
 #endif
+    // H line written this row: up: line r = T(r-1) + B(r) (rows >= r0); down: line r+1 =
+    // T(r) + B(r+1) (from the second row on; the ghost row r0 - 1 comes last and closes line r0)
+    const int hl = down ? r + 1 : r;
+    const bool hwr = down ? t >= 1 : r >= r0;
+    if (hwr) {
+      const bool hint = hcol && hl >= 1;
+      double* hrec = Y + rec(hl, w);
+#pragma unroll
+      for (int k = 0; k < N1; ++k) {
+        const double hv = hint ? (down ? yT[k] + tp[k] : tp[k] + yB[k]) : 0.0;
+#if HDG_SOA_STCS
+        __stcs(hrec + k * 32 + lane, hv);
+#else
+        hrec[k * 32 + lane] = hv;                      // lane 0 duplicates the left tile's slot 31
+#endif
+      }
+    }
     if (r >= r0) {
-      const bool hint = hcol && r >= 1;
-      double* hrec = Y + rec(r, w);                    // H line r
       double* vrec = Y + rec(r + 1, w) + VOFF;         // V of element row r
 #pragma unroll
       for (int k = 0; k < N1; ++k) {
         const double fromR = __shfl_down_sync(0xffffffffu, yL[k], 1);
-        const double hv = hint ? tp[k] + yB[k] : 0.0;
         const double vv = (vline && lane != 31) ? yR[k] + fromR : 0.0;
 #if HDG_SOA_STCS
-        __stcs(hrec + k * 32 + lane, hv);
         __stcs(vrec + k * VW + lane + 1 + (lane == 31), vv);
 #else
-        hrec[k * 32 + lane] = hv;                      // lane 0 duplicates the left tile's slot 31
         vrec[k * VW + lane + 1 + (lane == 31)] = vv;   // slots 1..31; lane 31 zeroes pad slot 33
 #endif
         if (VW > 34 && lane == 31)
@@ -317,8 +343,16 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
       }
     }
 #pragma unroll
-    for (int k = 0; k < N1; ++k) { tp[k] = yT[k]; xB[k] = xT[k]; }
+    for (int k = 0; k < N1; ++k) {
+      tp[k] = down ? yB[k] : yT[k];
+      xC[k] = down ? xB[k] : xT[k];
+    }
     __syncwarp();                                      // entry t is free for issue(t + RING)
+  }
+  if (down && r0 == 0) {                               // bottom boundary line (down walk)
+    double* hrec = Y + rec(0, w);
+#pragma unroll
+    for (int k = 0; k < N1; ++k) hrec[k * 32 + lane] = 0.0;
   }
   if (r1 == a.ny) {                                    // top boundary line
     double* hrec = Y + rec(a.ny, w);
