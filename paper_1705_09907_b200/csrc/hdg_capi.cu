@@ -67,6 +67,7 @@ struct hdg_level {
   int *g_ptr = nullptr, *g_col = nullptr, *gt_ptr = nullptr, *gt_col = nullptr;
   double *g_val = nullptr, *gt_val = nullptr;
   double lam_max = 1.0, cheb_frac = 0.15, fsai_omega = 1.0;
+  unsigned smoother_gen = 0;     // bumped by every smoother setter: cycle graphs captured before are stale
   double* tail_wd = nullptr;   // fused coarse tail, shared mode: device copy of Wh, Wv, Dh, Dv (n1 = 2)
   // facet-plane (SoA) device layout, shared mode (hdg_soa.cuh): element block + adapted blocks
   std::vector<double> blk;     // the 4n1 x 4n1 element block (shared mode)
@@ -101,6 +102,7 @@ struct hdg_mg {
   int tail_k0 = -1;              // first level of the fused coarse tail (-1: none)
   bool tail_enabled = true;
   bool fuse_first = true;        // first two Jacobi steps from x = 0 in one kernel (shared levels)
+  std::vector<unsigned> gens;    // levels' smoother_gen when the cached graphs were captured
 };
 
 // ------------------------------------------------------------------------------ helpers
@@ -441,6 +443,16 @@ int hdg_level_destroy(hdg_level* L) {
 int64_t hdg_level_ndof(const hdg_level* L) { return L ? L->ndof : -1; }
 int64_t hdg_level_operator_bytes(const hdg_level* L) { return L ? L->op_bytes : -1; }
 
+}  // extern "C"
+
+// a new smoother invalidates the fused-tail copy of D and every cycle graph captured with the old one
+static void smoother_changed(hdg_level* L) {
+  ++L->smoother_gen;
+  if (L->tail_wd) { cudaFree(L->tail_wd); L->tail_wd = nullptr; }
+}
+
+extern "C" {
+
 int hdg_level_set_blockjacobi(hdg_level* L, double omega) {
   if (!L) return fail(HDG_EINVAL, "null level");
   L->omega = omega;
@@ -478,6 +490,7 @@ int hdg_level_set_blockjacobi(hdg_level* L, double omega) {
   L->has_bj = true;
   L->use_fsai = false;
   L->bj_cheb = false;
+  smoother_changed(L);
   return 0;
 }
 
@@ -573,6 +586,7 @@ int hdg_level_set_bj_chebyshev(hdg_level* L, double lo, double hi) {
   if (!L->has_bj) return fail(HDG_ESTATE, "set block-Jacobi first");
   if (!(hi > lo && lo > 0.0)) return fail(HDG_EINVAL, "need 0 < lo < hi");
   L->bj_cheb = true; L->bj_lo = lo; L->bj_hi = hi;
+  smoother_changed(L);
   return 0;
 }
 
@@ -648,6 +662,7 @@ int hdg_level_set_fsai(hdg_level* L, int64_t n, const int32_t* g_ptr, const int3
   L->lam_max = lam_max; L->cheb_frac = cheb_fraction; L->fsai_omega = omega;
   L->has_fsai = true;
   L->use_fsai = true;
+  smoother_changed(L);
   return 0;
 }
 
@@ -1135,6 +1150,15 @@ static int cycle_issue(hdg_mg* mg, const double* b, const double* x0, double* x,
 int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int nu1, int nu2, int visits,
                  int use_graph, void* stream) {
   if (!mg || !b || !x) return fail(HDG_EINVAL, "null argument");
+  {
+    std::vector<unsigned> gens(mg->n);
+    for (int k = 0; k < mg->n; ++k) gens[k] = mg->L[k]->smoother_gen;
+    if (gens != mg->gens) {                          // smoothers re-attached since the last capture
+      for (auto& kv : mg->graphs) cudaGraphExecDestroy(kv.second.exec);
+      mg->graphs.clear();
+      mg->gens = gens;
+    }
+  }
   if (nu1 < 0 || nu2 < 0 || visits < 1) return fail(HDG_EINVAL, "bad cycle parameters");
   if (mg->L[0]->ndof == 0) return 0;
   cudaStream_t s = S(stream);

@@ -339,9 +339,13 @@ def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother
                       matrix_free=True, rhs=fine.rhs)]
     op = fine.operator
 
+    # FSAI smoothers are built from each level's CSR (host element blocks), so their levels keep
+    # the blocks; block-Jacobi (or a smoother attached later) lets large levels drop them
+    keep_blocks = smoother is not None and smoother not in _BJ_MODES
+
     def retire(prev):
         # large device-condensed levels: keep only the native facet stream (memory)
-        if not isinstance(prev.S_cls, np.ndarray) and prev.ndof > RELEASE_NDOF:
+        if not keep_blocks and not isinstance(prev.S_cls, np.ndarray) and prev.ndof > RELEASE_NDOF:
             prev.release_blocks()
 
     for q in range(p - 1, 0, -1):                                   # multigrid.py:317-321
@@ -390,6 +394,9 @@ def _rhs(level):
     return level.rhs.resolve() if isinstance(level.rhs, _LazyRhs) else level.rhs
 
 
+_BJ_MODES = ("blockjacobi", "bj", "bj-chebyshev", "chebyshev")
+
+
 def attach_smoothers(levels, mode, omega=None):
     """multigrid.py:345-352 on every level but the coarsest.  mode: "baseline" (FSAI on the
     pattern of A), "aggressive" (pattern of A^2), an int power, or "blockjacobi".  omega
@@ -407,6 +414,10 @@ def attach_smoothers(levels, mode, omega=None):
     if not isinstance(power, int) or isinstance(power, bool) or power < 1:
         raise ValueError(f"unknown smoother mode {mode!r}")
     w = 1.0 if omega is None else float(omega)
+    for lev in levels[:-1]:
+        if getattr(lev.block_op, "S_cls", True) is None:
+            raise HierarchyError("FSAI needs the level's element blocks, released after building a large "
+                                 "device-condensed hierarchy: pass smoother=%r to build_hierarchy" % (mode,))
     for lev in levels[:-1]:
         lev.smoother = fsai_build(lev.operator.tocsr(), power, w).bind(lev.block_op)
     return levels

@@ -569,3 +569,51 @@ def test_half_stored_stream_mesh_widths(P, nx, ny, p):
             sl = slice(blk * n1, (blk + 1) * n1)
             ref[sl] = x[sl] + 0.8 * np.linalg.solve(Ad[sl, sl], r[sl])
         assert rel(got, ref) < 1e-11
+
+
+def test_fsai_on_large_condensed_hierarchy_keeps_blocks(P, monkeypatch):
+    """Large device-condensed levels drop their element blocks after the hierarchy is built;
+    FSAI smoothers need them (fsai_build reads the level CSR, multigrid.py:123-159): asking for
+    FSAI in build_hierarchy keeps them and matches the oracle, attaching it afterwards to a
+    hierarchy whose blocks were released raises HierarchyError."""
+    monkeypatch.setattr(P.tr.TraceSystem, "GPU_CLASSES", 0)
+    monkeypatch.setattr(P.mg, "RELEASE_NDOF", 0)
+    n, p = 16, 2
+    Kg = specs.hetero_K(n, seed=2)
+    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+    bare = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother=None)
+    assert bare[0].block_op.S_cls is None
+    with pytest.raises(P.mg.HierarchyError):
+        P.mg.attach_smoothers(bare, "baseline")
+    P.mg.attach_smoothers(bare, "blockjacobi")            # block-Jacobi only needs the facet stream
+    levels = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother="baseline")
+    assert levels[0].block_op.S_cls is not None
+    lo = O.build_levels(O.Grid(n, n), p, O.Spec(O.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0),
+                        smoother="baseline")
+    b = np.random.default_rng(9).uniform(-1, 1, levels[0].ndof)
+    x, it = levels[0].system.solve_cg(tol=1e-10, precond=P.mg.mg_preconditioner(levels), b=b)
+    xo, ito = lo[0].system.solve_cg(b=b, tol=1e-10, precond=O.mg_preconditioner(lo))
+    assert it == ito
+    assert rel(x, xo) < 1e-9
+
+
+def test_reattached_smoother_recaptures_cycle_graphs(P):
+    """Cycle graphs are cached per (b, x0, x, nu1, nu2, visits); attaching another smoother to
+    the same levels (attach_smoothers, multigrid.py:345-352) must not replay the old one."""
+    n, p = 16, 2
+    Kg = specs.hetero_K(n, seed=4)
+    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+    b = np.random.default_rng(3).uniform(-1, 1, 2 * n * (n - 1) * (p + 1))
+    levels = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother="blockjacobi")
+    import torch
+    bd = torch.from_numpy(b).cuda()   # same device b every call: the cached graphs are hit
+    x_bj = P.mg.v_cycle(levels, bd).cpu().numpy()
+    for mode in ("bj-chebyshev", "baseline", "blockjacobi"):
+        P.mg.attach_smoothers(levels, mode)
+        x = P.mg.v_cycle(levels, bd).cpu().numpy()
+        fresh = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother=mode)
+        xf = P.mg.v_cycle(fresh, bd).cpu().numpy()
+        assert rel(x, xf) < 1e-13, mode
+        if mode != "blockjacobi":
+            assert rel(x, x_bj) > 1e-6, mode
+    assert rel(x, x_bj) < 1e-13

@@ -1,6 +1,7 @@
 """MG-PCG preconditioner variants on configs[2]'s coefficient generator (log-U[1e-2,1e2] per
 element, seed 2) at a reduced mesh: iterations to 1e-10 and device time per variant.
-    python tools/pcg_variants.py 512 8
+    PCG_VARIANTS="V(2,2);W(2,2);V(4,4)" python tools/pcg_variants.py 512 8
+W(2,2) visits level k 2^k times: with 18 levels its latency-bound coarse tail dominates.
 """
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -20,15 +21,17 @@ maxit = int(sys.argv[3]) if len(sys.argv) > 3 else 1500
 rng = np.random.default_rng(2)
 Kg = np.exp(rng.uniform(np.log(1e-2), np.log(1e2), (n, n)))
 spec = ProblemSpec(piecewise_coefficient(Kg), zero, zero, 1.0)
-levels = build_hierarchy(build_cartesian(n, n), p, spec, smoother=None)
+levels = build_hierarchy(build_cartesian(n, n), p, spec, smoother="baseline")   # keeps the blocks for FSAI
 b = torch.from_numpy(rng.uniform(-1.0, 1.0, levels[0].ndof)).cuda()
 bn = float(b.norm())
-for smoother in ("blockjacobi", "baseline"):
+for smoother in ("blockjacobi", "bj-chebyshev", "baseline"):
     t0 = time.time()
     attach_smoothers(levels, smoother)
     torch.cuda.synchronize()
     ts = time.time() - t0
-    for name, cyc, nu in (("V(2,2)", v_cycle, 2), ("W(2,2)", w_cycle, 2), ("V(4,4)", v_cycle, 4)):
+    variants = [v for v in (("V(2,2)", v_cycle, 2), ("W(2,2)", w_cycle, 2), ("V(4,4)", v_cycle, 4))
+                if v[0] in os.environ.get("PCG_VARIANTS", "V(2,2);V(4,4)").split(";")]
+    for name, cyc, nu in variants:
         M = lambda r, cyc=cyc, nu=nu: cyc(levels, r, None, nu, nu)
         M(b); torch.cuda.synchronize()
         t1 = time.time()
