@@ -162,13 +162,35 @@ def cpu_matvec_threads(osys, x, threads):
     return osys._sum_owners(ye)
 
 
+# both CPU legs (the reference arm and the GPU arm's cpu_baseline) run the oracle port of
+# trace.py:87-94 with the same thread policy: every host thread, element rows split evenly
+def cpu_threads():
+    return os.cpu_count() or 1
+
+
+CPU_APPLIES_PER_STEP = 2   # the reference arm's bounded step: 2 full applies (~1 s of host work)
+
+
+def workload_config(ws):
+    """The config dict both arms print (identical, so the driver can pair the lines)."""
+    return {"workload": f"configs[1]: {N_MESH}x{N_MESH} quad mesh, p={P_ORDER}, K=I (shared block), "
+                        f"fp64, x~U[-1,1] seed 1; GPU step = {APPLIES} applies",
+            "ndof": 2 * N_MESH * (N_MESH - 1) * (P_ORDER + 1),
+            "l2": "inputs larger than L2: 4 rotating (x, y) pairs (736 MB > 126 MB L2)",
+            "parallelism": f"strips{ws} (1024 element rows per GPU, NCCL halo rows)" if ws > 1 else "single"}
+
+
 def run_reference(args, rank, ws):
+    """--impl reference: the reference algorithm's CPU implementation (the oracle port of
+    trace.py:87-94; the reference is pure Python and cannot travel to the GPU box) on all host
+    threads.  One step = CPU_APPLIES_PER_STEP full applies of the configs[1] system, and
+    ms_per_step is exactly the time of such a step; value is the same GDOF/s rate metric."""
     if rank != 0:
         return
     osys = oracle_system()
     x = np.random.default_rng(1).uniform(-1.0, 1.0, osys.ndof)
-    threads = os.cpu_count() or 1
-    sample = 2  # applies per step (bounded sample of the 100-apply step)
+    threads = cpu_threads()
+    sample = CPU_APPLIES_PER_STEP
     for _ in range(args.warmup):
         cpu_matvec_threads(osys, x, threads)
     t0 = time.perf_counter()
@@ -178,14 +200,13 @@ def run_reference(args, rank, ws):
     dt = time.perf_counter() - t0
     val = osys.ndof * sample * args.steps / dt / 1e9
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3 * APPLIES / sample,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "applies_per_step": sample,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"configs[1]: {N_MESH}x{N_MESH} quad mesh, p={P_ORDER}, K=I, fp64, "
-                                   f"{APPLIES} applies/step", "ndof": osys.ndof},
+            "data": "synthetic", "impl": "reference", "config": workload_config(ws),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": f"{sample} applies of the full {N_MESH}^2 p={P_ORDER} system per step "
-                                       f"(oracle port of trace.py:87-94, {threads} threads)"},
+                                       f"(oracle port of trace.py:87-94, {threads} threads, element rows "
+                                       "split evenly; the timed step is exactly these applies)"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -347,11 +368,7 @@ def run_ours(args, rank, ws):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"configs[1]: {N_MESH}x{N_MESH} quad mesh, p={P_ORDER}, K=I (shared block), "
-                                   f"fp64, {APPLIES} applies/step, x~U[-1,1] seed 1",
-                       "ndof": ndof, "l2": "rotating %d (x,y) pairs = %.0f MB > 126 MB L2" % (NB, NB * 16 * xs[0].numel() / 1e6),
-                       "parallelism": f"strips{ws} (1024 element rows per GPU, NCCL halo rows)" if ws > 1
-                       else "single"},
+            "applies_per_step": APPLIES, "config": workload_config(ws),
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8 * ndof, "d2h_bytes_per_step": 8 * ndof,
                     "path": ("per step: pinned H2D of x, TraceSystem.facet_planes (pack), matvec_free x100 on the "
                              "facet records, .tensor() (unpack), D2H of y" if records else
@@ -449,16 +466,21 @@ def strip_vcycle_timing(rank, ws, steps=10):
 
 def cpu_baseline(y_gpu, x_host):
     osys = oracle_system()
-    cpu_matvec_threads(osys, x_host, 1)   # warm-up + parity reference for the timed output
+    threads = cpu_threads()
+    cpu_matvec_threads(osys, x_host, threads)   # warm-up + parity reference for the timed output
     t0 = time.perf_counter()
     sample = 5
     for _ in range(sample):
-        y = cpu_matvec_threads(osys, x_host, 1)
+        y = cpu_matvec_threads(osys, x_host, threads)
     dt = time.perf_counter() - t0
     err = float(np.abs(y - y_gpu).max() / np.abs(y).max())
-    return {"value": osys.ndof * sample / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
+    t1 = time.perf_counter()
+    cpu_matvec_threads(osys, x_host, 1)
+    one = osys.ndof / (time.perf_counter() - t1) / 1e9
+    return {"value": osys.ndof * sample / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{sample} applies of the full {N_MESH}^2 p={P_ORDER} system (oracle port of "
-                      f"trace.py:87-94, single-threaded numpy like the reference)",
+                      f"trace.py:87-94, {threads} threads, element rows split evenly: the reference arm's policy)",
+            "single_core_value": one,
             "parity_rel_err_vs_gpu": err}
 
 

@@ -166,6 +166,26 @@ int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int n
                  int visits, int use_graph, void* stream);
 /* coarse solve on the last level alone: x = A_c^-1 b (multigrid.py:209-212) */
 int hdg_coarse_solve(hdg_mg* mg, const double* b, double* x, void* stream);
+/* CUDA graphs instantiated by hdg_mg_cycle so far (LRU cache of 8 per hierarchy; a smoother
+ * change drops them all) */
+int64_t hdg_mg_graph_captures(const hdg_mg* mg);
+
+/* ---------------------------------------------------------------- solve loops
+ * Replaces solve_mg (multigrid.py:421-439): cycles x <- cycle(b, x) until
+ * ||b - A x|| <= tol ||b|| (checked before each cycle), at most max_cycles, stopping early when
+ * the last 5 ratios are >= 1 (ConvergenceMonitor.diverged, multigrid.py:388-390).  x holds x0 on
+ * entry and the iterate on return; res_hist (HOST, max_cycles + 1 doubles) receives
+ * ||b - A x_k|| for k = 0..*ncycles.  One scalar D2H per cycle. */
+int hdg_solve_mg(hdg_mg* mg, const double* b, double* x, int nu1, int nu2, int visits, double tol,
+                 int max_cycles, double* res_hist, int* ncycles, void* stream);
+/* Replaces TraceSystem.solve_cg (trace.py:142-163) with mg_preconditioner (multigrid.py:457-463):
+ * conjugate gradients on `lev`, preconditioned by one V(nu1, nu2) cycle of `mg` from zero (mg may
+ * be NULL: plain CG).  x0 = x if use_x0 else 0.  Stops when ||r|| <= tol ||b|| (checked at the top
+ * of each iteration, as the reference) or after maxiter iterations; *iters = the reference's
+ * returned count.  res_hist (HOST, maxiter + 1 doubles, may be NULL) receives ||r_k||.  The
+ * iteration body is one CUDA graph; one scalar D2H per iteration. */
+int hdg_pcg(const hdg_level* lev, hdg_mg* mg, const double* b, double* x, int use_x0, double tol, int maxiter,
+            int nu1, int nu2, double* res_hist, int* iters, void* stream);
 
 /* ---------------------------------------------------------------- reductions */
 /* *out = sum_i a_i b_i (deterministic two-pass; device scalar out) */

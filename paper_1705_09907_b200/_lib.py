@@ -60,6 +60,11 @@ SIGNATURES = [
     ("hdg_mg_cycle", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
                              c_void_p]),
     ("hdg_coarse_solve", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("hdg_mg_graph_captures", c_int64, [c_void_p]),
+    ("hdg_solve_mg", c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, ctypes.c_double, c_int,
+                             c_double_p, ctypes.POINTER(c_int), c_void_p]),
+    ("hdg_pcg", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, ctypes.c_double, c_int, c_int, c_int,
+                        c_double_p, ctypes.POINTER(c_int), c_void_p]),
     ("hdg_dot", c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     ("hdg_cg_update", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, ctypes.c_double, c_int64, c_void_p]),
     ("hdg_xpby", c_int, [c_void_p, ctypes.c_double, c_void_p, c_int64, c_void_p]),

@@ -88,7 +88,11 @@ struct hdg_transfer {
 struct GraphEntry {
   cudaGraphExec_t exec;
   long long nkern;
+  unsigned long long last_use;
 };
+// cycle graphs are keyed by buffer pointers: callers whose addresses vary would otherwise grow the
+// cache without bound, so the least recently replayed graph is dropped beyond this many
+static const size_t MAX_CYCLE_GRAPHS = 8;
 
 struct hdg_mg {
   std::vector<hdg_level*> L;
@@ -103,6 +107,8 @@ struct hdg_mg {
   bool tail_enabled = true;
   bool fuse_first = true;        // first two Jacobi steps from x = 0 in one kernel (shared levels)
   std::vector<unsigned> gens;    // levels' smoother_gen when the cached graphs were captured
+  unsigned long long use_clock = 0;
+  long long graph_captures = 0;  // graphs instantiated so far (tests: re-capture after a smoother change)
 };
 
 // ------------------------------------------------------------------------------ helpers
@@ -654,6 +660,11 @@ int hdg_level_set_fsai(hdg_level* L, int64_t n, const int32_t* g_ptr, const int3
                        double lam_max, double cheb_fraction, double omega) {
   if (!L) return fail(HDG_EINVAL, "null level");
   if (n != L->ndof) return fail(HDG_EINVAL, "FSAI factor size != level ndof");
+  // invalidate first: a failed upload must leave a level the cycle refuses, never stale graphs
+  // replaying freed factor arrays
+  L->has_fsai = false;
+  L->use_fsai = false;
+  smoother_changed(L);
   int rc;
   if ((rc = upload(&L->g_ptr, g_ptr, n + 1)) || (rc = upload(&L->g_col, g_col, nnz)) ||
       (rc = upload(&L->g_val, g_val, nnz)) || (rc = upload(&L->gt_ptr, gt_ptr, n + 1)) ||
@@ -806,28 +817,39 @@ int hdg_restrict(const hdg_transfer* t, const double* rf, double* rc, void* stre
 
 // ---------------------------------------------------------------------------- reductions
 
-static double* g_dot_partials = nullptr;
-static const int DOT_BLOCKS = 4 * 148;
+// streaming grid of the vector kernels: 4 CTAs of 256 threads per SM of this device
+static int vec_blocks() { return 4 * sm_count(); }
 
-int hdg_dot(const double* a, const double* b, int64_t n, double* out, void* stream) {
-  if (!g_dot_partials) CK(cudaMalloc(&g_dot_partials, sizeof(double) * DOT_BLOCKS));
-  dot_partials_kernel<<<DOT_BLOCKS, 256, 0, S(stream)>>>(a, b, n, g_dot_partials);
+// partials live in a stream-ordered allocation per call: concurrent streams / threads never share
+// a buffer, and the allocation is captured as a graph node when the call is captured
+static int dot_into(const double* a, const double* b, int64_t n, double* out, double* partials, cudaStream_t s) {
+  const int nb = vec_blocks();
+  dot_partials_kernel<<<nb, 256, 0, s>>>(a, b, n, partials);
   CKL();
-  sum_partials_kernel<<<1, 32, 0, S(stream)>>>(g_dot_partials, DOT_BLOCKS, out);
+  sum_partials_kernel<<<1, 32, 0, s>>>(partials, nb, out);
   CKL();
   return 0;
 }
 
+int hdg_dot(const double* a, const double* b, int64_t n, double* out, void* stream) {
+  if (!out || (n > 0 && (!a || !b))) return fail(HDG_EINVAL, "null argument");
+  double* partials = nullptr;
+  CK(cudaMallocAsync((void**)&partials, sizeof(double) * vec_blocks(), S(stream)));
+  const int rc = dot_into(a, b, n, out, partials, S(stream));
+  cudaFreeAsync(partials, S(stream));
+  return rc;
+}
+
 int hdg_cg_update(double* x, double* r, const double* d, const double* ad, double alpha, int64_t n, void* stream) {
   if (n <= 0) return 0;
-  cg_update_kernel<<<DOT_BLOCKS, 256, 0, S(stream)>>>(x, r, d, ad, alpha, n);
+  cg_update_kernel<<<vec_blocks(), 256, 0, S(stream)>>>(x, r, d, ad, alpha, n);
   CKL();
   return 0;
 }
 
 int hdg_xpby(const double* z, double beta, double* d, int64_t n, void* stream) {
   if (n <= 0) return 0;
-  xpby_kernel<<<DOT_BLOCKS, 256, 0, S(stream)>>>(z, beta, d, n);
+  xpby_kernel<<<vec_blocks(), 256, 0, S(stream)>>>(z, beta, d, n);
   CKL();
   return 0;
 }
@@ -1147,18 +1169,21 @@ static int cycle_issue(hdg_mg* mg, const double* b, const double* x0, double* x,
   return cycle_rec(mg, 0, b, zero, nu1, nu2, visits, s);
 }
 
+// smoothers re-attached since the last capture: every cached cycle graph is stale
+static void refresh_graphs(hdg_mg* mg) {
+  std::vector<unsigned> gens(mg->n);
+  for (int k = 0; k < mg->n; ++k) gens[k] = mg->L[k]->smoother_gen;
+  if (gens != mg->gens) {
+    for (auto& kv : mg->graphs) cudaGraphExecDestroy(kv.second.exec);
+    mg->graphs.clear();
+    mg->gens = gens;
+  }
+}
+
 int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int nu1, int nu2, int visits,
                  int use_graph, void* stream) {
   if (!mg || !b || !x) return fail(HDG_EINVAL, "null argument");
-  {
-    std::vector<unsigned> gens(mg->n);
-    for (int k = 0; k < mg->n; ++k) gens[k] = mg->L[k]->smoother_gen;
-    if (gens != mg->gens) {                          // smoothers re-attached since the last capture
-      for (auto& kv : mg->graphs) cudaGraphExecDestroy(kv.second.exec);
-      mg->graphs.clear();
-      mg->gens = gens;
-    }
-  }
+  refresh_graphs(mg);
   if (nu1 < 0 || nu2 < 0 || visits < 1) return fail(HDG_EINVAL, "bad cycle parameters");
   if (mg->L[0]->ndof == 0) return 0;
   cudaStream_t s = S(stream);
@@ -1181,11 +1206,164 @@ int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int n
     if (e != cudaSuccess) return fail(HDG_ECUDA, std::string("instantiate: ") + cudaGetErrorString(e));
     ge.nkern = g_launches.load() - c0;
     g_launches.fetch_sub(ge.nkern);
+    ++mg->graph_captures;
+    while (mg->graphs.size() >= MAX_CYCLE_GRAPHS) {          // LRU eviction
+      auto old = mg->graphs.begin();
+      for (auto g2 = mg->graphs.begin(); g2 != mg->graphs.end(); ++g2)
+        if (g2->second.last_use < old->second.last_use) old = g2;
+      cudaGraphExecDestroy(old->second.exec);
+      mg->graphs.erase(old);
+    }
     it = mg->graphs.emplace(key, ge).first;
   }
+  it->second.last_use = ++mg->use_clock;
   CK(cudaGraphLaunch(it->second.exec, s));
   g_launches.fetch_add(it->second.nkern);
   return 0;
+}
+
+int64_t hdg_mg_graph_captures(const hdg_mg* mg) { return mg ? mg->graph_captures : -1; }
+
+// ------------------------------------------------------------------ native solve loops
+// solve_mg (multigrid.py:421-439) and solve_cg (trace.py:142-163) with every vector on the
+// device: one scalar crosses to the host per cycle / iteration (the stop test), as in the
+// reference's own loop structure.
+
+static int fetch(const double* dsrc, double* h, int count, cudaStream_t s) {
+  CK(cudaMemcpyAsync(h, dsrc, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int hdg_solve_mg(hdg_mg* mg, const double* b, double* x, int nu1, int nu2, int visits, double tol,
+                 int max_cycles, double* res_hist, int* ncycles, void* stream) {
+  if (!mg || !b || !x || !res_hist || !ncycles) return fail(HDG_EINVAL, "null argument");
+  if (max_cycles < 0) return fail(HDG_EINVAL, "max_cycles must be >= 0");
+  cudaStream_t s = S(stream);
+  const hdg_level* L0 = mg->L[0];
+  const long long n = L0->ndof;
+  *ncycles = 0;
+  if (n == 0) { res_hist[0] = 0.0; return 0; }
+  double* scal = nullptr;
+  double* partials = nullptr;
+  CK(cudaMallocAsync((void**)&scal, sizeof(double) * 2, s));
+  CK(cudaMallocAsync((void**)&partials, sizeof(double) * vec_blocks(), s));
+  int rc = dot_into(b, b, n, scal, partials, s);
+  double h[2];
+  if (!rc) rc = hdg_residual(L0, b, x, nullptr, scal + 1, s);
+  if (!rc) rc = fetch(scal, h, 2, s);
+  const double bnorm = (rc || h[0] == 0.0) ? 1.0 : std::sqrt(h[0]);
+  if (!rc) res_hist[0] = std::sqrt(h[1]);
+  int k = 0;
+  while (!rc && k < max_cycles) {
+    if (res_hist[k] <= tol * bnorm) break;                     // multigrid.py:433
+    rc = hdg_mg_cycle(mg, b, x, x, nu1, nu2, visits, 1, stream);
+    if (!rc) rc = hdg_residual(L0, b, x, nullptr, scal + 1, s);
+    if (!rc) rc = fetch(scal + 1, h + 1, 1, s);
+    if (rc) break;
+    res_hist[++k] = std::sqrt(h[1]);
+    if (k >= 5) {                                               // monitor.diverged(): 5 rho >= 1
+      bool div = true;
+      for (int i = k - 5; i < k; ++i) {
+        const double rho = res_hist[i] > 0.0 ? res_hist[i + 1] / res_hist[i] : 0.0;
+        if (!(rho >= 1.0)) { div = false; break; }
+      }
+      if (div) break;
+    }
+  }
+  cudaFreeAsync(partials, s);
+  cudaFreeAsync(scal, s);
+  *ncycles = k;
+  return rc;
+}
+
+int hdg_pcg(const hdg_level* L, hdg_mg* mg, const double* b, double* x, int use_x0, double tol, int maxiter,
+            int nu1, int nu2, double* res_hist, int* iters, void* stream) {
+  if (!L || !b || !x || !iters) return fail(HDG_EINVAL, "null argument");
+  if (mg && mg->L[0]->ndof != L->ndof) return fail(HDG_EINVAL, "preconditioner size != operator size");
+  if (maxiter < 0) return fail(HDG_EINVAL, "maxiter must be >= 0");
+  cudaStream_t s = S(stream);
+  const long long n = L->ndof;
+  *iters = 0;
+  if (n == 0) { if (res_hist) res_hist[0] = 0.0; return 0; }
+  const int nb = vec_blocks();
+  const size_t vb = sizeof(double) * (size_t)n;
+  double *r = nullptr, *z = nullptr, *d = nullptr, *ad = nullptr, *scal = nullptr, *part = nullptr;
+  CK(cudaMallocAsync((void**)&r, vb, s));
+  CK(cudaMallocAsync((void**)&d, vb, s));
+  CK(cudaMallocAsync((void**)&ad, vb, s));
+  if (mg) CK(cudaMallocAsync((void**)&z, vb, s)); else z = r;
+  CK(cudaMallocAsync((void**)&scal, sizeof(double) * 8, s));
+  CK(cudaMallocAsync((void**)&part, sizeof(double) * 2 * nb, s));
+  cudaStream_t cs = nullptr;
+  cudaGraphExec_t body = nullptr;
+  int rc = 0;
+  auto precond = [&](cudaStream_t st) -> int {                   // z = M r (one V-cycle from zero)
+    return mg ? cycle_issue(mg, r, nullptr, z, nu1, nu2, 1, st) : 0;
+  };
+  do {
+    if (mg) { refresh_graphs(mg); if ((rc = tail_prepare(mg))) break; }
+    // r = b - A x0 (trace.py:147), z = M r, d = z, rz = r.z
+    if (use_x0) { if ((rc = hdg_residual(L, b, x, r, nullptr, s))) break; }
+    else {
+      if (cudaMemsetAsync(x, 0, vb, s) != cudaSuccess || cudaMemcpyAsync(r, b, vb, cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+        rc = fail(HDG_ECUDA, "pcg init copies"); break;
+      }
+    }
+    if ((rc = precond(s))) break;
+    if (cudaMemcpyAsync(d, z, vb, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { rc = fail(HDG_ECUDA, "pcg copy"); break; }
+    if ((rc = dot_into(r, z, n, scal + 0, part, s))) break;
+    if ((rc = dot_into(b, b, n, scal + 4, part, s))) break;
+    if ((rc = dot_into(r, r, n, scal + 3, part, s))) break;
+    // one iteration body (trace.py:153-162) captured once, replayed per iteration
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) { rc = fail(HDG_ECUDA, "stream"); break; }
+    const long long c0 = g_launches.load();
+    if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { rc = fail(HDG_ECUDA, "capture"); break; }
+    {
+      MvArgs a{};
+      a.x = d; a.out = ad;
+      rc = apply(L, EPI_Y, a, cs);                                            // ad = A d
+      if (!rc) rc = dot_into(d, ad, n, scal + 1, part, cs);                   // d.Ad
+      if (!rc) { cg_update_dev_kernel<<<nb, 256, 0, cs>>>(x, r, d, ad, scal, n); CKL(); }
+      if (!rc) rc = precond(cs);                                              // z = M r
+      if (!rc) { dot2_partials_kernel<<<nb, 256, 0, cs>>>(r, z, r, r, n, part); CKL(); }
+      if (!rc) { sum_partials_kernel<<<1, 32, 0, cs>>>(part, nb, scal + 2); CKL(); }       // r.z
+      if (!rc) { sum_partials_kernel<<<1, 32, 0, cs>>>(part + nb, nb, scal + 3); CKL(); }  // r.r
+      if (!rc) { xpby_dev_kernel<<<nb, 256, 0, cs>>>(z, scal, d, n); CKL(); }              // d = z + beta d
+      if (!rc && cudaMemcpyAsync(scal, scal + 2, sizeof(double), cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
+        rc = fail(HDG_ECUDA, "pcg scalar copy");
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(cs, &g);
+    const long long nk = g_launches.load() - c0;
+    g_launches.fetch_sub(nk);
+    if (rc) { if (g) cudaGraphDestroy(g); break; }
+    if (ec != cudaSuccess) { rc = fail(HDG_ECUDA, std::string("pcg capture: ") + cudaGetErrorString(ec)); break; }
+    const cudaError_t ei = cudaGraphInstantiate(&body, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) { rc = fail(HDG_ECUDA, std::string("pcg instantiate: ") + cudaGetErrorString(ei)); break; }
+    double h[2];
+    if ((rc = fetch(scal + 3, h, 2, s))) break;                   // r.r, b.b
+    const double bnorm = h[1] > 0.0 ? std::sqrt(h[1]) : 1.0;
+    double rr = h[0];
+    int it = 0;
+    for (; it < maxiter; ++it) {
+      const double rn = std::sqrt(rr);
+      if (res_hist) res_hist[it] = rn;
+      if (rn <= tol * bnorm) break;                                // trace.py:152
+      if (cudaGraphLaunch(body, s) != cudaSuccess) { rc = fail(HDG_ECUDA, "pcg graph launch"); break; }
+      g_launches.fetch_add(nk);
+      if ((rc = fetch(scal + 3, &rr, 1, s))) break;
+    }
+    if (!rc && it == maxiter && res_hist) res_hist[maxiter] = std::sqrt(rr);
+    *iters = it;
+  } while (false);
+  if (body) cudaGraphExecDestroy(body);
+  if (cs) cudaStreamDestroy(cs);
+  cudaFreeAsync(part, s); cudaFreeAsync(scal, s);
+  cudaFreeAsync(ad, s); cudaFreeAsync(d, s); cudaFreeAsync(r, s);
+  if (mg) cudaFreeAsync(z, s);
+  return rc;
 }
 
 }  // extern "C"

@@ -219,16 +219,26 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned by
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-// bounded wait: a lost arrival must surface as an error (trap), never as a hung GPU
+// bounded wait: a lost arrival must surface as an error (trap), never as a hung GPU.  The limit is
+// wall-clock (%globaltimer, 20 s), so profiler replay, sanitizers or heavy contention cannot trip it.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, unsigned parity) {
+  unsigned done;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  unsigned done = 0;
-  for (int spin = 0; spin < (1 << 20); ++spin) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-    if (done) return;
-  }
-  __trap();
+  if (mbar_try(bar, parity)) return;
+  const unsigned long long t0 = global_ns();
+#pragma unroll 1
+  while (!mbar_try(bar, parity))
+    if (global_ns() - t0 > 20000000000ull) __trap();
 }
 __device__ __forceinline__ void fence_proxy_async() {
 #ifndef HDG_EXP_NOFENCE
@@ -1519,6 +1529,50 @@ __global__ void cg_update_kernel(double* __restrict__ x, double* __restrict__ r,
     x[t] = fma(alpha, d[t], x[t]);
     r[t] = fma(-alpha, ad[t], r[t]);
   }
+}
+
+// two dot products in one pass (same per-thread order as dot_partials_kernel, so each result is
+// bitwise the one a separate hdg_dot would give): partials[blk] = a.b, partials[grid + blk] = c.e
+__global__ void dot2_partials_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                     const double* __restrict__ c, const double* __restrict__ e, long long n,
+                                     double* __restrict__ partials) {
+  double s = 0.0, u = 0.0;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    s = fma(__ldg(a + t), __ldg(b + t), s);
+    u = fma(__ldg(c + t), __ldg(e + t), u);
+  }
+  __shared__ double red[2][32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    u += __shfl_xor_sync(0xffffffffu, u, o);
+  }
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = s; red[1][threadIdx.x >> 5] = u; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t0 += red[0][w]; t1 += red[1][w]; }
+    partials[blockIdx.x] = t0;
+    partials[gridDim.x + blockIdx.x] = t1;
+  }
+}
+
+// CG updates with the step lengths read from device scalars (no host round trip):
+// sc[0] = r.z, sc[1] = d.Ad, sc[2] = r_new.z_new  (trace.py:156-161)
+__global__ void cg_update_dev_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ d,
+                                     const double* __restrict__ ad, const double* __restrict__ sc, long long n) {
+  const double alpha = sc[0] / sc[1];
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+    x[t] = fma(alpha, d[t], x[t]);
+    r[t] = fma(-alpha, ad[t], r[t]);
+  }
+}
+
+__global__ void xpby_dev_kernel(const double* __restrict__ z, const double* __restrict__ sc, double* __restrict__ d,
+                                long long n) {
+  const double beta = sc[2] / sc[0];
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
+    d[t] = fma(beta, d[t], z[t]);
 }
 
 __global__ void xpby_kernel(const double* __restrict__ z, double beta, double* __restrict__ d, long long n) {

@@ -47,6 +47,11 @@
 #ifndef HDG_SOA_RING
 #define HDG_SOA_RING 3
 #endif
+#ifndef HDG_SOA_MCONST
+#define HDG_SOA_MCONST -1      // blocks from the constant bank (1) or shared memory (0); -1: by order
+                               // (constant bank for p <= 4: 36.7 vs 37.3 us at 1024^2; at p = 8
+                               // the 326 entries overflow the uniform registers: 264 vs 220 us)
+#endif
 #ifndef HDG_SOA_MINB_HI
 #define HDG_SOA_MINB_HI 3      // CTAs per SM for p >= 3 (154 registers at p = 4 without a cap)
 #endif
@@ -191,6 +196,33 @@ __device__ __forceinline__ void soa_blocks(const double* __restrict__ Ms, const 
   soa_block<C::A3, M::O3, C::A0 + C::A1 + C::A2>(Ms, t, z);
 }
 
+// The same product with the blocks read from the kernel-parameter (constant) bank: every lane
+// uses the same entry at the same time, so DFMA takes it as a uniform c[][] operand and the
+// shared-memory pipe carries only the ring.
+template <int SZ, int MOFF, int TOFF>
+__device__ __forceinline__ void soa_block_c(const double* M, const double* t, double* z) {
+#pragma unroll
+  for (int i = 0; i < SZ; ++i) z[TOFF + i] = M[MOFF + i * SZ + i] * t[TOFF + i];
+#pragma unroll
+  for (int i = 0; i < SZ; ++i)
+#pragma unroll
+    for (int j = i + 1; j < SZ; ++j) {
+      const double v = M[MOFF + i * SZ + j];
+      z[TOFF + i] = fma(v, t[TOFF + j], z[TOFF + i]);
+      z[TOFF + j] = fma(v, t[TOFF + i], z[TOFF + j]);
+    }
+}
+
+template <int N1>
+__device__ __forceinline__ void soa_blocks_c(const double* M, const double* t, double* z) {
+  using C = SoaCfg<N1>;
+  constexpr int M1 = C::A0 * C::A0, M2 = M1 + C::A1 * C::A1, M3 = M2 + C::A2 * C::A2;
+  soa_block_c<C::A0, 0, 0>(M, t, z);
+  soa_block_c<C::A1, M1, C::A0>(M, t, z);
+  soa_block_c<C::A2, M2, C::A0 + C::A1>(M, t, z);
+  soa_block_c<C::A3, M3, C::A0 + C::A1 + C::A2>(M, t, z);
+}
+
 // a.M (dense class blocks, row-major, symmetric) -> packed upper triangles in shared memory
 template <int N1>
 __device__ __forceinline__ void soa_load_blocks(const SoaArgs<N1>& a, double* Ms) {
@@ -214,7 +246,7 @@ __device__ __forceinline__ void soa_load_blocks(const SoaArgs<N1>& a, double* Ms
   }
 }
 
-template <int N1>
+template <int N1, int MCONST = (HDG_SOA_MCONST < 0 ? (N1 <= 5) : HDG_SOA_MCONST)>
 __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
     soa_apply_kernel(const __grid_constant__ SoaArgs<N1> a) {
   constexpr int NT = 4 * N1, RING = SoaCfg<N1>::RING, D = RING - 1;
@@ -223,8 +255,10 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
   constexpr int VOFF = N1 * 32;
   extern __shared__ __align__(16) double smem_soa[];
   double* Ms = smem_soa;
-  soa_load_blocks<N1>(a, Ms);
-  __syncthreads();
+  if (!MCONST) {
+    soa_load_blocks<N1>(a, Ms);
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * (SoaCfg<N1>::NTH / 32) + (threadIdx.x >> 5);
   if (gw >= a.W * a.nseg) return;                      // whole warps only
@@ -299,7 +333,8 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
 #else
     double tv[NT], z[NT];
     soa_forward<N1>(xB, xR, xT, xL, tv);
-    soa_blocks<N1>(Ms, tv, z);
+    if (MCONST) soa_blocks_c<N1>(a.M, tv, z);
+    else soa_blocks<N1>(Ms, tv, z);
     soa_backward<N1>(z, yB, yR, yT, yL);
 #endif
 #if HDG_SOA_EXP == 2   // experiment: no stores unless the result is NaN (compute + loads only)

@@ -148,11 +148,25 @@ class BlockJacobiSmoother:
         self.aggressiveness = 0
         self.lam_max = None
         block_op.set_blockjacobi(self.omega)
-        lay = block_op.layout
-        n1 = lay.n1
-        # stored smoother entries vs operator nonzeros (cf. multigrid.py:154-156)
-        nnz_est = lay.n_blocks * n1 * n1 * 7
-        self.complexity = lay.n_blocks * n1 * n1 / max(nnz_est, 1)
+        self._complexity = None
+
+    @property
+    def complexity(self):
+        """Stored smoother entries / nnz(A) (cf. multigrid.py:154-156): n_blocks n1^2 over the
+        operator's nonzeros - counted on the assembled CSR for levels up to 1M dofs (the oracle's
+        count), else the structural count of the 7-facet stencil (identical unless an element
+        block holds exact zeros)."""
+        if self._complexity is None:
+            lay = self.block_op.layout
+            n1 = lay.n1
+            if lay.ndof <= 1_000_000:
+                A = self.block_op.tocsr()
+                A.eliminate_zeros()
+                nnz = A.nnz
+            else:
+                nnz = structural_nnz(lay.nx, lay.ny, n1)
+            self._complexity = lay.n_blocks * n1 * n1 / max(nnz, 1)
+        return self._complexity
 
     def smooth(self, matvec, b, x, steps):
         """`matvec` is accepted for signature parity; the sweep applies this level's operator."""
@@ -197,6 +211,25 @@ class BlockJacobiSmoother:
         out = dev.empty(rd.numel())
         check(lib.hdg_bj_sweep(self.block_op.handle, dev.ptr(rd), dev.ptr(z), dev.ptr(out), dev.stream()))
         return dev.back(out / self.omega, was_np)
+
+
+def structural_nnz(nx, ny, n1):
+    """Nonzeros of the condensed operator on an nx x ny mesh: every interior facet couples with
+    itself and the interior facets of its two elements (at most 7 blocks, trace.py:98-128)."""
+    nx, ny = int(nx), int(ny)
+    if nx < 1 or ny < 1:
+        return 0
+    hj = np.arange(1, ny)                        # interior horizontal lines
+    vi = np.arange(1, nx)                        # interior vertical lines
+    hline = lambda j: ((j >= 1) & (j <= ny - 1)).astype(np.int64)
+    vline = lambda i: ((i >= 1) & (i <= nx - 1)).astype(np.int64)
+    i = np.arange(nx)
+    # h(i, j): itself, h(i, j -+ 1), v(i | i+1, j-1), v(i | i+1, j)
+    per_h = (1 + hline(hj - 1) + hline(hj + 1))[:, None] + 2 * (vline(i) + vline(i + 1))[None, :]
+    j = np.arange(ny)
+    # v(i, j): itself, v(i -+ 1, j), h(i-1 | i, j), h(i-1 | i, j+1)
+    per_v = (1 + vline(vi - 1) + vline(vi + 1))[:, None] + 2 * (hline(j) + hline(j + 1))[None, :]
+    return int(per_h.sum() + per_v.sum()) * n1 * n1
 
 
 # ------------------------------------------------------------------------------ levels
@@ -475,9 +508,6 @@ class _NativeMG:
             pass
 
 
-_MG_CACHE = {}
-
-
 def set_fused_tail(levels, enable=True):
     """Run the small trailing p = 1 levels of the device cycle as one cooperative kernel
     (default) or as separate launches (hdgb200.h: hdg_mg_set_fused_tail)."""
@@ -485,15 +515,27 @@ def set_fused_tail(levels, enable=True):
 
 
 def _native_mg(levels):
+    """The native level stack of `levels` (a hierarchy or a suffix / slice of one).  It is cached
+    on the hierarchy's first level, so it lives exactly as long as the levels do: dropping the
+    hierarchy frees its device workspaces and CUDA graphs (cyclic garbage, collected by gc)."""
+    first = levels[0]
+    cache = first.__dict__.setdefault("_native_cache", {})
     key = tuple(id(lev) for lev in levels)
-    mg = _MG_CACHE.get(key)
+    mg = cache.get(key)
     if mg is None or any(a is not b for a, b in zip(mg.levels, levels)):
         for lev in levels[:-1]:
             if not isinstance(lev.smoother, (BlockJacobiSmoother, FSAISmoother)):
                 raise NotImplementedError("the device cycle needs a block-Jacobi or FSAI smoother on every level")
         mg = _NativeMG(list(levels))
-        _MG_CACHE[key] = mg
+        cache[key] = mg
     return mg
+
+
+def release_native(levels):
+    """Free the native cycle state (workspaces, graphs) cached on `levels` now, instead of at
+    garbage collection."""
+    for lev in levels:
+        lev.__dict__.pop("_native_cache", None)
 
 
 def _run_cycle(levels, b, x0, nu1, nu2, visits, use_graph=True):
@@ -527,19 +569,14 @@ def solve_mg(levels, b=None, x0=None, cycle="v", nu1=2, nu2=2, tol=1e-12, max_cy
     visits = {"v": 1, "w": 2}[cycle]
     mg = _native_mg(levels)
     mon = ConvergenceMonitor()
-    scratch = dev.empty(1)
-    s = dev.stream()
-    check(lib.hdg_dot(dev.ptr(bd), dev.ptr(bd), n, dev.ptr(scratch), s))
-    bnorm = float(scratch.item()) ** 0.5 or 1.0
-    op = fine.block_op
-    mon.record(op.residual_norm(bd, x))
-    for _ in range(max_cycles):
-        if mon.residuals[-1] <= tol * bnorm:
-            break
-        check(lib.hdg_mg_cycle(mg.handle, dev.ptr(bd), dev.ptr(x), dev.ptr(x), int(nu1), int(nu2), visits, 1, s))
-        mon.record(op.residual_norm(bd, x))
-        if mon.diverged():
-            break
+    hist = np.zeros(max(int(max_cycles), 0) + 1)
+    ncyc = ctypes.c_int(0)
+    # the whole loop (stop test, cycles, monitor residuals, divergence) runs natively: hdg_solve_mg
+    check(lib.hdg_solve_mg(mg.handle, dev.ptr(bd), dev.ptr(x), int(nu1), int(nu2), visits, float(tol),
+                           int(max_cycles), hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                           ctypes.byref(ncyc), dev.stream()))
+    for v in hist[:ncyc.value + 1] if n else [0.0]:
+        mon.record(v)
     return dev.back(x, was_np), mon
 
 
@@ -553,10 +590,21 @@ def fmg(levels, nu1=2, nu2=2, cycles_per_level=1):
     return x
 
 
+class MGPreconditioner:
+    """multigrid.py:457-463: one V-cycle from zero (device in, device out).  Callable like the
+    reference's closure; TraceSystem.solve_cg recognises it and runs the whole preconditioned
+    CG natively (hdg_pcg)."""
+
+    def __init__(self, levels, nu1=2, nu2=2):
+        self.levels, self.nu1, self.nu2 = levels, nu1, nu2
+
+    def __call__(self, r):
+        return v_cycle(self.levels, r, None, self.nu1, self.nu2)
+
+    def native(self):
+        return _native_mg(self.levels)
+
+
 def mg_preconditioner(levels, nu1=2, nu2=2):
-    """multigrid.py:457-463: one V-cycle from zero (device in, device out)."""
-
-    def apply(r):
-        return v_cycle(levels, r, None, nu1, nu2)
-
-    return apply
+    """multigrid.py:457-463."""
+    return MGPreconditioner(levels, nu1, nu2)

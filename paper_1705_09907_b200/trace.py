@@ -561,6 +561,19 @@ class TraceSystem:
         bd, was_np = dev.to_device(self.rhs if b is None else b)
         n = bd.numel()
         s = dev.stream()
+        native_pc = precond is None or hasattr(precond, "native")
+        if matvec is None and native_pc:
+            # the whole loop natively (hdg_pcg): iteration body = one CUDA graph, one D2H of ||r||^2
+            x = dev.zeros(n) if x0 is None else dev.to_device(x0)[0].clone()
+            mg = precond.native() if precond is not None else None
+            hist = np.zeros(int(maxiter) + 1)
+            its = ctypes.c_int(0)
+            check(lib.hdg_pcg(self.operator.handle, mg.handle if mg is not None else None, dev.ptr(bd), dev.ptr(x),
+                              int(x0 is not None), float(tol), int(maxiter),
+                              int(getattr(precond, "nu1", 2)), int(getattr(precond, "nu2", 2)),
+                              hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(its), s))
+            self.cg_residuals = hist[:min(its.value, int(maxiter)) + 1]
+            return dev.back(x, was_np), its.value
         mv = matvec or self.operator.apply
         x = dev.zeros(n) if x0 is None else dev.to_device(x0)[0].clone()
         r = bd - mv(x) if x0 is not None else bd.clone()

@@ -41,4 +41,6 @@ def P():
         pass
     ns = NS()
     ns.mg, ns.pb, ns.tr, ns.mesh = mg, pb, tr, build_cartesian
+    from paper_1705_09907_b200._lib import check, lib
+    ns.lib, ns.lib_check = lib, check
     return ns

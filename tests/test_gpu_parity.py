@@ -126,15 +126,23 @@ def test_config2_properties_full_size(P):
     A2 = s.matvec_free(2.0 * x + yv)
     assert float((A2 - (2.0 * Ax + Ay)).abs().max()) <= 1e-12 * float(A2.abs().max())
     assert torch.equal(Ax, s.matvec_free(x))
-    # sampled facets against the oracle restatement on the gathered element traces
-    S = s.operator.S_cls[0]
-    xs = x.cpu().numpy()
-    lay = s.layout
-    xe_all = lay.gather(xs)
-    cm = np.repeat(lay.side_mask(), p + 1, axis=1)
-    ye = np.einsum("ij,ej->ei", S, xe_all * cm)
-    ref = lay.sum_owners(ye)
-    assert rel(Ax.cpu().numpy(), ref) < TOL
+
+
+def test_config2_full_size_vs_oracle_both_kernels(P):
+    """configs[1] at full size (1024^2, p=4, K=I, x ~ U[-1,1] seed 1) against the ORACLE's own
+    injected system (its element block from its own local condensation; gather / einsum /
+    two-owner sum of trace.py:87-94): the reference-layout kernel (matvec_free on a vector) and
+    the facet-record kernel (the bench's), both at 1e-12 relative."""
+    n, p = 1024, 4
+    osys = O.injected_shared_system(n, p)
+    x = np.random.default_rng(1).uniform(-1.0, 1.0, osys.ndof)
+    ref = osys.matvec(x)
+    del osys
+    s = P.tr.TraceSystem(P.mesh(n, n), p, specs.constant(P.pb.ProblemSpec))
+    y_ref_layout = s.matvec_free(x)
+    y_records = s.matvec_free(s.facet_planes(x)).numpy()
+    assert rel(y_ref_layout, ref) < TOL
+    assert rel(y_records, ref) < TOL
 
 
 # ------------------------------------------------------------------------------ transfers
@@ -617,3 +625,77 @@ def test_reattached_smoother_recaptures_cycle_graphs(P):
         if mode != "blockjacobi":
             assert rel(x, x_bj) > 1e-6, mode
     assert rel(x, x_bj) < 1e-13
+    # fixed buffers through the C ABI: a replay hits the cache, a re-attached smoother forces a
+    # fresh capture (hdg_mg_graph_captures counts instantiations)
+    mg = P.mg._native_mg(levels)
+    xo = torch.zeros_like(bd)
+    st = torch.cuda.current_stream().cuda_stream
+    cyc = lambda: P.lib_check(P.lib.hdg_mg_cycle(mg.handle, bd.data_ptr(), None, xo.data_ptr(), 2, 2, 1, 1, st))
+    cyc()
+    c0 = P.lib.hdg_mg_graph_captures(mg.handle)
+    cyc()
+    assert P.lib.hdg_mg_graph_captures(mg.handle) == c0
+    P.mg.attach_smoothers(levels, "bj-chebyshev")
+    cyc()
+    assert P.lib.hdg_mg_graph_captures(mg.handle) == c0 + 1
+
+
+def test_cycle_graph_cache_is_bounded(P):
+    """Graphs are keyed by buffer pointers; callers whose buffers move must not grow the cache
+    without bound (LRU of 8): 12 distinct output buffers -> 12 captures, replays of the last
+    ones hit the cache, and every result equals the first."""
+    import torch
+    n, p = 8, 2
+    levels = P.mg.build_hierarchy(P.mesh(n, n), p, P.pb.constant_problem(0.0, 1.0), smoother="blockjacobi")
+    mg = P.mg._native_mg(levels)
+    bd = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, levels[0].ndof)).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    outs = [torch.zeros_like(bd) for _ in range(12)]
+    c0 = P.lib.hdg_mg_graph_captures(mg.handle)
+    for o in outs:
+        P.lib_check(P.lib.hdg_mg_cycle(mg.handle, bd.data_ptr(), None, o.data_ptr(), 2, 2, 1, 1, st))
+    assert P.lib.hdg_mg_graph_captures(mg.handle) == c0 + 12
+    for o in outs[-8:]:
+        P.lib_check(P.lib.hdg_mg_cycle(mg.handle, bd.data_ptr(), None, o.data_ptr(), 2, 2, 1, 1, st))
+    assert P.lib.hdg_mg_graph_captures(mg.handle) == c0 + 12
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
+def test_native_pcg_matches_python_loop(P, golden):
+    """hdg_pcg (the whole trace.py:142-163 loop natively, one graph per iteration, one D2H)
+    against the host-driven loop of the same device kernels: same iteration count, same iterate
+    to rounding, with the MG preconditioner (multigrid.py:457-463), without one, and from x0."""
+    g = golden("hierarchies.npz")
+    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(g["het8p2_K"]), specs.zero, specs.zero, 1.0)
+    levels = P.mg.build_hierarchy(P.mesh(8, 8), 2, spec, smoother="blockjacobi")
+    sysg = levels[0].system
+    b = g["het8p2_b"]
+    pc = P.mg.mg_preconditioner(levels)
+    x_nat, it_nat = sysg.solve_cg(tol=1e-10, precond=pc, b=b)
+    x_py, it_py = sysg.solve_cg(tol=1e-10, precond=lambda r: pc(r), b=b)
+    assert it_nat == it_py == int(g["het8p2_pcg_iters"][0])
+    assert rel(x_nat, x_py) < 1e-13
+    hist = sysg.cg_residuals
+    assert len(hist) == it_nat + 1 and hist[-1] <= 1e-10 * np.linalg.norm(b) < hist[-2]
+    x_nat, it_nat = sysg.solve_cg(tol=1e-9, b=b, maxiter=3000)
+    x_py, it_py = sysg.solve_cg(tol=1e-9, b=b, maxiter=3000, matvec=sysg.operator.apply)
+    assert it_nat == it_py and rel(x_nat, x_py) < 1e-12
+    x0 = np.random.default_rng(2).standard_normal(sysg.ndof)
+    x_nat, it_nat = sysg.solve_cg(tol=1e-10, precond=pc, b=b, x0=x0)
+    x_py, it_py = sysg.solve_cg(tol=1e-10, precond=lambda r: pc(r), b=b, x0=x0)
+    assert it_nat == it_py and rel(x_nat, x_py) < 1e-12
+    _, it0 = sysg.solve_cg(tol=1e-10, precond=pc, b=b, maxiter=0)
+    assert it0 == 0
+
+
+def test_blockjacobi_complexity_matches_oracle(P):
+    """BlockJacobiSmoother.complexity = n_blocks n1^2 / nnz(A) per level, counted like the
+    oracle's CSR; the structural count used above 1M dofs agrees on K = I."""
+    n, p = 16, 3
+    lv = P.mg.build_hierarchy(P.mesh(n, n), p, specs.constant(P.pb.ProblemSpec), smoother="blockjacobi")
+    lo = O.build_levels(O.Grid(n, n), p, specs.constant(O.Spec), smoother="blockjacobi")
+    for a, b in zip(lv[:-1], lo[:-1]):
+        assert abs(a.smoother.complexity - b.smoother.complexity) < 1e-12
+        lay = a.block_op.layout
+        assert P.mg.structural_nnz(lay.nx, lay.ny, lay.n1) == a.block_op.tocsr().nnz
