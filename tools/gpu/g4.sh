@@ -1,0 +1,2 @@
+for i in 1 2; do python bench.py --steps 10 --warmup 3 --no-cpu --no-vcycle > gpurun_out/bench4_$i.log 2>&1; python -c "
+import json;d=json.loads(open('gpurun_out/bench4_$i.log').read().strip().splitlines()[-1]);print(d['value'],d['e2e']['value'],d['roofline']['frac'],d['roofline']['kernel_us_avg'], d['roofline']['kernel_us_single_median'])"; done
