@@ -111,6 +111,20 @@ int hdg_level_set_fsai(hdg_level* lev, int64_t n, const int32_t* g_rowptr, const
 int hdg_fsai_rows(int64_t n, const int32_t* a_ptr, const int32_t* a_col, const double* a_val,
                   const int32_t* g_ptr, const int32_t* g_col, double* g_val, int32_t max_len,
                   int64_t* bad_row, void* stream);
+/* Facet-structured FSAI (hdg_fsai.cuh), the baseline pattern lower(A) of multigrid.py:127-131
+ * built ON THE DEVICE from the level's element blocks: S_cls (C, 4n1, 4n1) DEVICE, elem_class
+ * (E,) int64 DEVICE (element e = j nx + i -> class).  One Cholesky per facet gives its n1 rows of G
+ * (multigrid.py:133-152); lambda_max(G'GA) by lam_iters power steps from the DEVICE start vector
+ * v0 (the reference draws it with seed 1234, multigrid.py:162-173) -> *lam_max_out; Chebyshev
+ * lower fraction and omega as FSAISmoother (multigrid.py:76-88).  A non-SPD principal system
+ * returns HDG_ESTATE with *bad_row = the first failing DOF row (NotSPDError, multigrid.py:145-148).
+ * p <= 8. */
+int hdg_level_set_fsai_struct(hdg_level* lev, const double* S_cls, const int64_t* elem_class, const double* v0,
+                              int lam_iters, double cheb_fraction, double omega, double* lam_max_out,
+                              int64_t* bad_row, void* stream);
+/* copy the structured factor to the host: gh (nx (ny-1) * n1 * 2n1), gv ((nx-1) ny * n1 * 6n1),
+ * layout Gh[(k 2n1 + c) nh + f], Gv[(k 6n1 + c) nv + f] (hdg_fsai.cuh) */
+int hdg_level_fsai_struct_get(const hdg_level* lev, double* gh, double* gv);
 /* z = G'(G r)  (multigrid.py:72-74) */
 int hdg_fsai_apply(const hdg_level* lev, const double* r, double* z, void* stream);
 /* `steps` Chebyshev-weighted sweeps x <- x + w_k G'G(b - A x) in place (multigrid.py:83-88);

@@ -40,6 +40,9 @@ SIGNATURES = [
     ("hdg_bj_sweeps", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     ("hdg_level_set_fsai", c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p,
                                    c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_double]),
+    ("hdg_level_set_fsai_struct", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, ctypes.c_double,
+                                          ctypes.c_double, c_double_p, ctypes.POINTER(c_int64), c_void_p]),
+    ("hdg_level_fsai_struct_get", c_int, [c_void_p, c_void_p, c_void_p]),
     ("hdg_fsai_apply", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     ("hdg_fsai_sweeps", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     ("hdg_transfer_create_p", c_int, [c_void_p, c_void_p, c_void_p, ctypes.POINTER(c_void_p)]),

@@ -4,6 +4,7 @@
 #include "hdgb200.h"
 #include "hdg_kernels.cuh"
 #include "hdg_soa.cuh"
+#include "hdg_fsai.cuh"
 
 #include <algorithm>
 #include <climits>
@@ -67,6 +68,9 @@ struct hdg_level {
   int *g_ptr = nullptr, *g_col = nullptr, *gt_ptr = nullptr, *gt_col = nullptr;
   double *g_val = nullptr, *gt_val = nullptr;
   double lam_max = 1.0, cheb_frac = 0.15, fsai_omega = 1.0;
+  // facet-structured FSAI (hdg_fsai.cuh): G rows per facet, no column indices, G' by gathers
+  bool fsai_struct = false;
+  double *fGh = nullptr, *fGv = nullptr;
   unsigned smoother_gen = 0;     // bumped by every smoother setter: cycle graphs captured before are stale
   double* tail_wd = nullptr;   // fused coarse tail, shared mode: device copy of Wh, Wv, Dh, Dv (n1 = 2)
   // facet-plane (SoA) device layout, shared mode (hdg_soa.cuh): element block + adapted blocks
@@ -160,6 +164,9 @@ static int sm_count() {
   }
   return n;
 }
+
+static int vec_blocks();
+static int dot_into(const double* a, const double* b, int64_t n, double* out, double* partials, cudaStream_t s);
 
 // persistent grid: every SM gets as many CTAs as fit (<= MAX_CTAS_PER_SM), never more than tiles
 template <int N1, bool STORED, int EPI>
@@ -442,6 +449,7 @@ int hdg_level_destroy(hdg_level* L) {
   cudaFree(L->tail_wd);
   cudaFree(L->g_ptr); cudaFree(L->g_col); cudaFree(L->g_val);
   cudaFree(L->gt_ptr); cudaFree(L->gt_col); cudaFree(L->gt_val);
+  cudaFree(L->fGh); cudaFree(L->fGv);
   delete L;
   return 0;
 }
@@ -671,16 +679,46 @@ int hdg_level_set_fsai(hdg_level* L, int64_t n, const int32_t* g_ptr, const int3
       (rc = upload(&L->gt_col, gt_col, nnz)) || (rc = upload(&L->gt_val, gt_val, nnz)))
     return rc;
   L->lam_max = lam_max; L->cheb_frac = cheb_fraction; L->fsai_omega = omega;
+  L->fsai_struct = false;
   L->has_fsai = true;
   L->use_fsai = true;
   smoother_changed(L);
   return 0;
 }
 
+}  // extern "C"
+template <int N1>
+static int fsai_struct_apply_t(const hdg_level* L, bool transposed, const double* x, double* y, const double* xin,
+                               double w, cudaStream_t s) {
+  FsaiApplyArgs a{};
+  a.Gh = L->fGh; a.Gv = L->fGv; a.x = x; a.y = y; a.xin = xin; a.w = w;
+  a.nx = L->nx; a.ny = L->ny; a.nh = L->nh; a.nvf = (long long)(L->nx - 1) * L->ny;
+  const long long nf = a.nh + a.nvf;
+  const int bs = 128;
+  const unsigned grid = (unsigned)((nf + bs - 1) / bs);
+  if (!transposed) fsai_g_kernel<N1><<<grid, bs, 0, s>>>(a);
+  else if (xin) fsai_gt_kernel<N1, true><<<grid, bs, 0, s>>>(a);
+  else fsai_gt_kernel<N1, false><<<grid, bs, 0, s>>>(a);
+  CKL();
+  return 0;
+}
+
+#define HDG_FSAI_SWITCH(n1, CALL)                                             \
+  switch (n1) {                                                               \
+    case 2: CALL(2); case 3: CALL(3); case 4: CALL(4); case 5: CALL(5);       \
+    case 6: CALL(6); case 7: CALL(7); case 8: CALL(8); case 9: CALL(9);       \
+    default: return fail(HDG_EINVAL, "structured FSAI: p <= 8");              \
+  }
+
 static int spmv(const hdg_level* L, bool transposed, const double* x, double* y, const double* xin, double w,
                 cudaStream_t s) {
   const int n = (int)L->ndof;
   if (n == 0) return 0;
+  if (L->fsai_struct) {
+#define FSA_CASE(N) return fsai_struct_apply_t<N>(L, transposed, x, y, xin, w, s);
+    HDG_FSAI_SWITCH(L->n1, FSA_CASE)
+#undef FSA_CASE
+  }
   const int bs = 256;
   const unsigned grid = (unsigned)(((long long)n * 4 + bs - 1) / bs);
   const int* rp = transposed ? L->gt_ptr : L->g_ptr;
@@ -691,6 +729,8 @@ static int spmv(const hdg_level* L, bool transposed, const double* x, double* y,
   CKL();
   return 0;
 }
+
+extern "C" {
 
 // Chebyshev-weighted steps (multigrid.py:76-81)
 static double fsai_weight(const hdg_level* L, int k, int steps) {
@@ -727,6 +767,135 @@ int hdg_fsai_sweeps(const hdg_level* L, const double* b, double* x, double* work
   if (!L || !L->has_fsai) return fail(HDG_ESTATE, "FSAI state not set");
   if (L->ndof == 0 || steps < 1) return 0;
   return fsai_sweeps(L, b, x, work_r, work_t, steps, S(stream));
+}
+
+}  // extern "C"
+
+// --------------------------------------------------------------- facet-structured FSAI setup
+
+template <int N1>
+static int fsai_struct_setup_t(hdg_level* L, const double* S, const long long* cls, const double* v0, int iters,
+                               double* lams_host, long long* bad_host, cudaStream_t s) {
+  const long long nvf = (long long)(L->nx - 1) * L->ny;
+  const size_t ghb = sizeof(double) * (size_t)L->nh * N1 * 2 * N1;
+  const size_t gvb = sizeof(double) * (size_t)nvf * N1 * 6 * N1;
+  cudaFree(L->fGh); cudaFree(L->fGv);
+  L->fGh = L->fGv = nullptr;
+  if (cudaMalloc(&L->fGh, ghb ? ghb : 8) != cudaSuccess || cudaMalloc(&L->fGv, gvb ? gvb : 8) != cudaSuccess)
+    return fail(HDG_ENOMEM, "cannot allocate the FSAI factor");
+  double* Dg = nullptr;
+  long long* bad = nullptr;
+  CK(cudaMallocAsync((void**)&Dg, sizeof(double) * (size_t)L->n_blocks * N1 * N1, s));
+  CK(cudaMallocAsync((void**)&bad, sizeof(long long), s));
+  const long long init = LLONG_MAX;
+  CK(cudaMemcpyAsync(bad, &init, sizeof(long long), cudaMemcpyHostToDevice, s));
+  const long long nd = L->n_blocks * N1 * N1;
+  fsai_diag_kernel<N1><<<(unsigned)((nd + 255) / 256), 256, 0, s>>>(S, cls, L->nx, L->ny, L->nh, L->n_blocks, Dg);
+  CKL();
+  static int occ = -1;
+  if (occ < 0) {
+    CK(cudaFuncSetAttribute(fsai_setup_kernel<N1>, cudaFuncAttributeMaxDynamicSharedMemorySize, FsaiCfg<N1>::SMEM));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fsai_setup_kernel<N1>, 32 * FsaiCfg<N1>::WARPS,
+                                                      FsaiCfg<N1>::SMEM) != cudaSuccess || occ < 1)
+      occ = 1;
+  }
+  FsaiSetupArgs a{};
+  a.S = S; a.cls = cls; a.Dg = Dg; a.Gh = L->fGh; a.Gv = L->fGv; a.bad = bad;
+  a.nx = L->nx; a.ny = L->ny; a.nh = L->nh; a.nvf = nvf;
+  const long long nf = L->nh + nvf;
+  const long long want = (nf + FsaiCfg<N1>::WARPS - 1) / FsaiCfg<N1>::WARPS;
+  const long long grid = std::min(want, (long long)sm_count() * occ);
+  fsai_setup_kernel<N1><<<(unsigned)std::max(grid, 1LL), 32 * FsaiCfg<N1>::WARPS, FsaiCfg<N1>::SMEM, s>>>(a);
+  CKL();
+  cudaFreeAsync(Dg, s);
+  CK(cudaMemcpyAsync(bad_host, bad, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(bad, s);
+  CK(cudaStreamSynchronize(s));
+  if (*bad_host != LLONG_MAX) return 0;
+  // lambda_max(G'G A): power iteration from the caller's start vector (multigrid.py:162-173)
+  L->fsai_struct = true;   // spmv() below dispatches to the structured kernels
+  const size_t vb = sizeof(double) * (size_t)L->ndof;
+  double *v = nullptr, *q = nullptr, *t = nullptr, *w = nullptr, *nrm = nullptr, *lam = nullptr, *part = nullptr;
+  CK(cudaMallocAsync((void**)&v, vb, s)); CK(cudaMallocAsync((void**)&q, vb, s));
+  CK(cudaMallocAsync((void**)&t, vb, s)); CK(cudaMallocAsync((void**)&w, vb, s));
+  CK(cudaMallocAsync((void**)&nrm, sizeof(double), s));
+  CK(cudaMallocAsync((void**)&lam, sizeof(double) * std::max(iters, 1), s));
+  CK(cudaMallocAsync((void**)&part, sizeof(double) * vec_blocks(), s));
+  CK(cudaMemcpyAsync(v, v0, vb, cudaMemcpyDeviceToDevice, s));
+  int rc = 0;
+  for (int it = 0; it < iters && !rc; ++it) {
+    MvArgs ma{};
+    ma.x = v; ma.out = q;
+    rc = apply(L, EPI_Y, ma, s);                                      // A v
+    if (!rc) rc = spmv(L, false, q, t, nullptr, 0.0, s);              // G A v
+    if (!rc) rc = spmv(L, true, t, w, nullptr, 0.0, s);               // G' G A v
+    if (!rc) rc = dot_into(w, w, L->ndof, nrm, part, s);
+    if (!rc) { fsai_scale_kernel<<<vec_blocks(), 256, 0, s>>>(w, nrm, v, lam + it, L->ndof); CKL(); }
+  }
+  if (!rc && iters > 0) {
+    if (cudaMemcpyAsync(lams_host, lam, sizeof(double) * iters, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      rc = fail(HDG_ECUDA, "lambda_max readback");
+  }
+  cudaFreeAsync(v, s); cudaFreeAsync(q, s); cudaFreeAsync(t, s); cudaFreeAsync(w, s);
+  cudaFreeAsync(nrm, s); cudaFreeAsync(lam, s); cudaFreeAsync(part, s);
+  return rc;
+}
+
+extern "C" {
+
+int hdg_level_set_fsai_struct(hdg_level* L, const double* S_cls, const int64_t* elem_class, const double* v0,
+                              int lam_iters, double cheb_fraction, double omega, double* lam_max_out,
+                              int64_t* bad_row, void* stream) {
+  if (!L || !lam_max_out || !bad_row) return fail(HDG_EINVAL, "null argument");
+  *bad_row = -1;
+  // invalidate first (a failure leaves a level the cycle refuses)
+  L->has_fsai = L->use_fsai = L->fsai_struct = false;
+  smoother_changed(L);
+  if (L->ndof == 0) {
+    *lam_max_out = 1.0;
+    L->lam_max = 1.0; L->cheb_frac = cheb_fraction; L->fsai_omega = omega;
+    L->fsai_struct = L->has_fsai = L->use_fsai = true;
+    return 0;
+  }
+  if (!S_cls || !elem_class || !v0 || lam_iters < 1) return fail(HDG_EINVAL, "null argument");
+  std::vector<double> lams(lam_iters, 0.0);
+  long long bad = LLONG_MAX;
+  cudaStream_t s = S(stream);
+  int rc;
+#define FSS_CASE(N) { rc = fsai_struct_setup_t<N>(L, S_cls, reinterpret_cast<const long long*>(elem_class), v0, \
+                                                  lam_iters, lams.data(), &bad, s); break; }
+  switch (L->n1) {
+    case 2: FSS_CASE(2) case 3: FSS_CASE(3) case 4: FSS_CASE(4) case 5: FSS_CASE(5)
+    case 6: FSS_CASE(6) case 7: FSS_CASE(7) case 8: FSS_CASE(8) case 9: FSS_CASE(9)
+    default: return fail(HDG_EINVAL, "structured FSAI: p <= 8");
+  }
+#undef FSS_CASE
+  if (rc) { L->fsai_struct = false; return rc; }
+  if (bad != LLONG_MAX) {
+    L->fsai_struct = false;
+    *bad_row = bad;
+    return fail(HDG_ESTATE, "non-SPD principal submatrix in FSAI row " + std::to_string(bad));
+  }
+  double lam = 1.0;
+  for (int it = 0; it < lam_iters; ++it) {            // multigrid.py:167-172
+    lam = lams[it];
+    if (lam == 0.0) { lam = 1.0; break; }
+  }
+  *lam_max_out = lam;
+  L->lam_max = lam; L->cheb_frac = cheb_fraction; L->fsai_omega = omega;
+  L->fsai_struct = L->has_fsai = L->use_fsai = true;
+  smoother_changed(L);
+  return 0;
+}
+
+int hdg_level_fsai_struct_get(const hdg_level* L, double* gh_host, double* gv_host) {
+  if (!L || !L->fsai_struct) return fail(HDG_ESTATE, "no structured FSAI on this level");
+  const long long nvf = (long long)(L->nx - 1) * L->ny;
+  const int n1 = L->n1;
+  if (L->nh && gh_host) CK(cudaMemcpy(gh_host, L->fGh, sizeof(double) * L->nh * n1 * 2 * n1, cudaMemcpyDeviceToHost));
+  if (nvf && gv_host) CK(cudaMemcpy(gv_host, L->fGv, sizeof(double) * nvf * n1 * 6 * n1, cudaMemcpyDeviceToHost));
+  return 0;
 }
 
 // ---------------------------------------------------------------------------- transfers
@@ -817,6 +986,8 @@ int hdg_restrict(const hdg_transfer* t, const double* rf, double* rc, void* stre
 
 // ---------------------------------------------------------------------------- reductions
 
+}  // extern "C"
+
 // streaming grid of the vector kernels: 4 CTAs of 256 threads per SM of this device
 static int vec_blocks() { return 4 * sm_count(); }
 
@@ -830,6 +1001,8 @@ static int dot_into(const double* a, const double* b, int64_t n, double* out, do
   CKL();
   return 0;
 }
+
+extern "C" {
 
 int hdg_dot(const double* a, const double* b, int64_t n, double* out, void* stream) {
   if (!out || (n > 0 && (!a || !b))) return fail(HDG_EINVAL, "null argument");

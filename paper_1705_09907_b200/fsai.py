@@ -165,6 +165,108 @@ class FSAISmoother:
         return dev.back(xd, was_np)
 
 
+class StructuredFSAI(FSAISmoother):
+    """FSAISmoother with the baseline pattern lower(A) (multigrid.py:123-159) set up ENTIRELY on
+    the device from the level's element blocks (hdg_level_set_fsai_struct, hdg_fsai.cuh): one
+    Cholesky per facet gives the facet's n1 rows of G, stored per facet without column indices;
+    lambda_max(G'GA) by the reference's 20 power steps from its seed-1234 start vector
+    (multigrid.py:162-173).  No host CSR, no host pattern: this is the path for large levels.
+    `.G` / `.Gt` assemble scipy CSR views on demand (small levels; tests and API parity)."""
+
+    LAM_ITERS = 20
+
+    def __init__(self, block_op, omega=1.0, seed=1234):
+        import torch
+        self.block_op = block_op
+        self.omega = float(omega)
+        self.aggressiveness = 1
+        self.cheb_fraction = CHEB_LOWER_FRACTION
+        self.complexity = 1.0          # (2 nnz(lower A) - n) / nnz(A) for a symmetric pattern
+        self._G = None
+        n = block_op.ndof
+        S = block_op.S_cls
+        if S is None:
+            raise ValueError("structured FSAI needs the level's element blocks (build it before release_blocks)")
+        S = S if isinstance(S, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(S))
+        S = S.to(device="cuda", dtype=torch.float64).contiguous()
+        cls = torch.from_numpy(np.ascontiguousarray(block_op.elem_class, dtype=np.int64)).cuda()
+        v0 = torch.from_numpy(np.random.default_rng(seed).standard_normal(n)).cuda() if n else None
+        lam = ctypes.c_double(1.0)
+        bad = ctypes.c_int64(-1)
+        rc = lib.hdg_level_set_fsai_struct(block_op.handle, S.data_ptr(), cls.data_ptr(),
+                                           v0.data_ptr() if v0 is not None else None, self.LAM_ITERS,
+                                           self.cheb_fraction, self.omega, ctypes.byref(lam), ctypes.byref(bad),
+                                           dev.stream())
+        if bad.value >= 0:
+            raise NotSPDError(f"non-SPD principal submatrix in FSAI row {bad.value}")
+        check(rc)
+        self.lam_max = float(lam.value)
+
+    def bind(self, block_op):
+        if block_op is not self.block_op:
+            raise ValueError("a structured FSAI factor belongs to the level it was built on")
+        return self
+
+    @property
+    def G(self):
+        if self._G is None:
+            self._G = self._assemble()
+        return self._G
+
+    @property
+    def Gt(self):
+        return self.G.T.tocsr()
+
+    def _assemble(self):
+        """Host CSR of the device factor: rows (f, k), columns of the pattern lower(A)."""
+        lay = self.block_op.layout
+        nx, ny, n1, nh = lay.nx, lay.ny, lay.n1, lay.nh
+        nv = (nx - 1) * ny
+        gh = np.zeros(nh * n1 * 2 * n1)
+        gv = np.zeros(max(nv, 0) * n1 * 6 * n1)
+        check(lib.hdg_level_fsai_struct_get(self.block_op.handle, gh.ctypes.data, gv.ctypes.data))
+        rows, cols, vals = [], [], []
+
+        def hb(i, j):
+            return np.where((j >= 1) & (j <= ny - 1) & (i >= 0) & (i < nx), (j - 1) * nx + i, -1)
+
+        def vb(i, j):
+            return np.where((i >= 1) & (i <= nx - 1) & (j >= 0) & (j < ny), nh + (i - 1) * ny + j, -1)
+
+        def emit(G, nslot, own_blk, slot_blk, nf):
+            G = G.reshape(n1, nslot * n1, nf)
+            for k in range(n1):
+                for s_ in range(nslot):
+                    for m in range(n1):
+                        if s_ == nslot - 1 and m > k:
+                            continue
+                        blk = slot_blk[s_]
+                        ok = blk >= 0
+                        rows.append(own_blk[ok] * n1 + k)
+                        cols.append(blk[ok] * n1 + m)
+                        vals.append(G[k, s_ * n1 + m, ok])
+
+        if nh:
+            f = np.arange(nh)
+            j, i = f // nx + 1, f % nx
+            emit(gh, 2, f, [hb(i, j - 1), f], nh)
+        if nv > 0:
+            fv = np.arange(nv)
+            j, i = fv // (nx - 1), fv % (nx - 1) + 1
+            own = vb(i, j)
+            emit(gv, 6, own, [hb(i - 1, j), hb(i - 1, j + 1), hb(i, j), hb(i, j + 1), vb(i - 1, j), own], nv)
+        n = lay.ndof
+        if not rows:
+            return sp.csr_matrix((n, n))
+        G = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n, n)).tocsr()
+        G.sort_indices()
+        return G
+
+
+def structured_fsai_supported(block_op, aggressiveness=1):
+    return aggressiveness == 1 and 1 <= block_op.layout.n1 <= 9 and getattr(block_op, "S_cls", None) is not None
+
+
 def _estimate_lam_max(A, G, iters=20, seed=1234):
     """multigrid.py:162-173 (host, deterministic)."""
     Gt = G.T.tocsr()

@@ -20,7 +20,7 @@ from . import _device as dev
 from ._lib import check, lib
 from .discretization import (ElementClasses, classify_rows, galerkin_h, galerkin_p, h_child_maps,
                              h_cross_maps, h_halves, p_transfer_matrix, ref_element)
-from .fsai import FSAISmoother, NotSPDError, fsai_build  # noqa: F401  (re-exported like the reference)
+from .fsai import FSAISmoother, NotSPDError, StructuredFSAI, fsai_build, structured_fsai_supported  # noqa: F401
 from .mesh import coarsen
 from .trace import BlockOperator, TraceLayout, TraceSystem
 
@@ -372,11 +372,17 @@ def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother
                       matrix_free=True, rhs=fine.rhs)]
     op = fine.operator
 
-    # FSAI smoothers are built from each level's CSR (host element blocks), so their levels keep
-    # the blocks; block-Jacobi (or a smoother attached later) lets large levels drop them
-    keep_blocks = smoother is not None and smoother not in _BJ_MODES
+    # The baseline FSAI (the reference default) is set up on the device from each level's element
+    # blocks as soon as the level exists (StructuredFSAI), so large levels can then drop their
+    # blocks; the aggressive FSAI builds from host CSR and keeps them.
+    struct_fsai = smoother == "baseline"
+    keep_blocks = smoother is not None and smoother not in _BJ_MODES and not struct_fsai
+    w_fsai = 1.0 if omega is None else float(omega)
+    early = {}
 
-    def retire(prev):
+    def retire(prev, lev):
+        if struct_fsai and structured_fsai_supported(prev):
+            early[id(lev)] = StructuredFSAI(prev, w_fsai)
         # large device-condensed levels: keep only the native facet stream (memory)
         if not keep_blocks and not isinstance(prev.S_cls, np.ndarray) and prev.ndof > RELEASE_NDOF:
             prev.release_blocks()
@@ -387,7 +393,7 @@ def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother
         levels[-1].prolong = Prolongation(op, cop, "p", V=V)
         levels.append(MGLevel(mesh, q, _LevelSystem(mesh, q, cop), kind="p-level",
                               operator=DeviceOperator(cop), matrix_free=False))
-        retire(op)
+        retire(op, levels[-2])
         op = cop
     m = mesh
     while m.n_x % 2 == 0 and m.n_y % 2 == 0 and m.n_x >= 4 and m.n_y >= 4:   # :322-327
@@ -397,7 +403,7 @@ def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother
         levels[-1].prolong = Prolongation(op, cop, "h", halves=halves, cross=cross)
         levels.append(MGLevel(m, 1, _LevelSystem(m, 1, cop), kind="h-level",
                               operator=DeviceOperator(cop), matrix_free=False))
-        retire(op)
+        retire(op, levels[-2])
         op = cop
     levels[-1].kind = "coarsest"
     if levels[-1].ndof > coarse_cap:                                  # :336-339
@@ -406,7 +412,7 @@ def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother
         prev = levels[k - 1]
         levels[k].rhs = _LazyRhs(prev, k) if prev.rhs is not None else None
     if smoother is not None:
-        attach_smoothers(levels, smoother, omega)
+        attach_smoothers(levels, smoother, omega, prebuilt=early)
     return levels
 
 
@@ -430,7 +436,7 @@ def _rhs(level):
 _BJ_MODES = ("blockjacobi", "bj", "bj-chebyshev", "chebyshev")
 
 
-def attach_smoothers(levels, mode, omega=None):
+def attach_smoothers(levels, mode, omega=None, prebuilt=None):
     """multigrid.py:345-352 on every level but the coarsest.  mode: "baseline" (FSAI on the
     pattern of A), "aggressive" (pattern of A^2), an int power, or "blockjacobi".  omega
     defaults: FSAI 1.0 (reference), block-Jacobi 0.8 (north star)."""
@@ -447,12 +453,18 @@ def attach_smoothers(levels, mode, omega=None):
     if not isinstance(power, int) or isinstance(power, bool) or power < 1:
         raise ValueError(f"unknown smoother mode {mode!r}")
     w = 1.0 if omega is None else float(omega)
+    prebuilt = prebuilt or {}
     for lev in levels[:-1]:
-        if getattr(lev.block_op, "S_cls", True) is None:
+        if id(lev) not in prebuilt and getattr(lev.block_op, "S_cls", True) is None:
             raise HierarchyError("FSAI needs the level's element blocks, released after building a large "
                                  "device-condensed hierarchy: pass smoother=%r to build_hierarchy" % (mode,))
     for lev in levels[:-1]:
-        lev.smoother = fsai_build(lev.operator.tocsr(), power, w).bind(lev.block_op)
+        if id(lev) in prebuilt and prebuilt[id(lev)].omega == w:
+            lev.smoother = prebuilt[id(lev)]
+        elif structured_fsai_supported(lev.block_op, power):
+            lev.smoother = StructuredFSAI(lev.block_op, w)       # device setup (baseline pattern)
+        else:
+            lev.smoother = fsai_build(lev.operator.tocsr(), power, w).bind(lev.block_op)
     return levels
 
 

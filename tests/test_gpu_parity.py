@@ -580,10 +580,11 @@ def test_half_stored_stream_mesh_widths(P, nx, ny, p):
 
 
 def test_fsai_on_large_condensed_hierarchy_keeps_blocks(P, monkeypatch):
-    """Large device-condensed levels drop their element blocks after the hierarchy is built;
-    FSAI smoothers need them (fsai_build reads the level CSR, multigrid.py:123-159): asking for
-    FSAI in build_hierarchy keeps them and matches the oracle, attaching it afterwards to a
-    hierarchy whose blocks were released raises HierarchyError."""
+    """Large device-condensed levels drop their element blocks after the hierarchy is built.
+    The baseline FSAI is set up on the device from each level's blocks while the hierarchy is
+    built (so the blocks can go), the aggressive one builds from the level CSR and keeps them;
+    attaching FSAI afterwards to a hierarchy whose blocks were released raises HierarchyError.
+    Both match the oracle."""
     monkeypatch.setattr(P.tr.TraceSystem, "GPU_CLASSES", 0)
     monkeypatch.setattr(P.mg, "RELEASE_NDOF", 0)
     n, p = 16, 2
@@ -595,7 +596,10 @@ def test_fsai_on_large_condensed_hierarchy_keeps_blocks(P, monkeypatch):
         P.mg.attach_smoothers(bare, "baseline")
     P.mg.attach_smoothers(bare, "blockjacobi")            # block-Jacobi only needs the facet stream
     levels = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother="baseline")
-    assert levels[0].block_op.S_cls is not None
+    assert levels[0].block_op.S_cls is None
+    assert all(isinstance(lev.smoother, P.mg.StructuredFSAI) for lev in levels[:-1])
+    agg = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother="aggressive")
+    assert agg[0].block_op.S_cls is not None
     lo = O.build_levels(O.Grid(n, n), p, O.Spec(O.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0),
                         smoother="baseline")
     b = np.random.default_rng(9).uniform(-1, 1, levels[0].ndof)
@@ -699,3 +703,61 @@ def test_blockjacobi_complexity_matches_oracle(P):
         assert abs(a.smoother.complexity - b.smoother.complexity) < 1e-12
         lay = a.block_op.layout
         assert P.mg.structural_nnz(lay.nx, lay.ny, lay.n1) == a.block_op.tocsr().nnz
+
+
+@pytest.mark.parametrize("case", ["kI", "het", "aniso"])
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+def test_structured_fsai_matches_host_fsai(P, case, p):
+    """The facet-structured device FSAI (one Cholesky per facet, hdg_fsai.cuh) reproduces the
+    host restatement of fsai_build (per-row solves on lower(A), multigrid.py:123-159): same
+    pattern, same values to rounding, same lambda_max (seed-1234 power iteration), and the same
+    smoothing sweeps."""
+    from paper_1705_09907_b200.fsai import StructuredFSAI, fsai_build
+    n = 6 if p == 8 else 8
+    if case == "kI":
+        spec = specs.constant(P.pb.ProblemSpec)
+    elif case == "het":
+        spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(specs.hetero_K(n, seed=7)), specs.zero, specs.zero, 1.0)
+    else:
+        kx, ky = specs.hetero_K(n, seed=8), specs.hetero_K(n, seed=9)
+        spec = P.pb.ProblemSpec(P.pb.piecewise_anisotropic(kx, ky), specs.zero, specs.zero, 1.0)
+    levels = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother=None)
+    for lev in levels[:-1]:
+        A = lev.operator.tocsr()
+        ref = fsai_build(A, 1, 1.0, device=False)
+        sm = StructuredFSAI(lev.block_op, 1.0)
+        G, Gr = sm.G, ref.G
+        assert G.nnz == Gr.nnz
+        assert (abs(G - Gr)).max() <= 1e-11 * abs(Gr).max()
+        assert abs(sm.lam_max - ref.lam_max) <= 1e-10 * ref.lam_max
+        assert abs(sm.complexity - ref.complexity) < 1e-12
+        b = np.random.default_rng(1).uniform(-1, 1, lev.ndof)
+        x0 = np.random.default_rng(2).uniform(-1, 1, lev.ndof)
+        x = sm.smooth(None, b, x0, 3)
+        xr = x0.copy()
+        for w in ref.sweep_weights(3):
+            xr = xr + w * (ref.Gt @ (ref.G @ (b - A @ xr)))
+        assert rel(x, xr) < 1e-11
+
+
+def test_structured_fsai_released_blocks_hierarchy(P, monkeypatch):
+    """build_hierarchy(smoother="baseline") on a device-condensed heterogeneous hierarchy whose
+    large levels release their element blocks: every level gets its device FSAI before the
+    release, and the V-cycle / MG-PCG agree with the oracle's FSAI hierarchy."""
+    import paper_1705_09907_b200.multigrid as mgm
+    monkeypatch.setattr(mgm, "RELEASE_NDOF", 100)
+    monkeypatch.setattr(P.tr.TraceSystem, "GPU_CLASSES", 0)
+    n, p = 16, 3
+    Kg = specs.hetero_K(n, seed=11)
+    spec = P.pb.ProblemSpec(P.pb.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0)
+    levels = P.mg.build_hierarchy(P.mesh(n, n), p, spec, smoother="baseline")
+    assert all(isinstance(lev.smoother, mgm.StructuredFSAI) for lev in levels[:-1])
+    lo = O.build_levels(O.Grid(n, n), p, O.Spec(O.piecewise_coefficient(Kg), specs.zero, specs.zero, 1.0),
+                        smoother="baseline")
+    b = np.random.default_rng(3).uniform(-1, 1, levels[0].ndof)
+    assert rel(P.mg.v_cycle(levels, b), O.v_cycle(lo, b)) < 1e-10
+    assert levels[0].block_op.S_cls is None                       # released after its FSAI was built
+    x, it = levels[0].system.solve_cg(tol=1e-10, precond=P.mg.mg_preconditioner(levels), b=b)
+    xo, ito = lo[0].system.solve_cg(b=b, tol=1e-10, precond=O.mg_preconditioner(lo))
+    assert it == ito
+    assert rel(x, xo) < 1e-9
