@@ -387,8 +387,9 @@ class OracleTrace:
             return np.zeros(0)
         return spla.splu(self.csr().tocsc()).solve(b)
 
-    def solve_cg(self, b=None, tol=1e-12, maxiter=5000, precond=None, x0=None):
-        """trace.py:142-163 - (preconditioned) CG; returns (x, iterations)."""
+    def solve_cg(self, b=None, tol=1e-12, maxiter=5000, precond=None, x0=None, hist=None):
+        """trace.py:142-163 - (preconditioned) CG; returns (x, iterations).  `hist` (a list, test
+        instrumentation only) receives ||r|| at every stop test."""
         b = self.rhs if b is None else b
         x = np.zeros_like(b) if x0 is None else x0.copy()
         r = b - self.matvec(x)
@@ -397,7 +398,10 @@ class OracleTrace:
         rz = r @ z
         bn = np.linalg.norm(b) or 1.0
         for it in range(maxiter):
-            if np.linalg.norm(r) <= tol * bn:
+            rn = np.linalg.norm(r)
+            if hist is not None:
+                hist.append(rn)
+            if rn <= tol * bn:
                 return x, it
             ad = self.matvec(d)
             a = rz / (d @ ad)

@@ -193,6 +193,8 @@ class StructuredFSAI(FSAISmoother):
         v0 = torch.from_numpy(np.random.default_rng(seed).standard_normal(n)).cuda() if n else None
         lam = ctypes.c_double(1.0)
         bad = ctypes.c_int64(-1)
+        import time
+        t0 = time.perf_counter()
         rc = lib.hdg_level_set_fsai_struct(block_op.handle, S.data_ptr(), cls.data_ptr(),
                                            v0.data_ptr() if v0 is not None else None, self.LAM_ITERS,
                                            self.cheb_fraction, self.omega, ctypes.byref(lam), ctypes.byref(bad),
@@ -201,6 +203,7 @@ class StructuredFSAI(FSAISmoother):
             raise NotSPDError(f"non-SPD principal submatrix in FSAI row {bad.value}")
         check(rc)
         self.lam_max = float(lam.value)
+        self.setup_s = time.perf_counter() - t0        # factor + lambda_max (the call synchronises)
 
     def bind(self, block_op):
         if block_op is not self.block_op:

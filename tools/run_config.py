@@ -30,17 +30,21 @@ def main():
     ap.add_argument("--p", type=int, default=8)
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--maxiter", type=int, default=500)
-    ap.add_argument("--smoother", default="blockjacobi")
+    ap.add_argument("--smoother", default="baseline", help="baseline (the reference FSAI, device setup) | blockjacobi")
+    ap.add_argument("--nu", type=int, default=2, help="pre- and post-smoothing sweeps")
+    ap.add_argument("--hist", default=None, help="write the PCG residual history here")
     a = ap.parse_args()
     rng = np.random.default_rng(2)
     Kg = np.exp(rng.uniform(np.log(1e-2), np.log(1e2), (a.n, a.n)))
     spec = ProblemSpec(piecewise_coefficient(Kg), zero, zero, 1.0)
     t0 = time.time()
-    levels = build_hierarchy(build_cartesian(a.n, a.n), a.p, spec, smoother=None)
-    attach_smoothers(levels, a.smoother)
+    # the smoother is attached while the hierarchy is built: the device FSAI of each level is set
+    # up from its element blocks before the large levels release them
+    levels = build_hierarchy(build_cartesian(a.n, a.n), a.p, spec, smoother=a.smoother)
     mg = _native_mg(levels)
     torch.cuda.synchronize()
     t_setup = time.time() - t0
+    fsai_s = sum(getattr(lev.smoother, "setup_s", 0.0) for lev in levels[:-1])
     ndof = levels[0].ndof
     b = torch.from_numpy(rng.uniform(-1.0, 1.0, ndof)).cuda()
     free, total = torch.cuda.mem_get_info()
@@ -48,13 +52,13 @@ def main():
     x = torch.zeros_like(b)
     st = torch.cuda.current_stream()
     for _ in range(2):
-        _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), 0, x.data_ptr(), 2, 2, 1, 1, st.cuda_stream))
+        _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), 0, x.data_ptr(), a.nu, a.nu, 1, 1, st.cuda_stream))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     R = 5
     e0.record(st)
     for _ in range(R):
-        _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), 0, x.data_ptr(), 2, 2, 1, 1, st.cuda_stream))
+        _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), 0, x.data_ptr(), a.nu, a.nu, 1, 1, st.cuda_stream))
     e1.record(st)
     torch.cuda.synchronize()
     vms = e0.elapsed_time(e1) / R
@@ -62,15 +66,21 @@ def main():
     from paper_1705_09907_b200.multigrid import mg_preconditioner
     torch.cuda.synchronize()
     t1 = time.time()
-    xs, iters = levels[0].system.solve_cg(tol=a.tol, maxiter=a.maxiter, precond=mg_preconditioner(levels), b=b)
+    xs, iters = levels[0].system.solve_cg(tol=a.tol, maxiter=a.maxiter, precond=mg_preconditioner(levels, a.nu, a.nu), b=b)
     torch.cuda.synchronize()
     t_solve = time.time() - t1
     r = b - levels[0].matvec(xs)
     relres = float(torch.linalg.vector_norm(r) / torch.linalg.vector_norm(b))
-    print(json.dumps({"config": f"{a.n}^2 p={a.p} heterogeneous K log-U[1e-2,1e2] seed 2, MG-PCG ({a.smoother} V(2,2))",
+    hist = getattr(levels[0].system, "cg_residuals", None)
+    if a.hist and hist is not None:
+        np.savetxt(a.hist, np.asarray(hist) / float(torch.linalg.vector_norm(b)), header="||r_k|| / ||b||, k = 0..iters")
+    print(json.dumps({"config": f"{a.n}^2 p={a.p} heterogeneous K log-U[1e-2,1e2] seed 2, MG-PCG ({a.smoother} V({a.nu},{a.nu}))",
                       "ndof": ndof, "levels": len(levels), "setup_s": round(t_setup, 2),
+                      "fsai_setup_s": round(fsai_s, 2),
                       "vcycle_ms": round(vms, 3), "pcg_iterations": iters, "solve_s": round(t_solve, 3),
-                      "final_rel_residual": relres, "gpu_mem_used_GB": round((total - free) / 1e9, 1)}))
+                      "final_rel_residual": relres, "gpu_mem_used_GB": round((total - free) / 1e9, 1),
+                      "torch_reserved_GB": round(torch.cuda.memory_reserved() / 1e9, 1),
+                      "operator_stream_GB": round(sum(lev.block_op.operator_bytes() for lev in levels) / 1e9, 1)}))
 
 
 if __name__ == "__main__":
