@@ -53,6 +53,14 @@ int hdg_level_create_shared(int nx, int ny, int p, const double* block, hdg_leve
  * ownership; it may be freed after the call).  Dirichlet columns must already
  * be zero (local.py:186-188); boundary-side rows are ignored. */
 int hdg_level_create_stored(int nx, int ny, int p, const double* blocks, hdg_level** out);
+/* The same stored operator filled by element-row chunks, for levels whose element blocks cannot
+ * exist at once (configs[4]'s 8192^2 p=4 fine level: 214.7 GB of blocks, 107 GB of stream).
+ * create_stored_empty allocates the stream; fill_stored_rows writes stream rows
+ * [row0, row0 + nrows) from `blocks` = the element blocks of element rows
+ * [max(row0 - 1, 0), row0 + nrows) (DEVICE, same layout as hdg_level_create_stored).  Every row
+ * must be filled once before the level is applied. */
+int hdg_level_create_stored_empty(int nx, int ny, int p, hdg_level** out);
+int hdg_level_fill_stored_rows(hdg_level* lev, int row0, int nrows, const double* blocks, void* stream);
 int hdg_level_destroy(hdg_level* lev);
 int64_t hdg_level_ndof(const hdg_level* lev);
 /* bytes the operator streams from HBM per apply (0 for shared: held in constant bank) */

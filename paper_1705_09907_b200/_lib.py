@@ -25,6 +25,8 @@ SIGNATURES = [
     ("hdg_launch_count", c_int64, []),
     ("hdg_level_create_shared", c_int, [c_int, c_int, c_int, c_void_p, ctypes.POINTER(c_void_p)]),
     ("hdg_level_create_stored", c_int, [c_int, c_int, c_int, c_void_p, ctypes.POINTER(c_void_p)]),
+    ("hdg_level_create_stored_empty", c_int, [c_int, c_int, c_int, ctypes.POINTER(c_void_p)]),
+    ("hdg_level_fill_stored_rows", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
     ("hdg_level_destroy", c_int, [c_void_p]),
     ("hdg_level_ndof", c_int64, [c_void_p]),
     ("hdg_level_operator_bytes", c_int64, [c_void_p]),

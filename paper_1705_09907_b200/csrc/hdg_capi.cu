@@ -443,6 +443,78 @@ static int create_stored(int nx, int ny, int p, const double* blocks, bool bcast
   return 0;
 }
 
+// --------------------------------------------------------- stored levels filled by row chunks
+// A level whose element blocks never exist at once (configs[4]: 214.7 GB of blocks for a 107 GB
+// half-stored stream): the stream is allocated empty and filled chunk by chunk.
+
+int hdg_level_create_stored_empty(int nx, int ny, int p, hdg_level** out) {
+  if (!out) return fail(HDG_EINVAL, "null argument");
+  hdg_level* L = new hdg_level();
+  L->stored = true;
+  int rc = init_level(L, nx, ny, p);
+  if (rc) { delete L; return rc; }
+  const int n1 = L->n1;
+  const long long nslots = (long long)ny * L->nxp;
+  const size_t wbytes = sizeof(double) * (size_t)nslots * (HDG_SYMSTORE ? 4 : 7) * n1 * n1;
+  L->op_bytes = 0;
+  if (L->ndof > 0) {
+    if (cudaMalloc(&L->dWh, wbytes) != cudaSuccess || cudaMalloc(&L->dWv, wbytes) != cudaSuccess) {
+      hdg_level_destroy(L);
+      return fail(HDG_ENOMEM, "cannot allocate stored operator streams");
+    }
+    CK(cudaMemset(L->dWh, 0, wbytes));
+    CK(cudaMemset(L->dWv, 0, wbytes));
+    L->op_bytes = (long long)L->n_blocks * (HDG_SYMSTORE ? 4 : 7) * n1 * n1 * 8;
+  }
+  if ((rc = prepare(n1, true))) { hdg_level_destroy(L); return rc; }
+  *out = L;
+  return 0;
+}
+
+int hdg_level_fill_stored_rows(hdg_level* L, int row0, int nrows, const double* blocks, void* stream) {
+  if (!L || !L->stored) return fail(HDG_EINVAL, "need a stored level");
+  if (row0 < 0 || nrows < 1 || row0 + nrows > L->ny) return fail(HDG_EINVAL, "row chunk outside the mesh");
+  if (L->ndof == 0) return 0;
+  if (!blocks) return fail(HDG_EINVAL, "null blocks");
+  const int n1 = L->n1, nx = L->nx;
+  const int erow0 = row0 > 0 ? row0 - 1 : 0;
+  const long long E = (long long)(row0 + nrows - erow0) * nx;
+  cudaStream_t s = S(stream);
+  if (HDG_SYMSTORE) {
+    unsigned long long* dchk = nullptr;
+    CK(cudaMallocAsync((void**)&dchk, 2 * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(dchk, 0, 2 * sizeof(unsigned long long), s));
+    const long long tot = E * 16 * n1 * n1;
+#define ASYMC_CASE(N) { block_asym_kernel<N><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(blocks, E, dchk); CKL(); break; }
+    HDG_N1_SWITCH(n1, ASYMC_CASE)
+#undef ASYMC_CASE
+    unsigned long long hchk[2];
+    CK(cudaMemcpyAsync(hchk, dchk, sizeof(hchk), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFreeAsync(dchk, s);
+    double asym, mag;
+    std::memcpy(&asym, &hchk[0], sizeof(double));
+    std::memcpy(&mag, &hchk[1], sizeof(double));
+    if (!(asym <= 1e-10 * mag)) return fail(HDG_EINVAL, "stored element blocks are not symmetric");
+  }
+  const long long nthr = (long long)nrows * L->nxp * (HDG_SYMSTORE ? 4 : 7) * n1 * n1;
+  const int bs = 256;
+  const long long nbk = (nthr + bs - 1) / bs;
+#define RELAYC_CASE(N)                                                                                        \
+  {                                                                                                           \
+    relayout_kernel<N><<<(unsigned)nbk, bs, 0, s>>>(blocks, nx, L->ny, L->nxp, false, L->dWh, false, row0,   \
+                                                    row0 + nrows, erow0);                                     \
+    CKL();                                                                                                    \
+    relayout_kernel<N><<<(unsigned)nbk, bs, 0, s>>>(blocks, nx, L->ny, L->nxp, true, L->dWv, false, row0,    \
+                                                    row0 + nrows, erow0);                                     \
+    CKL();                                                                                                    \
+    break;                                                                                                    \
+  }
+  HDG_N1_SWITCH(n1, RELAYC_CASE)
+#undef RELAYC_CASE
+  return 0;
+}
+
 int hdg_level_destroy(hdg_level* L) {
   if (!L) return 0;
   cudaFree(L->dWh); cudaFree(L->dWv); cudaFree(L->dDh); cudaFree(L->dDv); cudaFree(L->partials);

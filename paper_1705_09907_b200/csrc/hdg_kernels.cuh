@@ -1104,25 +1104,30 @@ __host__ __device__ inline void merged_entry_src(bool vert, int q, int k, int m,
   }
 }
 
+// Slot rows [j0, j1) of the stream (all rows: j0 = 0, j1 = ny).  S holds the element blocks of
+// element rows [erow0, ...): a slot row j needs element rows j - 1 (horizontal facet below) and j,
+// so a chunk of slot rows [j0, j1) is complete given element rows [max(j0 - 1, 0), j1).
 template <int N1>
 __global__ void relayout_kernel(const double* __restrict__ S, int nx, int ny, int nxp, bool vert,
-                                double* __restrict__ W, bool bcast = false) {
+                                double* __restrict__ W, bool bcast = false, int j0 = 0, int j1 = -1,
+                                int erow0 = 0) {
   using C = Cfg<N1>;
-  const long long nslots = (long long)ny * nxp;
+  if (j1 < 0) j1 = ny;
+  const long long nslots = (long long)(j1 - j0) * nxp;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= nslots * C::WSZ) return;
   // thread -> (group, entry, lane): consecutive threads write consecutive addresses
   const int lane = tid & 31;
   const long long rest = tid >> 5;
   const int idx = (int)(rest % C::WSZ);
-  const long long grp = rest / C::WSZ;
+  const long long grp = rest / C::WSZ + (long long)j0 * nxp / 32;   // nxp is a multiple of 32
   const long long slot = grp * 32 + lane;
   const int j = (int)(slot / nxp), i = (int)(slot % nxp);
   const bool valid = vert ? (i >= 1 && i <= nx - 1 && j < ny) : (i < nx && j >= 1 && j <= ny - 1);
   long long e1 = 0, e2 = 0;
   if (valid) {
-    e1 = vert ? ((long long)j * nx + (i - 1)) : ((long long)(j - 1) * nx + i);
-    e2 = (long long)j * nx + i;
+    e1 = vert ? ((long long)(j - erow0) * nx + (i - 1)) : ((long long)(j - 1 - erow0) * nx + i);
+    e2 = (long long)(j - erow0) * nx + i;
     if (bcast) e1 = e2 = 0;   // one block for every element (asymmetric constant operator)
   }
   const int L = 4 * N1;

@@ -387,6 +387,22 @@ def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother
         if not keep_blocks and not isinstance(prev.S_cls, np.ndarray) and prev.ndof > RELEASE_NDOF:
             prev.release_blocks()
 
+    _extend_levels(levels, op, mesh, p, spec, tau_per_facet, retire)
+    levels[-1].kind = "coarsest"
+    if levels[-1].ndof > coarse_cap:                                  # :336-339
+        raise HierarchyError(f"coarsest level has {levels[-1].ndof} unknowns, above cap {coarse_cap}")
+    for k in range(1, len(levels)):                                   # :333 rhs_k = P^T rhs_{k-1}
+        prev = levels[k - 1]
+        levels[k].rhs = _LazyRhs(prev, k) if prev.rhs is not None else None
+    if smoother is not None:
+        attach_smoothers(levels, smoother, omega, prebuilt=early)
+    return levels
+
+
+def _extend_levels(levels, op, mesh, p, spec, tau_per_facet, retire=None):
+    """Append the coarse levels below (mesh, p, op): orders p-1..1 on the same mesh, then mesh
+    halving at p = 1 (multigrid.py:317-327), Galerkin operators in element form."""
+    retire = retire or (lambda prev, lev: None)
     for q in range(p - 1, 0, -1):                                   # multigrid.py:317-321
         V = p_transfer_matrix(q + 1)
         cop = BlockOperator(mesh, q, galerkin_p(op.S_cls, V), op.elem_class)
@@ -405,14 +421,30 @@ def build_hierarchy(mesh, p, spec, tau_per_facet=None, coarse_cap=4096, smoother
                               operator=DeviceOperator(cop), matrix_free=False))
         retire(op, levels[-2])
         op = cop
+    return levels
+
+
+def level_schedule(nx, ny, p):
+    """(nx, ny, p) of every level build_hierarchy makes (multigrid.py:317-327), fine first."""
+    out = [(nx, ny, q) for q in range(p, 0, -1)]
+    while nx % 2 == 0 and ny % 2 == 0 and nx >= 4 and ny >= 4:
+        nx, ny = nx // 2, ny // 2
+        out.append((nx, ny, 1))
+    return out
+
+
+def hierarchy_from_operator(mesh, p, op, spec, tau_per_facet=None, coarse_cap=4096, smoother="blockjacobi",
+                            omega=None):
+    """The hierarchy below an already-built level operator `op` on (mesh, p): the replicated coarse
+    tail of a strip-partitioned hierarchy starts from an agglomerated level (distributed.py)."""
+    levels = [MGLevel(mesh, p, _LevelSystem(mesh, p, op), kind="p-level" if p > 1 else "h-level",
+                      operator=DeviceOperator(op), matrix_free=False)]
+    _extend_levels(levels, op, mesh, p, spec, tau_per_facet)
     levels[-1].kind = "coarsest"
-    if levels[-1].ndof > coarse_cap:                                  # :336-339
+    if levels[-1].ndof > coarse_cap:
         raise HierarchyError(f"coarsest level has {levels[-1].ndof} unknowns, above cap {coarse_cap}")
-    for k in range(1, len(levels)):                                   # :333 rhs_k = P^T rhs_{k-1}
-        prev = levels[k - 1]
-        levels[k].rhs = _LazyRhs(prev, k) if prev.rhs is not None else None
-    if smoother is not None:
-        attach_smoothers(levels, smoother, omega, prebuilt=early)
+    if smoother is not None and len(levels) > 1:
+        attach_smoothers(levels, smoother, omega)
     return levels
 
 

@@ -226,13 +226,82 @@ class BlockOperator:
         return sp.coo_matrix((S[m], (rr[m], cc[m])), shape=(lay.ndof, lay.ndof)).tocsr()
 
 
+def element_blocks_device(op):
+    """(E, 4n1, 4n1) CUDA tensor of a BlockOperator's per-element blocks (classes expanded)."""
+    import torch
+    S = op.S_cls if isinstance(op.S_cls, torch.Tensor) else torch.from_numpy(op.S_cls)
+    S = S.to(device="cuda", dtype=torch.float64)
+    E = op.elem_class.size
+    if S.shape[0] == E and np.array_equal(op.elem_class, np.arange(E)):
+        return S.contiguous()
+    return S.index_select(0, torch.from_numpy(op.elem_class).cuda()).contiguous()
+
+
+class RowChunkedOperator:
+    """The stored trace operator of (mesh, p, spec) condensed and streamed chunk by chunk of
+    element rows (hdg_level_create_stored_empty / hdg_level_fill_stored_rows): the element blocks
+    of the whole mesh never exist at once.  configs[4]'s 8192^2 p=4 fine level on one GPU: 214.7 GB
+    of blocks, 107 GB of half-stored stream.  Offers the BlockOperator apply interface."""
+
+    def __init__(self, mesh, p, spec, rows_per_chunk=256, tau_per_facet=None):
+        import torch
+        from .mesh import Mesh
+        dev.require_cuda()
+        self.mesh, self.p = mesh, p
+        self.layout = TraceLayout(mesh, p)
+        self.S_cls = None
+        h = ctypes.c_void_p()
+        nx, ny = mesh.n_x, mesh.n_y
+        check(lib.hdg_level_create_stored_empty(nx, ny, p, ctypes.byref(h)))
+        self._handle = h
+        for a in range(0, ny, rows_per_chunk):
+            b = min(ny, a + rows_per_chunk)
+            ea = max(a - 1, 0)
+            win = Mesh(nx, b - ea, mesh.x0, mesh.y0 + ea * mesh.dy, mesh.dx, mesh.dy)
+            tau = None
+            if tau_per_facet is not None:
+                raise NotImplementedError("row-chunked build with per-facet tau")
+            ts = TraceSystem(win, p, spec, tau, with_rhs=False)
+            blocks = element_blocks_device(ts.operator)
+            del ts
+            check(lib.hdg_level_fill_stored_rows(h, a, b - a, blocks.data_ptr(), dev.stream()))
+            torch.cuda.synchronize()
+            del blocks
+            torch.cuda.empty_cache()
+
+    @property
+    def handle(self):
+        return self._handle
+
+    @property
+    def ndof(self):
+        return self.layout.ndof
+
+    def operator_bytes(self):
+        return int(lib.hdg_level_operator_bytes(self._handle))
+
+    def apply(self, x):
+        xd, was_np = dev.to_device(x)
+        y = dev.empty(self.ndof)
+        check(lib.hdg_matvec(self._handle, dev.ptr(xd), dev.ptr(y), dev.stream()))
+        return dev.back(y, was_np)
+
+    def __del__(self):
+        try:
+            lib.hdg_level_destroy(self._handle)
+        except Exception:
+            pass
+
+
 class TraceSystem:
     """Condensed HDG system A lam = b on the interior facet skeleton (trace.py:26-69)."""
 
     # more distinct element classes than this are condensed on the GPU (PiecewiseCondenser)
     GPU_CLASSES = 4096
 
-    def __init__(self, mesh, p, spec, tau_per_facet=None, threads=1):
+    def __init__(self, mesh, p, spec, tau_per_facet=None, threads=1, with_rhs=True):
+        """with_rhs=False skips the condensed load (operator-only windows of strip / chunked
+        builds)."""
         self.mesh, self.p, self.spec = mesh, p, spec
         self.ops = LocalOps(mesh, p)
         self.layout = TraceLayout(mesh, p)
@@ -257,7 +326,7 @@ class TraceSystem:
                 self.elem_class = np.arange(E, dtype=np.int64)
                 self.class_K = Ke
                 self.operator = BlockOperator(mesh, p, self.piecewise.blocks(Ke), self.elem_class)
-                self.rhs = self._condensed_rhs(spec)
+                self.rhs = self._condensed_rhs(spec) if with_rhs else None
                 return
             kx = np.repeat(uk[:, :1], nq2, axis=1)
             ky = np.repeat(uk[:, -1:], nq2, axis=1) if aniso else None
@@ -269,7 +338,7 @@ class TraceSystem:
                                       kq_y=rows[:, nq2:nk] if aniso else None)
         self.elem_class = np.asarray(inv).reshape(-1)
         self.operator = BlockOperator(mesh, p, self.classes.S, self.elem_class)
-        self.rhs = self._condensed_rhs(spec)
+        self.rhs = self._condensed_rhs(spec) if with_rhs else None
 
     def _quad_points(self, e0, e1):
         m = self.mesh
