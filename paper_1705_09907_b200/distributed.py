@@ -343,6 +343,41 @@ class DeviceStripBackend:
                 lev.smoother = BlockJacobiSmoother(lev.block_op, self.omega)
         self._zero = {}
 
+    @classmethod
+    def from_local(cls, H, omega=0.8):
+        """The same window kernels on a rank-local hierarchy (LocalStripHierarchy): no global
+        operator is ever built."""
+        import ctypes
+
+        import torch
+        from . import _device as dev
+        from ._lib import check, lib
+        from .multigrid import BlockJacobiSmoother, Prolongation
+        self = cls.__new__(cls)
+        self.torch, self.dev, self.lib, self.check, self.ct = torch, dev, lib, check, ctypes
+        self.levels, self.layouts, self.d, self.omega = None, H.layouts, H.d, float(omega)
+        self.ops, self.links, self.transfers = list(H.ops), list(H.links), []
+        for l in range(H.d + 1):
+            self.ops[l].set_blockjacobi(self.omega)
+        for l in range(H.d + 1):
+            if H.links[l] == "p":
+                self.transfers.append(Prolongation(self.ops[l], self.ops[l + 1], "p", V=H.tspecs[l]))
+            else:
+                halves, cross = H.tspecs[l]
+                hv, cr = np.ascontiguousarray(halves), np.ascontiguousarray(cross)
+                h = ctypes.c_void_p()
+                check(lib.hdg_transfer_create_h_window(self.ops[l].handle, self.ops[l + 1].handle, hv.ctypes.data,
+                                                       cr.ctypes.data, cr.shape[0], H.layouts[l].lo,
+                                                       H.layouts[l + 1].lo, ctypes.byref(h)))
+                t = Prolongation(self.ops[l], self.ops[l + 1], "h", halves=hv, cross=cr)
+                t._handle = h
+                self.transfers.append(t)
+        self.sub = H.sub
+        for lev in self.sub[:-1]:
+            lev.smoother = BlockJacobiSmoother(lev.block_op, self.omega)
+        self._zero = {}
+        return self
+
     def _empty(self, l):
         return self.dev.empty(self.ops[l].ndof)
 
@@ -385,6 +420,13 @@ class DeviceStripBackend:
         return _run_cycle(self.sub, bg, xg, nu1, nu2, visits)
 
 
+def local_strip_multigrid(mesh, p, spec, group=None, omega=0.8, min_rows=4):
+    """StripMG over a rank-local hierarchy (LocalStripHierarchy): each rank condenses and
+    coarsens only its own window.  Returns (mg, H)."""
+    H = LocalStripHierarchy(mesh, p, spec, RowComm(group), min_rows=min_rows)
+    return StripMG(DeviceStripBackend.from_local(H, omega), H.layouts, H.d, group), H
+
+
 def strip_multigrid(levels, world=None, rank=None, group=None, omega=0.8, min_rows=4):
     """StripMG over a hierarchy from build_hierarchy(..., smoother=None): levels whose strips
     keep >= min_rows element rows per rank are distributed, the rest replicated."""
@@ -396,6 +438,257 @@ def strip_multigrid(levels, world=None, rank=None, group=None, omega=0.8, min_ro
     d, rows = plan_strips(shapes, world, min_rows)
     if d < 0:
         raise ValueError("mesh too small to distribute")
+    from .multigrid import HierarchyError
+    for l in range(d + 2):
+        if getattr(levels[l].block_op, "S_cls", True) is None:
+            raise HierarchyError("strip_multigrid slices the global levels' element blocks, released on large "
+                                 "device-condensed hierarchies: use local_strip_multigrid (rank-local build)")
     layouts = [StripLayout(shapes[l][0], shapes[l][1], shapes[l][2], world, rank, rows=rows[l][rank])
                for l in range(d + 2)]
     return StripMG(DeviceStripBackend(levels, layouts, d, omega), layouts, d, group)
+
+
+# ------------------------------------------------------------- rank-local strip hierarchies
+
+
+class RowComm:
+    """Neighbour exchange and all-gather over torch.distributed (NCCL between GPUs, gloo on CPU
+    for the tests).  world 1 without an initialised process group is allowed."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        on = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if on else 1
+        self.rank = dist.get_rank(group) if on else 0
+        self.backend = dist.get_backend(group) if on else None
+        self.device = "cuda" if self.backend == "nccl" else "cpu"
+
+    def _t(self, a):
+        import torch
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        return t.to(device=self.device, dtype=torch.float64).contiguous()
+
+    def sendrecv(self, to_below, to_above, n_below, n_above):
+        """Send flat arrays to rank-1 / rank+1 and receive n_below / n_above values from them
+        (one grouped send/recv)."""
+        import torch
+        dist = self.dist
+        if self.world == 1:
+            return None, None
+        ops, out = [], {}
+        for peer, snd, nrc, key in ((self.rank - 1, to_below, n_below, "below"),
+                                    (self.rank + 1, to_above, n_above, "above")):
+            if not (0 <= peer < self.world):
+                continue
+            if snd is not None and np.prod(snd.shape) > 0:
+                ops.append(dist.P2POp(dist.isend, self._t(snd).reshape(-1), peer, self.group))
+            if nrc:
+                buf = torch.empty(int(nrc), dtype=torch.float64, device=self.device)
+                ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+                out[key] = buf
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return out.get("below"), out.get("above")
+
+    def all_gather(self, a):
+        """list (by rank) of every rank's flat array (lengths may differ)."""
+        import torch
+        t = self._t(a).reshape(-1)
+        if self.world == 1:
+            return [t]
+        dist = self.dist
+        n = torch.tensor([t.numel()], dtype=torch.int64, device=self.device)
+        ns = [torch.zeros_like(n) for _ in range(self.world)]
+        dist.all_gather(ns, n, group=self.group)
+        m = int(max(int(v.item()) for v in ns))
+        pad = torch.zeros(m, dtype=torch.float64, device=self.device)
+        pad[:t.numel()] = t
+        outs = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(outs, pad, group=self.group)
+        return [o[:int(k.item())] for o, k in zip(outs, ns)]
+
+    def all_max(self, v):
+        import torch
+        if self.world == 1:
+            return v
+        t = torch.tensor([float(v)], dtype=torch.float64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def all_sum(self, t):
+        if self.world > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+
+def _window_mesh(gm, lo, nyl):
+    from .mesh import Mesh
+    return Mesh(gm.n_x, nyl, gm.x0, gm.y0 + lo * gm.dy, gm.dx, gm.dy)
+
+
+class _RowsView:
+    """Element rows [a, a + nrows) of a level operator, as _h_level reads it (mesh.n_x, S_cls,
+    elem_class)."""
+
+    def __init__(self, op, a, nrows):
+        from .mesh import Mesh
+        nx = op.mesh.n_x
+        self.mesh = Mesh(nx, nrows, 0.0, 0.0, 1.0, 1.0)
+        self.S_cls = op.S_cls
+        self.elem_class = op.elem_class[a * nx:(a + nrows) * nx]
+
+
+class LocalStripHierarchy:
+    """The strip-partitioned hierarchy built RANK-LOCALLY: no rank ever holds the
+    global operator.  Rank g owns element rows [r0, r1) of every distributed level and keeps the
+    window [r0 - 2, r1 + 1) (StripLayout).  Per level:
+
+      fine level   the window is condensed on its own (TraceSystem on the window mesh: element
+                   blocks depend only on the element's data, local.py:133-237);
+      p-link       Galerkin blocks are element-local (S_c = Q^T S Q, multigrid.py:328-334): the
+                   coarse window is the fine window's rows;
+      h-link       each rank forms the Galerkin blocks of the coarse elements it OWNS (their
+                   children are owned fine rows) and the h-transfer cross maps of its coarse
+                   window (rediscretised coarse K, multigrid.py:269-293, from the coefficient
+                   callable); the three ghost coarse rows come from the neighbours (one grouped
+                   send/recv of element blocks);
+      tail         below the last distributed level d the owned blocks of level d + 1 are
+                   all-gathered and the rest of the hierarchy is built replicated on every rank
+                   (agglomeration).
+
+    `ops[l]` are the window operators (BlockOperator), `links[l]` / `tspecs[l]` the transfer
+    l -> l+1 (("p", V) or ("h", (halves, window cross maps))), `sub` the replicated tail (MGLevel
+    list starting at level d + 1), `layouts` the StripLayouts."""
+
+    def __init__(self, mesh, p, spec, comm=None, tau_per_facet=None, min_rows=4, release_ndof=4_000_000):
+        from .discretization import galerkin_p, h_cross_maps, h_halves, p_transfer_matrix
+        from .multigrid import _coarse_classes, _h_level, hierarchy_from_operator, level_schedule
+        from .trace import BlockOperator, TraceSystem
+        if tau_per_facet is not None:
+            raise NotImplementedError("strip hierarchies with per-facet tau")
+        comm = comm or RowComm()
+        self.comm = comm
+        world, rank = comm.world, comm.rank
+        sched = level_schedule(mesh.n_x, mesh.n_y, p)
+        shapes = [(nx, ny, q, None) for nx, ny, q in sched]
+        d, rows = plan_strips(shapes, world, min_rows)
+        if d < 0:
+            raise ValueError("mesh too small to distribute")
+        self.d, self.sched = d, sched
+        self.layouts = [StripLayout(sched[l][0], sched[l][1], sched[l][2], world, rank, rows=rows[l][rank])
+                        for l in range(d + 2)]
+        # global geometry of every level l <= d + 1
+        gms = [mesh]
+        for l in range(1, d + 2):
+            prev = gms[-1]
+            if sched[l][0] == sched[l - 1][0]:
+                gms.append(prev)
+            else:
+                from .mesh import Mesh
+                gms.append(Mesh(sched[l][0], sched[l][1], prev.x0, prev.y0, 2 * prev.dx, 2 * prev.dy))
+        self.gmeshes = gms
+        L0 = self.layouts[0]
+        op = TraceSystem(_window_mesh(mesh, L0.lo, L0.nyl), p, spec, with_rhs=False).operator
+        self.ops, self.links, self.tspecs = [op], [], []
+        for l in range(d + 1):
+            Lf, Lc = self.layouts[l], self.layouts[l + 1]
+            qf, qc = sched[l][2], sched[l + 1][2]
+            if sched[l + 1][0] == sched[l][0]:                       # p-link (same mesh)
+                assert (Lc.lo, Lc.hi) == (Lf.lo, Lf.hi)
+                V = p_transfer_matrix(qf)
+                cop = BlockOperator(_window_mesh(gms[l + 1], Lc.lo, Lc.nyl), qc, galerkin_p(op.S_cls, V),
+                                    op.elem_class)
+                self.links.append("p")
+                self.tspecs.append(V)
+            else:                                                     # h-link
+                cop, cross = self._h_window(op, Lf, Lc, gms[l + 1], spec, _h_level, _coarse_classes,
+                                            h_cross_maps)
+                self.links.append("h")
+                self.tspecs.append((h_halves(), cross))
+            if op.ndof > release_ndof and not isinstance(op.S_cls, np.ndarray) and l > 0:
+                op.release_blocks()
+            self.ops.append(cop)
+            op = cop
+        # replicated tail: all-gather the owned blocks of level d + 1
+        Lt = self.layouts[d + 1]
+        nxt, qt = sched[d + 1][0], sched[d + 1][2]
+        Lw = 4 * (qt + 1)
+        tail_op = self.ops[d + 1]
+        if self._is_shared(tail_op):
+            S_g, ec_g = np.asarray(self._host(tail_op.S_cls[:1])), np.zeros(nxt * sched[d + 1][1], np.int64)
+        else:
+            a = (Lt.r0 - Lt.lo) * nxt
+            own = self._elem_blocks(tail_op)[a:a + (Lt.r1 - Lt.r0) * nxt]
+            parts = comm.all_gather(own)
+            S_g = np.concatenate([np.asarray(self._host(t)) for t in parts]).reshape(-1, Lw, Lw)
+            ec_g = np.arange(S_g.shape[0], dtype=np.int64)
+        gop = BlockOperator(gms[d + 1], qt, S_g, ec_g)
+        self.sub = hierarchy_from_operator(gms[d + 1], qt, gop, spec, None, smoother=None)
+
+    # -- helpers --------------------------------------------------------------------------------
+    @staticmethod
+    def _host(t):
+        return t if isinstance(t, np.ndarray) else t.detach().cpu().numpy()
+
+    @staticmethod
+    def _is_shared(op):
+        return op.S_cls is not None and op.S_cls.shape[0] == 1
+
+    @staticmethod
+    def _elem_blocks(op):
+        S = op.S_cls
+        if isinstance(S, np.ndarray):
+            return S[op.elem_class]
+        import torch
+        return S.index_select(0, torch.as_tensor(op.elem_class, device=S.device))
+
+    def _h_window(self, op, Lf, Lc, gmc, spec, _h_level, _coarse_classes, h_cross_maps):
+        from .trace import BlockOperator
+        comm = self.comm
+        nxc = gmc.n_x
+        r0c, r1c = Lc.r0, Lc.r1
+        a = 2 * r0c - Lf.lo                                   # first owned fine row, window-local
+        view = _RowsView(op, a, 2 * (r1c - r0c))
+        mco = _window_mesh(gmc, r0c, r1c - r0c)
+        S_c, inv, _, _ = _h_level(view, mco, spec, None)      # Galerkin blocks of the owned coarse rows
+        mcw = _window_mesh(gmc, Lc.lo, Lc.nyl)
+        ucols, ucls = _coarse_classes(mcw, spec, None)        # h-transfer maps of the coarse window
+        cross_u = h_cross_maps(ucols)
+        cross = cross_u if cross_u.shape[0] == 1 else cross_u[ucls]
+        shared = comm.all_max(S_c.shape[0]) == 1 and self._agree(S_c)
+        if shared:
+            return BlockOperator(mcw, 1, S_c, np.zeros(nxc * Lc.nyl, np.int64)), cross
+        owned = S_c[inv] if isinstance(S_c, np.ndarray) else S_c.index_select(
+            0, __import__("torch").as_tensor(inv, device=S_c.device))
+        per_row = nxc * 64
+        nb, na = (r0c - Lc.lo), (Lc.hi - r1c)                # ghost rows below / above
+        to_below = owned[:nxc] if comm.rank > 0 else None                    # my first owned row
+        to_above = owned[-2 * nxc:] if comm.rank < comm.world - 1 else None   # my last two owned rows
+        rb, ra = comm.sendrecv(to_below, to_above, nb * per_row, na * per_row)
+        parts = []
+        tgt = owned
+        as_np = isinstance(tgt, np.ndarray)
+        conv = (lambda t: self._host(t)) if as_np else (lambda t: t.to(tgt.device))
+        if rb is not None:
+            parts.append(conv(rb).reshape(-1, 8, 8))
+        parts.append(tgt)
+        if ra is not None:
+            parts.append(conv(ra).reshape(-1, 8, 8))
+        if as_np:
+            win = np.concatenate(parts)
+        else:
+            import torch
+            win = torch.cat(parts).contiguous()
+        assert win.shape[0] == nxc * Lc.nyl
+        return BlockOperator(mcw, 1, win, np.arange(win.shape[0], dtype=np.int64)), cross
+
+    def _agree(self, S_c):
+        """every rank formed the same single coarse block (constant coefficients)"""
+        if self.comm.world == 1:
+            return True
+        blk = np.asarray(self._host(S_c)).reshape(-1)
+        ref = self.comm.all_gather(blk)
+        r0 = np.asarray(self._host(ref[0]))
+        return all(np.array_equal(np.asarray(self._host(t)), r0) for t in ref)
