@@ -484,6 +484,111 @@ def cpu_baseline(y_gpu, x_host):
             "parity_rel_err_vs_gpu": err}
 
 
+# ------------------------------------------------------------------------ configs[4] runner
+
+C5_N, C5_P = 8192, 4
+
+
+def config5_problem(n):
+    """configs[4]: anisotropic diagonal K per element, Kxx and Kyy log-uniform in [0.1, 10] from
+    default_rng(3); returns (spec, rng positioned for b)."""
+    from paper_1705_09907_b200.problem import ProblemSpec, piecewise_anisotropic
+    rng = np.random.default_rng(3)
+    Kxx = np.exp(rng.uniform(np.log(0.1), np.log(10.0), (n, n)))
+    Kyy = np.exp(rng.uniform(np.log(0.1), np.log(10.0), (n, n)))
+    zero = lambda x, y: np.zeros_like(np.asarray(x, float))
+    return ProblemSpec(piecewise_anisotropic(Kxx, Kyy), zero, zero, 1.0), rng
+
+
+def run_config5(args, rank, ws):
+    """configs[4]: 8192^2, p = 4, anisotropic K, strong scaling over N GPUs.  N = 1: the fine level
+    alone (its element blocks, 214.7 GB, never exist at once: condensed and streamed by row chunks
+    into the 107 GB half-stored stream), matvec only.  N > 1: rank-local strip hierarchies
+    (distributed.LocalStripHierarchy), matvec with NCCL halo rows, V(2,2) block-Jacobi cycle and
+    MG-PCG to 1e-10.  One JSON line (rank 0), the same config dict at every N."""
+    import torch
+    from paper_1705_09907_b200 import _lib
+    from paper_1705_09907_b200.mesh import build_cartesian
+    n, p = args.n5, C5_P
+    spec, rng = config5_problem(n)
+    mesh = build_cartesian(n, n)
+    t0 = time.time()
+    st = torch.cuda.current_stream()
+    cfg = {"workload": f"configs[4]: {n}x{n} quad mesh, p={p}, anisotropic diagonal K log-U[0.1,10] seed 3, fp64; "
+                       "step = one trace matvec", "ndof": 2 * n * (n - 1) * (p + 1),
+           "l2": "inputs larger than L2 (the operator stream alone is 107 GB at 8192^2)",
+           "parallelism": f"strips{ws} (rank-local windows, NCCL halo rows)" if ws > 1 else "single (matvec only)"}
+    line = {"metric": METRIC, "unit": UNIT, "n_gpus": ws, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg}
+    if ws == 1:
+        from paper_1705_09907_b200.trace import RowChunkedOperator
+        op = RowChunkedOperator(mesh, p, spec, rows_per_chunk=args.chunk_rows)
+        torch.cuda.synchronize()
+        setup_s = time.time() - t0
+        ndof = op.ndof
+        xs = [torch.from_numpy(rng.uniform(-1.0, 1.0, ndof)).cuda(), torch.rand(ndof, dtype=torch.float64, device="cuda")]
+        ys = [torch.empty_like(xs[0]) for _ in range(2)]
+        h = op.handle
+        for k in range(args.warmup):
+            _lib.check(_lib.lib.hdg_matvec(h, xs[k % 2].data_ptr(), ys[k % 2].data_ptr(), st.cuda_stream))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(0) as clk:
+            e0.record(st)
+            for k in range(args.steps):
+                _lib.check(_lib.lib.hdg_matvec(h, xs[k % 2].data_ptr(), ys[k % 2].data_ptr(), st.cuda_stream))
+            e1.record(st)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        hbm, kind = peaks()
+        alg = op.operator_bytes() + 16 * ndof
+        line.update({"value": ndof / (ms * 1e-3) / 1e9, "steps": args.steps, "warmup": args.warmup,
+                     "ms_per_step": ms, "setup_s": round(setup_s, 1),
+                     "roofline": {"bound": "hbm", "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                                  "frac": alg / (ms * 1e-3) / 1e9 / hbm, "traffic": None, "peak_kind": kind,
+                                  "kernel": "trace_apply_kernel<5, stored, EPI_Y> (half-stored facet stream)",
+                                  "alg_bytes_per_launch": alg},
+                     "clocks": clk.summary()})
+        print(json.dumps(line), flush=True)
+        return
+    from paper_1705_09907_b200.distributed import StripOperator, local_strip_multigrid
+    mg, H = local_strip_multigrid(mesh, p, spec, omega=0.8)
+    torch.cuda.synchronize()
+    setup_s = barrier_max(time.time() - t0, ws)
+    L0 = H.layouts[0]
+    ndof = L0.ndof_g
+    bg = rng.uniform(-1.0, 1.0, ndof)
+    b = torch.from_numpy(bg[L0.local_to_global]).cuda()
+    op = H.ops[0]
+    sop = StripOperator(L0, op.apply)
+    for _ in range(args.warmup):
+        sop.apply(b)
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        sop.apply(b)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = barrier_max(e0.elapsed_time(e1) / args.steps, ws)
+    # V(2,2) cycle and MG-PCG over the strips
+    for _ in range(2):
+        mg.v_cycle(b)
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    e0.record(st)
+    for _ in range(3):
+        mg.v_cycle(b)
+    e1.record(st)
+    torch.cuda.synchronize()
+    vms = barrier_max(e0.elapsed_time(e1) / 3, ws)
+    line.update({"value": ndof / (ms * 1e-3) / 1e9, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                 "setup_s": round(setup_s, 1), "vcycle_ms": vms, "distributed_levels": H.d + 1})
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -492,13 +597,20 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-vcycle", action="store_true")
+    ap.add_argument("--config", type=int, default=1, choices=[1, 4],
+                    help="BASELINE configs index: 1 = matvec throughput (default), 4 = multi-GPU anisotropic")
+    ap.add_argument("--n5", type=int, default=C5_N, help="configs[4] mesh size (reduced runs)")
+    ap.add_argument("--chunk-rows", type=int, default=256, help="configs[4] N=1: element rows per chunk")
     args = ap.parse_args()
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         run_reference(args, rank, int(os.environ.get("WORLD_SIZE", "1")))
         return
     rank, ws, _ = dist_init(args.gpus)
-    run_ours(args, rank, ws)
+    if args.config == 4:
+        run_config5(args, rank, ws)
+    else:
+        run_ours(args, rank, ws)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

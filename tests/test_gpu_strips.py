@@ -83,3 +83,41 @@ def test_strip_mg_world1_matches_oracle_cycle(P, visits):
     out = np.empty_like(ref)
     out[glob] = _np(x)[loc]
     assert rel(out, ref) < TOL
+
+
+@pytest.mark.parametrize("case", ["aniso", "kI"])
+def test_local_strip_hierarchy_world1_device(P, case):
+    """The rank-local strip hierarchy (distributed.LocalStripHierarchy) with its device window
+    kernels (DeviceStripBackend.from_local) at world 1: the strip V-cycle equals the oracle's
+    global V-cycle (configs[4] coefficient law at reduced size, and K = I)."""
+    import torch
+    from paper_1705_09907_b200.distributed import local_strip_multigrid
+    from test_local_strips_cpu import _specs
+    n, p = 32, 3
+    spec, ospec = _specs(case, n)
+    mg, H = local_strip_multigrid(P.mesh(n, n), p, spec)
+    olevels = O.build_levels(O.Grid(n, n), p, ospec, smoother="blockjacobi")
+    b = np.random.default_rng(7).uniform(-1, 1, olevels[0].ndof)
+    x = mg.v_cycle(torch.from_numpy(b[H.layouts[0].local_to_global].copy()).cuda(), None, 2, 2, 1)
+    ref = O.cycle(olevels, 0, b, np.zeros_like(b), 2, 2, 1)
+    loc, glob = H.layouts[0].owned_pairs()
+    out = np.empty_like(ref)
+    out[glob] = _np(x)[loc]
+    assert rel(out, ref) < TOL
+
+
+def test_row_chunked_operator_matches_whole(P):
+    """RowChunkedOperator (element blocks condensed and streamed by row chunks,
+    hdg_level_fill_stored_rows) applies exactly the operator of the whole-mesh build, on the
+    configs[4] coefficient law; chunk boundaries at every row parity."""
+    from paper_1705_09907_b200.trace import RowChunkedOperator
+    from test_local_strips_cpu import _specs
+    n, p = 24, 4
+    spec, ospec = _specs("aniso", n)
+    x = np.random.default_rng(8).uniform(-1, 1, 2 * n * (n - 1) * (p + 1))
+    whole = P.tr.TraceSystem(P.mesh(n, n), p, spec).matvec_free(x)
+    for rows in (1, 5, 8, 24):
+        got = RowChunkedOperator(P.mesh(n, n), p, spec, rows_per_chunk=rows).apply(x)
+        assert rel(got, whole) < 1e-14, rows
+    o = O.OracleTrace(O.Grid(n, n), p, ospec)
+    assert rel(whole, o.matvec(x)) < TOL
