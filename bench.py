@@ -250,7 +250,7 @@ def run_ours(args, rank, ws):
         xs = [op.to_planes(x) for x in xs]
         ys = [torch.empty_like(xs[0]) for _ in range(NB)]
         apply_fn, kname = lib.hdg_matvec_soa, "soa_apply_kernel<5> (facet records)"
-        ncu_keys = "ncu_soa_apply_p4_r01_key_metrics.txt"
+        ncu_keys = "ncu_soa_apply_p4_r02_key_metrics.txt"
     else:
         apply_fn, kname = lib.hdg_matvec, "trace_apply_kernel<5,shared,EPI_Y>"
         ncu_keys = "ncu_trace_apply_p4_r01_key_metrics.txt"
@@ -376,7 +376,9 @@ def run_ours(args, rank, ws):
                             "; steps pipelined over 3 streams (copies of neighbouring steps overlap the applies)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": ncu_traffic(ncu_keys),
-                         "traffic_source": "profiles/" + ncu_keys + " (ncu --set full)",
+                         "traffic_source": "profiles/" + ncu_keys + (" (steady state: ncu --cache-control none, "
+                                                                     "6 consecutive launches)" if records else
+                                                                     " (ncu --set full)"),
                          "peak_kind": kind,
                          "kernel": kname, "alg_bytes_per_launch": alg_bytes,
                          "ref_layout_kernel_us": ref_layout_us,
