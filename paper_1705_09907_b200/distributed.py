@@ -216,33 +216,48 @@ class StripMG:
         self.ops = [StripOperator(L, None, group) for L in layouts]
         self.torch, self.dist, self.group = torch, dist, group
 
+    def _gather_plan(self, l, device):
+        """Static agglomeration plan of level l (sizes and global indices of every rank's owned
+        values): exchanged once, so a cycle costs ONE all_gather of values and no host sync."""
+        key = (l, str(device))
+        if not hasattr(self, "_plans"):
+            self._plans = {}
+        if key not in self._plans:
+            torch, dist = self.torch, self.dist
+            L = self.layouts[l]
+            loc, glob = L.owned_pairs()
+            plan = {"loc": torch.as_tensor(loc, device=device)}
+            if L.world == 1:
+                plan["glob"] = torch.as_tensor(glob, device=device)
+            else:
+                n = torch.tensor([loc.size], device=device)
+                sizes = [torch.zeros_like(n) for _ in range(L.world)]
+                dist.all_gather(sizes, n, group=self.group)
+                m = int(max(int(s.item()) for s in sizes))
+                pi = torch.full((m,), -1, dtype=torch.int64, device=device)
+                pi[:glob.size] = torch.as_tensor(glob, device=device)
+                alli = [torch.empty_like(pi) for _ in range(L.world)]
+                dist.all_gather(alli, pi, group=self.group)
+                gi = torch.cat(alli)
+                plan.update(m=m, keep=gi >= 0, glob=gi[gi >= 0])
+            self._plans[key] = plan
+        return self._plans[key]
+
     def _gather_owned(self, l, v):
         """assemble the global vector of level l from every rank's owned values"""
         torch, dist = self.torch, self.dist
         L = self.layouts[l]
-        loc, glob = L.owned_pairs()
-        vals = v[torch.as_tensor(loc, device=v.device)]
-        idx = torch.as_tensor(glob, device=v.device)
-        if L.world == 1:
-            out = torch.zeros(L.ndof_g, dtype=v.dtype, device=v.device)
-            out[idx] = vals
-            return out
-        n = torch.tensor([vals.numel()], device=v.device)
-        sizes = [torch.zeros_like(n) for _ in range(L.world)]
-        dist.all_gather(sizes, n, group=self.group)
-        m = int(max(s.item() for s in sizes))
-        pv = torch.zeros(m, dtype=v.dtype, device=v.device)
-        pi = torch.full((m,), -1, dtype=torch.int64, device=v.device)
-        pv[:vals.numel()] = vals
-        pi[:idx.numel()] = idx
-        allv = [torch.empty_like(pv) for _ in range(L.world)]
-        alli = [torch.empty_like(pi) for _ in range(L.world)]
-        dist.all_gather(allv, pv, group=self.group)
-        dist.all_gather(alli, pi, group=self.group)
+        plan = self._gather_plan(l, v.device)
+        vals = v[plan["loc"]]
         out = torch.zeros(L.ndof_g, dtype=v.dtype, device=v.device)
-        for vv, ii in zip(allv, alli):
-            k = ii >= 0
-            out[ii[k]] = vv[k]
+        if L.world == 1:
+            out[plan["glob"]] = vals
+            return out
+        pv = torch.zeros(plan["m"], dtype=v.dtype, device=v.device)
+        pv[:vals.numel()] = vals
+        allv = [torch.empty_like(pv) for _ in range(L.world)]
+        dist.all_gather(allv, pv, group=self.group)
+        out[plan["glob"]] = torch.cat(allv)[plan["keep"]]
         return out
 
     def cycle(self, l, b, x, zero_init, nu1, nu2, visits):

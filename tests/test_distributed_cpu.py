@@ -47,6 +47,9 @@ def _worker(rank, world, port, nx, ny, p, kind, out):
     import torch.distributed as dist
     from paper_1705_09907_b200.distributed import StripLayout, StripOperator
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    from threadpoolctl import threadpool_limits
+    lim = threadpool_limits(1)  # noqa: F841  (world processes share the host: no BLAS oversubscription)
+    torch.set_num_threads(1)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         L = StripLayout(nx, ny, p, world, rank)
