@@ -591,6 +591,81 @@ def run_config5(args, rank, ws):
         print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------------ configs[3] runner
+
+C4_MESH = {1: 4096, 2: 3328, 4: 2560, 8: 1920, 12: 1536}   # ~64M trace DOFs each
+
+
+def run_config4(args, rank, ws):
+    """configs[3]: order sweep at ~64M trace DOFs, K = I, fp64: trace matvec throughput (the
+    facet-record kernel for p <= 8, the reference-layout kernel above) and the V(2,2)
+    block-Jacobi cycle per order.  value = all orders' DOF applies / their total time; per-order
+    numbers (GDOF/s, fraction of HBM on 16 B/DOF, reference-formula FP64 rate, V-cycle ms) in
+    "orders"."""
+    import torch
+    from paper_1705_09907_b200 import _lib
+    from paper_1705_09907_b200.mesh import build_cartesian
+    from paper_1705_09907_b200.multigrid import _native_mg, attach_smoothers, build_hierarchy
+    from paper_1705_09907_b200.problem import constant_problem
+    if rank != 0:
+        return
+    hbm, kind = peaks()
+    st = torch.cuda.current_stream()
+    orders, tot_dof, tot_us = {}, 0.0, 0.0
+    for p, n in sorted(C4_MESH.items()):
+        levels = build_hierarchy(build_cartesian(n, n), p, constant_problem(0.0, 1.0), smoother=None)
+        attach_smoothers(levels, "blockjacobi", 0.8)
+        op = levels[0].block_op
+        ndof = levels[0].ndof
+        xr = [torch.rand(ndof, dtype=torch.float64, device="cuda") for _ in range(2)]
+        records = p <= 8
+        if records:
+            xs = [op.to_planes(x) for x in xr]
+            ys = [torch.empty_like(xs[0]) for _ in range(2)]
+            fn, kern = _lib.lib.hdg_matvec_soa, "soa_apply_kernel (facet records)"
+        else:
+            xs, ys = xr, [torch.empty_like(xr[0]) for _ in range(2)]
+            fn, kern = _lib.lib.hdg_matvec, "trace_apply_kernel (reference layout)"
+        h = op.handle
+        for k in range(max(args.warmup, 3)):
+            _lib.check(fn(h, xs[k % 2].data_ptr(), ys[k % 2].data_ptr(), st.cuda_stream))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for k in range(args.steps):
+            _lib.check(fn(h, xs[k % 2].data_ptr(), ys[k % 2].data_ptr(), st.cuda_stream))
+        e1.record(st)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / args.steps
+        mg = _native_mg(levels)
+        b, x = xr[0], torch.zeros_like(xr[0])
+        for _ in range(2):
+            _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), 0, x.data_ptr(), 2, 2, 1, 1, st.cuda_stream))
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(5):
+            _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), 0, x.data_ptr(), 2, 2, 1, 1, st.cuda_stream))
+        e1.record(st)
+        torch.cuda.synchronize()
+        nb = levels[0].system.n_blocks
+        orders[str(p)] = {"mesh": n, "ndof": ndof, "kernel": kern, "matvec_us": round(us, 2),
+                          "gdofs": round(ndof / us / 1e3, 1), "hbm_frac": round(16 * ndof / us / 1e3 / hbm, 3),
+                          "fp64_tflops_ref_formula": round(nb * (16 * (p + 1) ** 2 - (p + 1)) / us / 1e6, 2),
+                          "vcycle_ms": round(e0.elapsed_time(e1) / 5, 3), "levels": len(levels)}
+        tot_dof += ndof * args.steps
+        tot_us += us * args.steps
+        del levels, mg, xs, ys, xr, op
+        torch.cuda.empty_cache()
+    line = {"metric": METRIC, "value": tot_dof / tot_us / 1e3, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": tot_us / args.steps / 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[3]: order sweep p in {1,2,4,8,12} at ~64M trace DOFs "
+                                   "(4096^2, 3328^2, 2560^2, 1920^2, 1536^2), K=I, fp64; step = one matvec per order",
+                       "l2": "inputs larger than L2 (2 rotating vectors of ~0.5 GB)", "parallelism": "single"},
+            "orders": orders, "peak": {"hbm_gbs": hbm, "kind": kind}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -599,8 +674,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-vcycle", action="store_true")
-    ap.add_argument("--config", type=int, default=1, choices=[1, 4],
-                    help="BASELINE configs index: 1 = matvec throughput (default), 4 = multi-GPU anisotropic")
+    ap.add_argument("--config", type=int, default=1, choices=[1, 3, 4],
+                    help="BASELINE configs index: 1 = matvec throughput (default), 3 = order sweep, "
+                         "4 = multi-GPU anisotropic")
     ap.add_argument("--n5", type=int, default=C5_N, help="configs[4] mesh size (reduced runs)")
     ap.add_argument("--chunk-rows", type=int, default=256, help="configs[4] N=1: element rows per chunk")
     args = ap.parse_args()
@@ -611,6 +687,8 @@ def main():
     rank, ws, _ = dist_init(args.gpus)
     if args.config == 4:
         run_config5(args, rank, ws)
+    elif args.config == 3:
+        run_config4(args, rank, ws)
     else:
         run_ours(args, rank, ws)
     if ws > 1:
