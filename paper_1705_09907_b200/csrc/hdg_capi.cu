@@ -77,7 +77,7 @@ struct hdg_level {
   std::vector<double> blk;     // the 4n1 x 4n1 element block (shared mode)
   int soa_state = 0;           // 0: not prepared, 1: ready, -1: not available for this level
   std::vector<double> soaM;
-  int soaW = 0, soaJ = 0, soaSeg = 0;
+  int soaW = 0, soaNss = 0;
 };
 
 struct hdg_transfer {
@@ -1711,32 +1711,42 @@ static int soa_prepare(hdg_level* L) {
     L->soa_state = -1;
     return fail(HDG_EINVAL, "element block is not invariant under the element mirrors: no facet-plane apply");
   }
-  L->soaW = std::max(1, (L->nx + 30) / 31);           // owned columns 31w .. 31w+30 cover 0 .. nx-1
-  // one wave of warps, equal row segments (each pays one ghost row)
-  const long long resident = (long long)sm_count() * occ * (SoaCfg<2>::NTH / 32);
-  long long nseg = std::max(1LL, resident / L->soaW);
-  if (nseg > L->ny) nseg = L->ny;
-  int J = (int)((L->ny + nseg - 1) / nseg);
-  if (const char* e = std::getenv("HDG_SOA_J")) J = std::max(1, std::atoi(e));
-  L->soaJ = J;
-  L->soaSeg = (L->ny + J - 1) / J;
+  L->soaW = std::max(1, (L->nx - 1 + 30) / 31);       // tile w = columns 31w .. 31w+31 (overlap 1)
+  // one wave of CTAs: nss super-segments (CTAs) per tile, each split into 4 stacked warp segments
+  const long long resident = (long long)sm_count() * occ;
+  long long nss = std::max(1LL, resident / L->soaW);
+  nss = std::min(nss, (long long)std::max(1, L->ny / (SoaCfg<2>::WPB * 2)));   // >= 2 rows per warp
+  if (const char* e = std::getenv("HDG_SOA_NSS")) nss = std::max(1, std::atoi(e));
+  L->soaNss = (int)nss;
   L->soa_state = 1;
   return 0;
 }
 
 static long long soa_len(const hdg_level* L) {
-  return (long long)(L->ny + 1) * L->soaW * L->n1 * (32 + HDG_SOA_VW);
+  return (long long)(L->ny + 1) * L->soaW * (L->n1 * 32 + ((L->n1 * 31 + 3) & ~3) + 2 * ((L->n1 + 3) & ~3));   // SoaCfg<N1>::ENT
 }
 
 template <int N1>
 static int soa_apply_t(const hdg_level* L, const double* xs, double* ys, cudaStream_t s) {
   SoaArgs<N1> a{};
   a.x = xs; a.y = ys;
-  a.nx = L->nx; a.ny = L->ny; a.W = L->soaW; a.J = L->soaJ; a.nseg = L->soaSeg;
+  a.nx = L->nx; a.ny = L->ny; a.W = L->soaW; a.nss = L->soaNss;
   std::memcpy(a.M, L->soaM.data(), sizeof(a.M));
-  const long long warps = (long long)a.W * a.nseg;
-  const int wpb = SoaCfg<N1>::NTH / 32;
-  soa_apply_kernel<N1><<<(unsigned)((warps + wpb - 1) / wpb), SoaCfg<N1>::NTH, soa_smem_bytes<N1>(), s>>>(a);
+  static_assert(SoaCfg<N1>::ENT % 4 == 0, "records are whole 32-byte sectors");
+  // programmatic stream serialization: this launch's prologue (barrier init, index setup) may
+  // overlap the tail of the kernel before it in the stream; the kernel executes
+  // griddepcontrol.wait (full completion + flush of that kernel) before touching x or y
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(a.W * a.nss));
+  cfg.blockDim = dim3(SoaCfg<N1>::NTH);
+  cfg.dynamicSmemBytes = soa_smem_bytes<N1>();
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = HDG_SOA_PDL ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, soa_apply_kernel<N1>, a);
   CKL();
   return 0;
 }

@@ -4,29 +4,38 @@
 // facets of each element, y_e = S x_e, sum the two owners of every facet), organised for the
 // B200 memory system instead of for the reference's [facet][node] layout:
 //
-//   Device layout ("facet planes"): node k of every horizontal facet line r (r = 0..ny, the
-//   boundary lines 0 and ny included as zeros) is one contiguous run over the element columns,
-//   H[k][r][slot], slot = column + 1; vertical facets are stored by element row,
-//   V[k][r][slot], slot = line + 1 (line 0 and nx are boundary zeros).  The pitch
-//   P = even(31 W + 4) (W = column warps) keeps zero pad slots on both sides, so every load is
-//   one unpredicated 16-byte-aligned bulk copy (TMA) of 34 doubles per node plane and row.
+//   Device layout ("facet records", see soa_pack_kernel): the mesh is cut into tiles of 32
+//   element columns that overlap by one (tile w = columns 31 w .. 31 w + 31).  Record (R, w) is one
+//   contiguous, 32-byte-aligned run
+//       H[N1][32] | V[N1][31] (+ pad to a sector) | Ein[2][EB]
+//   H: node k of horizontal line R over the tile's 32 columns; V: node k of the 31 vertical
+//   lines 31 w + 1 .. 31 w + 31 of element row R - 1 that the tile owns; Ein: the two
+//   lines the tile needs from its neighbours (left-in = line 31 w, right-in = line 31 w + 32),
+//   EB = N1 rounded up to 4 doubles each.  Boundary facets and pads are stored zeros.  Every 32-byte
+//   sector of a record has exactly one writer and is written whole: H rows by 256-byte warp
+//   stores, the packed V block by 32-byte vector stores staged through the ring, the edge blocks
+//   of the neighbouring tiles by 32-byte vector stores of lanes 0 / 30
+//   (partial sectors that meet late in L2 cost ~10% of the kernel at 1024^2, p = 4).
 //
-//   One warp walks a vertical segment of 32 element columns (lane = column); warps overlap by one
-//   column (31 owned).  Per element row the warp's lanes 0 .. 2 N1 - 1 issue one bulk copy each
-//   (node k of the H line above and of the V facets of the row: 34 consecutive slots) into a
-//   per-warp ring of RING entries completed on mbarriers, RING - 2 rows ahead; each lane then
-//   reads its four facets from the ring (bottom = the previous entry's H run).  The element product
-//   runs in the symmetry-adapted basis of the square element (mirrors x -> 1-x and y -> 1-y
-//   commute with S for a constant coefficient on a uniform mesh): sum/difference butterflies
-//   split the 4 n1 element values into four classes and S becomes four dense blocks
-//   (2h)^2 + 2 n1^2 + (2l)^2 FMAs, h = ceil(n1/2), l = floor(n1/2): 102 instead of 400 at p = 4.
-//   Facet sums: the top part of row r-1 stays in registers for the bottom part of row r; the
-//   right part of a lane meets the left part of lane+1 by shuffle.  Every slot of y is written
-//   exactly once (boundary and pad slots as zeros), so y is a valid input of the next apply.
-//   No shared memory, no atomics, no grid synchronisation: one writer per facet (trace.py:3-7).
+//   One warp walks a segment of element rows of one tile (lane = column); the four warps of a CTA
+//   take four consecutive segments of the same tile.  Per element row lane 0 issues ONE bulk copy
+//   (TMA) of the next record into a per-warp ring of RING entries completed on mbarriers,
+//   RING - 1 rows ahead; each lane then reads its four facets from the ring (the bottom H values
+//   stay in registers from the previous row).  The element product runs in the symmetry-adapted
+//   basis of the square element (mirrors x -> 1-x and y -> 1-y commute with S for a constant
+//   coefficient on a uniform mesh): sum/difference butterflies split the 4 n1 element values into
+//   four classes and S becomes four dense blocks, (2h)^2 + 2 n1^2 + (2l)^2 FMAs, h = ceil(n1/2),
+//   l = floor(n1/2): 102 instead of 400 at p = 4.  Facet sums: the top part of row r-1 stays in
+//   registers for the bottom part of row r; the right part of a lane meets the left part of
+//   lane+1 by shuffle.  Every slot of y is written exactly once (boundary and pad slots as
+//   zeros), so y is a valid input of the next apply.  No atomics, no grid synchronisation: one
+//   writer per facet (trace.py:3-7).
 //
-//   A segment of J element rows starts with one ghost row (its top part feeds the first
-//   horizontal line the segment owns): (J+1)/J compute, the extra loads are L2 hits.
+//   Segment boundaries: the first horizontal line of a segment also needs the top part of the
+//   element row below it.  Inside a CTA the upper warp keeps its bottom part in registers and
+//   closes the line after the loop with the lower warp's last top part (handed over through the
+//   lower warp's idle ring, one __syncthreads per kernel); only the first warp of a CTA walks a
+//   ghost row.  The first record of a segment is read for its H part only.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -35,14 +44,12 @@
 #ifndef HDG_SOA_EXP
 #define HDG_SOA_EXP 0          // experiment flags (tools/build_variants.sh), 0 in the product
 #endif
-#ifndef HDG_SOA_ALT
-#define HDG_SOA_ALT 0          // experiment: alternate the walk direction of neighbouring segments
+#ifndef HDG_SOA_BAL
+#define HDG_SOA_BAL 1          // the ghost-row warp of a CTA owns one row fewer
 #endif
-#ifndef HDG_SOA_STCS
-#define HDG_SOA_STCS 0         // experiment: streaming (evict-first) stores of y
-#endif
-#ifndef HDG_SOA_VW
-#define HDG_SOA_VW 34          // V row width of a facet record (36: 32-byte aligned records)
+#ifndef HDG_SOA_PDL
+#define HDG_SOA_PDL 1          // programmatic dependent launch: the prologue overlaps the previous kernel's
+                               // tail; griddepcontrol.wait before the first global access (32.7 vs 35.1 us)
 #endif
 #ifndef HDG_SOA_RING
 #define HDG_SOA_RING 3
@@ -64,19 +71,23 @@ struct SoaCfg {
   static constexpr int A0 = 2 * H, A1 = N1, A2 = N1, A3 = 2 * L;   // class sizes
   static constexpr int MSZ = A0 * A0 + A1 * A1 + A2 * A2 + A3 * A3;
   static constexpr int NTH = 128;
+  static constexpr int WPB = NTH / 32;                   // warps (= stacked segments) per CTA
   static constexpr int MINB = N1 <= 3 ? 4 : HDG_SOA_MINB_HI;
-  static constexpr int RING = HDG_SOA_RING;              // ring entries per warp (RING-2 rows in flight)
-  static constexpr int VW = HDG_SOA_VW;                  // V row width (34: slots 0..33)
-  static constexpr int ENT = N1 * (32 + VW);             // record: H[N1][32] + V[N1][VW] doubles
-  static constexpr int WSTRIDE = (RING * ENT + RING + 1) & ~1;   // doubles per warp (16-byte multiple)
-  static constexpr int SMEM_RING = (NTH / 32) * WSTRIDE * 8;
+  static constexpr int RING = HDG_SOA_RING;              // ring entries per warp (RING-1 rows in flight)
+  static constexpr int VOFF = N1 * 32;                   // V rows, 31 slots each, packed
+  static constexpr int VB = (N1 * 31 + 3) & ~3;          // doubles of the V block (whole sectors)
+  static constexpr int EOFF = VOFF + VB;                 // edge-in blocks: left-in | right-in
+  static constexpr int EB = (N1 + 3) & ~3;               // doubles per edge block (whole sectors)
+  static constexpr int ENT = EOFF + 2 * EB;              // doubles per record (multiple of 4)
+  static constexpr int WSTRIDE = (RING * ENT + RING + 3) & ~3;   // doubles per warp (32-byte multiple)
+  static constexpr int SMEM_RING = WPB * WSTRIDE * 8;
 };
 
 template <int N1>
 struct SoaArgs {
   const double* x;
   double* y;
-  int nx, ny, W, J, nseg;
+  int nx, ny, W, nss;                // tiles, super-segments (CTAs per tile)
   double M[SoaCfg<N1>::MSZ];        // symmetry-adapted blocks, row-major, classes 0..3
 };
 
@@ -154,7 +165,7 @@ struct SoaSmem {
   static constexpr int O1 = O0 + SoaTri<C::A0>::NP;
   static constexpr int O2 = O1 + SoaTri<C::A1>::NP;
   static constexpr int O3 = O2 + SoaTri<C::A2>::NP;
-  static constexpr int TOTAL = O3 + SoaTri<C::A3>::NP;   // doubles (even)
+  static constexpr int TOTAL = (O3 + SoaTri<C::A3>::NP + 3) & ~3;   // doubles (32-byte multiple)
 };
 
 template <int N1>
@@ -246,39 +257,59 @@ __device__ __forceinline__ void soa_load_blocks(const SoaArgs<N1>& a, double* Ms
   }
 }
 
+// one whole 32-byte sector per store (sm_100: 256-bit global stores)
+__device__ __forceinline__ void st_sector(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+// N1 values (+ zero pad) -> an edge block of EB doubles
+template <int N1>
+__device__ __forceinline__ void soa_store_edge(double* p, const double* v) {
+  constexpr int EB = SoaCfg<N1>::EB;
+#pragma unroll
+  for (int q = 0; q < EB; q += 4)
+    st_sector(p + q, q < N1 ? v[q] : 0.0, q + 1 < N1 ? v[q + 1] : 0.0, q + 2 < N1 ? v[q + 2] : 0.0,
+              q + 3 < N1 ? v[q + 3] : 0.0);
+}
+
 template <int N1, int MCONST = (HDG_SOA_MCONST < 0 ? (N1 <= 5) : HDG_SOA_MCONST)>
 __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
     soa_apply_kernel(const __grid_constant__ SoaArgs<N1> a) {
-  constexpr int NT = 4 * N1, RING = SoaCfg<N1>::RING, D = RING - 1;
-  constexpr int ENT = SoaCfg<N1>::ENT;                 // doubles per record: H[N1][32] | V[N1][VW]
-  constexpr int VW = SoaCfg<N1>::VW;
-  constexpr int VOFF = N1 * 32;
-  extern __shared__ __align__(16) double smem_soa[];
+  using C = SoaCfg<N1>;
+  constexpr int NT = 4 * N1, RING = C::RING, D = RING - 1, WPB = C::WPB;
+  constexpr int ENT = C::ENT, VOFF = C::VOFF, VB = C::VB, EOFF = C::EOFF, EB = C::EB;
+  extern __shared__ __align__(32) double smem_soa[];
   double* Ms = smem_soa;
   if (!MCONST) {
     soa_load_blocks<N1>(a, Ms);
     __syncthreads();
   }
-  const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * (SoaCfg<N1>::NTH / 32) + (threadIdx.x >> 5);
-  if (gw >= a.W * a.nseg) return;                      // whole warps only
-  double* ring = smem_soa + SoaSmem<N1>::TOTAL + (threadIdx.x >> 5) * SoaCfg<N1>::WSTRIDE;
-  const int w = gw % a.W, seg = gw / a.W;
-  const int c = 31 * w - 1 + lane;                     // element column of this lane
-  const int r0 = seg * a.J;
-  const int r1 = min(r0 + a.J, a.ny);
-  const int rs = r0 > 0 ? r0 - 1 : 0;                  // ghost row feeds the first owned line
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  double* ring0 = smem_soa + SoaSmem<N1>::TOTAL;
+  double* ring = ring0 + q * C::WSTRIDE;
+  const int w = blockIdx.x % a.W, ss = blockIdx.x / a.W;
+  const int c = 31 * w + lane;                         // element column of this lane
+  // the CTA's rows [c0, c1) (balanced over the tile's CTAs) split over its warps; the first warp of
+  // a CTA with rows below it also walks a ghost row, so it owns one row fewer
+  const int c0 = (int)((long long)ss * a.ny / a.nss), c1 = (int)((long long)(ss + 1) * a.ny / a.nss);
+  const int g = (HDG_SOA_BAL && c0 > 0) ? 1 : 0;
+  auto lo = [&](int u) { return u <= 0 ? c0 : min(c1, c0 + max(0, (c1 - c0 + g) * u / WPB - g)); };
+  const int r0 = lo(q), r1 = lo(q + 1);
+  const bool active = r1 > r0;
+  int below = -1;                                      // nearest non-empty segment below, same CTA
+  for (int u = q - 1; u >= 0 && below < 0; --u)
+    if (lo(u + 1) > lo(u)) below = u;
+  const bool defer = active && below >= 0;             // first line closed after the loop
+  const int rs = (active && below < 0 && r0 > 0) ? r0 - 1 : r0;   // ghost row (first warp of a CTA)
   const int nrows = r1 - rs;                           // element rows walked; records rs .. r1
-  // odd segments walk down: both rows a segment shares with a neighbour (its ghost row and the
-  // neighbour's ghost) are then read by the two warps at the same time (L2 hits, not DRAM)
-  const bool down = HDG_SOA_ALT && (seg & 1);
   const double* __restrict__ X = a.x;
   double* __restrict__ Y = a.y;
   const long long W = a.W;
   auto rec = [&](int R, long long tile) { return (R * W + tile) * ENT; };   // record R, tile
 
   // ring entry t = record rs + t of this warp's tile (H line rs+t, V of element row rs+t-1): one
-  // contiguous bulk copy (TMA) issued by lane 0, completion counted on the entry's mbarrier
+  // contiguous bulk copy (TMA) issued by lane 0, completion counted on the entry's mbarrier.
+  // The first record of a segment is needed for its H line only: a short copy.
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + RING * ENT);
   if (lane == 0) {
 #pragma unroll
@@ -286,130 +317,160 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
   }
   fence_proxy_async();
   __syncwarp();
+#if HDG_SOA_PDL
+#if HDG_SOA_PDL == 2
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // x may be the previous apply's y
+#endif
   auto issue = [&](int t) {
-    if (t > nrows || lane != 0) return;
+    if (t > nrows || lane != 0 || !active) return;
     uint64_t* bar = bars + (t % RING);
-    mbar_arrive_expect_tx(bar, ENT * 8u);
-    tma_load_1d(ring + (t % RING) * ENT, X + rec(down ? r1 - t : rs + t, w), ENT * 8u, bar);
+    const unsigned bytes = t == 0 ? VOFF * 8u : ENT * 8u;
+    mbar_arrive_expect_tx(bar, bytes);
+    tma_load_1d(ring + (t % RING) * ENT, X + rec(rs + t, w), bytes, bar);
   };
 #pragma unroll
   for (int t = 0; t < D; ++t) issue(t);
 
-  const bool hcol = c >= 0 && c < a.nx;
-  const bool vline = c + 1 >= 1 && c + 1 <= a.nx - 1;
-  // tp: the facet-sum partner carried between rows (walking up: T of the row below; down: B of
-  // the row above); xC: the shared H line carried (up: next bottom; down: next top)
-  double tp[N1], xC[N1];
+  const bool hcol = c < a.nx;
+  const bool vline = lane < 31 && c + 1 <= a.nx - 1;   // V line c + 1 (slot = lane) is a DOF
+  // per-lane V reads: right line = slot lane (lane 31: right-in), left line = slot lane - 1
+  // (lane 0: left-in); edge blocks are [k] contiguous, V rows 32 apart
+  const int oL = lane == 0 ? EOFF : VOFF + lane - 1, sL = lane == 0 ? 1 : 31;
+  const int oR = lane == 31 ? EOFF + EB : VOFF + lane, sR = lane == 31 ? 1 : 31;
+  // tp: the T part of the row below (facet-sum partner); xC: its top H line = this row's bottom
+  double tp[N1], xC[N1], hold[N1];
 #pragma unroll
-  for (int k = 0; k < N1; ++k) tp[k] = 0.0;
+  for (int k = 0; k < N1; ++k) tp[k] = hold[k] = 0.0;
 
+  if (active) {
 #pragma unroll 1
-  for (int t = 0; t < nrows; ++t) {
-    const int r = down ? r1 - 1 - t : rs + t;
-    fence_proxy_async();                               // generic reads of entry t-1 before its async refill
-    issue(t + D);                                      // entry t+D (slot of entry t-1: read last iteration)
-    if (t == 0) mbar_wait(bars, 0);
-    mbar_wait(bars + (t + 1) % RING, ((t + 1) / RING) & 1);
-    // lower entry = record r (H line r), upper entry = record r + 1 (H line r+1, V of row r)
-    const double* e0 = ring + ((down ? t + 1 : t) % RING) * ENT + lane;
-    const double* e1 = ring + ((down ? t : t + 1) % RING) * ENT + lane;
-    double xB[N1], xT[N1], xR[N1], xL[N1];
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      if (down) {
-        xT[k] = t == 0 ? e1[k * 32] : xC[k];
-        xB[k] = e0[k * 32];
-      } else {
-        xB[k] = t == 0 ? e0[k * 32] : xC[k];
-        xT[k] = e1[k * 32];
-      }
-      xL[k] = e1[VOFF + k * VW];
-      xR[k] = e1[VOFF + k * VW + 1];
-    }
-    double yB[N1], yR[N1], yT[N1], yL[N1];
-#if HDG_SOA_EXP == 1   // experiment: no element product (memory path only)
-#pragma unroll
-    for (int k = 0; k < N1; ++k) { yB[k] = xB[k]; yR[k] = xR[k]; yT[k] = xT[k]; yL[k] = xL[k]; }
-#else
-    double tv[NT], z[NT];
-    soa_forward<N1>(xB, xR, xT, xL, tv);
-    if (MCONST) soa_blocks_c<N1>(a.M, tv, z);
-    else soa_blocks<N1>(Ms, tv, z);
-    soa_backward<N1>(z, yB, yR, yT, yL);
-#endif
-#if HDG_SOA_EXP == 2   // experiment: no stores unless the result is NaN (compute + loads only)
-    if (yB[0] != yB[0] || yR[N1 - 1] != yR[N1 - 1])
-#endif
-    // H line written this row: up: line r = T(r-1) + B(r) (rows >= r0); down: line r+1 =
-    // T(r) + B(r+1) (from the second row on; the ghost row r0 - 1 comes last and closes line r0)
-    const int hl = down ? r + 1 : r;
-    const bool hwr = down ? t >= 1 : r >= r0;
-    if (hwr) {
-      const bool hint = hcol && hl >= 1;
-      double* hrec = Y + rec(hl, w);
+    for (int t = 0; t < nrows; ++t) {
+      const int r = rs + t;
+      fence_proxy_async();                             // generic reads of entry t-1 before its async refill
+      issue(t + D);                                    // entry t+D (slot of entry t-1: read last iteration)
+      if (t == 0) mbar_wait(bars, 0);
+      mbar_wait(bars + (t + 1) % RING, ((t + 1) / RING) & 1);
+      // lower entry = record r (H line r), upper entry = record r + 1 (H line r+1, V of row r)
+      const double* e0 = ring + (t % RING) * ENT;
+      const double* e1 = ring + ((t + 1) % RING) * ENT;
+      double xB[N1], xT[N1], xR[N1], xL[N1];
 #pragma unroll
       for (int k = 0; k < N1; ++k) {
-        const double hv = hint ? (down ? yT[k] + tp[k] : tp[k] + yB[k]) : 0.0;
-#if HDG_SOA_STCS
-        __stcs(hrec + k * 32 + lane, hv);
-#else
-        hrec[k * 32 + lane] = hv;                      // lane 0 duplicates the left tile's slot 31
-#endif
+        xB[k] = t == 0 ? e0[k * 32 + lane] : xC[k];
+        xT[k] = e1[k * 32 + lane];
+        xL[k] = e1[oL + k * sL];
+        xR[k] = e1[oR + k * sR];
       }
-    }
-    if (r >= r0) {
-      double* vrec = Y + rec(r + 1, w) + VOFF;         // V of element row r
+      double yB[N1], yR[N1], yT[N1], yL[N1];
+#if HDG_SOA_EXP == 1 || HDG_SOA_EXP == 4   // experiment: no element product (memory path only)
+#pragma unroll
+      for (int k = 0; k < N1; ++k) { yB[k] = xB[k]; yR[k] = xR[k]; yT[k] = xT[k]; yL[k] = xL[k]; }
+#else
+      double tv[NT], z[NT];
+      soa_forward<N1>(xB, xR, xT, xL, tv);
+      if (MCONST) soa_blocks_c<N1>(a.M, tv, z);
+      else soa_blocks<N1>(Ms, tv, z);
+      soa_backward<N1>(z, yB, yR, yT, yL);
+#endif
+#if HDG_SOA_EXP == 2 || HDG_SOA_EXP == 4   // experiment: no stores unless the result is NaN (compute + loads only)
+      if (yB[0] != yB[0] || yR[N1 - 1] != yR[N1 - 1])
+#endif
+      if (r >= r0) {
+        if (t == 0 && defer) {                         // line r0 waits for the warp below
+#pragma unroll
+          for (int k = 0; k < N1; ++k) hold[k] = yB[k];
+        } else {                                       // H line r = T(r-1) + B(r)
+          const bool hint = hcol && r >= 1;
+          double* hrec = Y + rec(r, w);
+#pragma unroll
+          for (int k = 0; k < N1; ++k) hrec[k * 32 + lane] = hint ? tp[k] + yB[k] : 0.0;
+        }
+        double* vrec = Y + rec(r + 1, w);              // V of element row r
+        double vv[N1];
+#pragma unroll
+        for (int k = 0; k < N1; ++k) {
+          const double fromR = __shfl_down_sync(0xffffffffu, yL[k], 1);
+          vv[k] = vline ? yR[k] + fromR : 0.0;
+        }
+        // the packed V block leaves as whole sectors through ring entry t (dead: its H line is in
+        // registers, it is refilled next iteration after the proxy fence)
+        double* stg = ring + (t % RING) * ENT;
+        __syncwarp();                                  // t == 0: every lane has read its xB
+#pragma unroll
+        for (int k = 0; k < N1; ++k)
+          if (lane < 31) stg[k * 31 + lane] = vv[k];
+        if (lane < VB - N1 * 31) stg[N1 * 31 + lane] = 0.0;
+        __syncwarp();
+#pragma unroll
+        for (int o = 0; o < VB / 4; o += 32)
+          if (o + lane < VB / 4) {
+            const double2 v0 = reinterpret_cast<const double2*>(stg)[2 * (o + lane)];
+            const double2 v1 = reinterpret_cast<const double2*>(stg)[2 * (o + lane) + 1];
+            st_sector(vrec + VOFF + 4 * (o + lane), v0.x, v0.y, v1.x, v1.y);
+          }
+        // edge-in blocks: line 31w+31 is the right tile's left-in, line 31w+1 the left tile's
+        // right-in; the mesh boundary tiles zero their own outer blocks
+        if (lane == 30) {
+          if (w + 1 < W) soa_store_edge<N1>(vrec + ENT + EOFF, vv);
+          else {
+#pragma unroll
+            for (int k = 0; k < N1; ++k) vv[k] = 0.0;
+            soa_store_edge<N1>(vrec + EOFF + EB, vv);
+          }
+        }
+        if (lane == 0) {
+          if (w > 0) soa_store_edge<N1>(vrec - ENT + EOFF + EB, vv);
+          else {
+#pragma unroll
+            for (int k = 0; k < N1; ++k) vv[k] = 0.0;
+            soa_store_edge<N1>(vrec + EOFF, vv);
+          }
+        }
+      }
 #pragma unroll
       for (int k = 0; k < N1; ++k) {
-        const double fromR = __shfl_down_sync(0xffffffffu, yL[k], 1);
-        const double vv = (vline && lane != 31) ? yR[k] + fromR : 0.0;
-#if HDG_SOA_STCS
-        __stcs(vrec + k * VW + lane + 1 + (lane == 31), vv);
-#else
-        vrec[k * VW + lane + 1 + (lane == 31)] = vv;   // slots 1..31; lane 31 zeroes pad slot 33
-#endif
-        if (VW > 34 && lane == 31)
-#pragma unroll
-          for (int q = 34; q < VW; ++q) vrec[k * VW + q] = 0.0;
-        if (lane == 30 && w + 1 < W) vrec[ENT + k * VW] = vv;         // duplicate: right tile slot 0
-        if (lane == 0 && w > 0) vrec[-ENT + k * VW + 32] = vv;        // duplicate: left tile slot 32
-        if (lane == 0 && w == 0) vrec[k * VW] = 0.0;                  // line -1 (pad)
-        if (lane == 31 && w + 1 == W) vrec[k * VW + 32] = 0.0;        // line 31 W >= nx (pad)
+        tp[k] = yT[k];
+        xC[k] = xT[k];
       }
+      __syncwarp();                                    // entry t is free for issue(t + RING)
     }
+#if HDG_SOA_PDL == 3
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+    // hand the last top part to the warp above (this warp's ring is idle now)
 #pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      tp[k] = down ? yB[k] : yT[k];
-      xC[k] = down ? xB[k] : xT[k];
-    }
-    __syncwarp();                                      // entry t is free for issue(t + RING)
+    for (int k = 0; k < N1; ++k) ring[k * 32 + lane] = tp[k];
   }
-  if (down && r0 == 0) {                               // bottom boundary line (down walk)
-    double* hrec = Y + rec(0, w);
+  __syncthreads();
+  if (defer) {
+    const double* src = ring0 + below * C::WSTRIDE;
+    const bool hint = hcol && r0 >= 1;
+    double* hrec = Y + rec(r0, w);
 #pragma unroll
-    for (int k = 0; k < N1; ++k) hrec[k * 32 + lane] = 0.0;
+    for (int k = 0; k < N1; ++k) hrec[k * 32 + lane] = hint ? src[k * 32 + lane] + hold[k] : 0.0;
   }
-  if (r1 == a.ny) {                                    // top boundary line
+  if (active && r1 == a.ny) {                          // top boundary line
     double* hrec = Y + rec(a.ny, w);
 #pragma unroll
     for (int k = 0; k < N1; ++k) hrec[k * 32 + lane] = 0.0;
   }
-  if (r0 == 0) {                                       // V of element row -1 (pad record 0)
+  if (active && r0 == 0) {                             // V, edges of element row -1 (pad part of record 0)
     double* vrec = Y + rec(0, w) + VOFF;
-#pragma unroll
-    for (int k = 0; k < N1; ++k) {
-      vrec[k * VW + lane] = 0.0;
-      if (lane < VW - 32) vrec[k * VW + 32 + lane] = 0.0;
-    }
+    for (int o = lane; o < VB + 2 * EB; o += 32) vrec[o] = 0.0;
   }
 }
 
-// Record layout: record R (R = 0..ny) of tile w holds H line R (slot j = column 31 w - 1 + j,
-// j < 32) and V of element row R - 1 (slot j = line 31 w - 1 + j, j < 34; slot 33 unused).
+// Record layout: record (R, w), R = 0..ny, w < W = ceil((nx - 1) / 31):
+//   H[k][j] (j < 32)  = node k of horizontal line R, column 31 w + j
+//   V[k][j] (j < 31)  = node k of vertical line 31 w + 1 + j, element row R - 1 (rows packed)
+//   Ein[0][k], Ein[1][k] = node k of vertical lines 31 w and 31 w + 32, element row R - 1
 template <int N1>
 __global__ void soa_pack_kernel(const double* __restrict__ x, double* __restrict__ xs, int nx, int ny, int W,
                                 long long nh, long long total) {
-  constexpr int ENT = SoaCfg<N1>::ENT, VOFF = N1 * 32;
+  using C = SoaCfg<N1>;
+  constexpr int ENT = C::ENT, VOFF = C::VOFF, EOFF = C::EOFF, EB = C::EB;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
   const long long rw = t / ENT;
@@ -417,12 +478,20 @@ __global__ void soa_pack_kernel(const double* __restrict__ x, double* __restrict
   const int R = (int)(rw / W), w = (int)(rw % W);
   double v = 0.0;
   if (o < VOFF) {
-    const int k = o / 32, col = 31 * w - 1 + o % 32;
-    if (R >= 1 && R <= ny - 1 && col >= 0 && col < nx) v = x[((long long)(R - 1) * nx + col) * N1 + k];
+    const int k = o / 32, col = 31 * w + o % 32;
+    if (R >= 1 && R <= ny - 1 && col < nx) v = x[((long long)(R - 1) * nx + col) * N1 + k];
   } else {
-    constexpr int VW = SoaCfg<N1>::VW;
-    const int k = (o - VOFF) / VW, j = (o - VOFF) % VW, line = 31 * w - 1 + j, r = R - 1;
-    if (j < 33 && r >= 0 && line >= 1 && line <= nx - 1) v = x[(nh + (long long)(line - 1) * ny + r) * N1 + k];
+    int k, line;
+    if (o < EOFF) {
+      k = (o - VOFF) / 31;
+      line = k < N1 ? 31 * w + 1 + (o - VOFF) % 31 : 0;
+      k = min(k, N1 - 1);
+    } else {
+      k = (o - EOFF) % EB;
+      line = k < N1 ? 31 * w + ((o - EOFF) / EB ? 32 : 0) : 0;
+    }
+    const int r = R - 1;
+    if (r >= 0 && line >= 1 && line <= nx - 1) v = x[(nh + (long long)(line - 1) * ny + r) * N1 + k];
   }
   xs[t] = v;
 }
@@ -430,19 +499,20 @@ __global__ void soa_pack_kernel(const double* __restrict__ x, double* __restrict
 template <int N1>
 __global__ void soa_unpack_kernel(const double* __restrict__ xs, double* __restrict__ x, int nx, int ny, int W,
                                   long long nh, long long ndof) {
-  constexpr int ENT = SoaCfg<N1>::ENT, VOFF = N1 * 32;
+  using C = SoaCfg<N1>;
+  constexpr int ENT = C::ENT, VOFF = C::VOFF;
   const long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= ndof) return;
   const long long blk = u / N1;
   const int k = (int)(u % N1);
   long long src;
   if (blk < nh) {
-    const int R = (int)(blk / nx) + 1, col = (int)(blk % nx), w = col / 31;
-    src = ((long long)R * W + w) * ENT + k * 32 + (col - 31 * w + 1);
+    const int R = (int)(blk / nx) + 1, col = (int)(blk % nx), w = min(col / 31, W - 1);
+    src = ((long long)R * W + w) * ENT + k * 32 + (col - 31 * w);
   } else {
     const long long b = blk - nh;
-    const int line = (int)(b / ny) + 1, r = (int)(b % ny), w = line / 31;
-    src = ((long long)(r + 1) * W + w) * ENT + VOFF + k * SoaCfg<N1>::VW + (line - 31 * w + 1);
+    const int line = (int)(b / ny) + 1, r = (int)(b % ny), w = (line - 1) / 31;
+    src = ((long long)(r + 1) * W + w) * ENT + VOFF + k * 31 + (line - 31 * w - 1);
   }
   x[u] = xs[src];
 }
