@@ -179,6 +179,17 @@ int hdg_mg_set_coarse_inverse(hdg_mg* mg, const double* inv, int64_t n);
  * per-launch cycle (multigrid.py:393-406).  enable = 0 issues everything as separate launches
  * (A/B timing, parity tests). */
 int hdg_mg_set_fused_tail(hdg_mg* mg, int enable);
+/* Record-layout cycle: the constant-coefficient, block-Jacobi-smoothed p-ladder of the finest
+ * mesh (levels 0 .. m-1, level m-1 is p = 1 and h-linked to level m) keeps every level vector as
+ * facet records and runs each sweep / residual of multigrid.py:397-405 as one pass of the
+ * record kernel with the update fused (first two sweeps from x = 0, residual + p-restriction,
+ * p-prolongation + first post-sweep are single passes); b is packed and x unpacked at the
+ * cycle's boundary, the levels below m use the reference layout.  mode 0: off, 1 (default):
+ * when level 0 has >= 2^20 dofs (env HDG_REC_MIN_DOF), 2: whenever the levels qualify, 3: as 2
+ * with the p-prolongation as its own kernel.  hdg_mg_record_levels returns m of the last
+ * cycle (0: reference layout). */
+int hdg_mg_set_records(hdg_mg* mg, int mode);
+int hdg_mg_record_levels(const hdg_mg* mg);
 /* x = cycle(b, x0) with nu1/nu2 smoothing sweeps (FSAI if attached to the level, else
  * block-Jacobi), visits = 1 (V) or 2 (W).
  * x0 may be NULL (zero initial guess, as v_cycle(x0=None)).  x may alias x0.

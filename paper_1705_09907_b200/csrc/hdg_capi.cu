@@ -1,8 +1,7 @@
 // hdg_capi.cu - C ABI (include/hdgb200.h) and native runtime: operator objects, transfers,
 // the device-resident multigrid cycle and its CUDA-graph cache.
 // Reference interfaces replaced: see include/hdgb200.h (each entry cites trace.py / multigrid.py).
-#include "hdgb200.h"
-#include "hdg_kernels.cuh"
+#include "hdg_internal.h"
 #include "hdg_soa.cuh"
 #include "hdg_fsai.cuh"
 
@@ -18,102 +17,13 @@
 #include <tuple>
 #include <vector>
 
-using namespace hdg;
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
 
-static const int SOA_MAXN1 = 9;
-
-static thread_local std::string g_err;
-static std::atomic<long long> g_launches{0};
-
-static int fail(int code, const std::string& msg) {
+int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
-
-#define CK(call)                                                                          \
-  do {                                                                                    \
-    cudaError_t e_ = (call);                                                              \
-    if (e_ != cudaSuccess) return fail(HDG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-
-#define CKL()                                                                             \
-  do {                                                                                    \
-    g_launches.fetch_add(1, std::memory_order_relaxed);                                   \
-    cudaError_t e_ = cudaGetLastError();                                                  \
-    if (e_ != cudaSuccess) return fail(HDG_ECUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
-  } while (0)
-
-static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
-
-struct hdg_level {
-  int nx = 0, ny = 0, p = 0, n1 = 0, nxp = 0;
-  long long nh = 0, n_blocks = 0, ndof = 0;
-  bool stored = false;
-  std::vector<double> Wh, Wv, Dh, Dv;                // shared mode (host copies -> kernel params)
-  std::vector<double> Gh, Gv;                        // shared mode: mirror-reduced stencils (Sym<N1>)
-  double *dWh = nullptr, *dWv = nullptr;             // stored mode streams
-  double *dDh = nullptr, *dDv = nullptr;
-  bool has_bj = false;
-  double omega = 0.8;
-  // Chebyshev-weighted block-Jacobi steps on [cheb_lo, cheb_hi] of D^-1 A (robust smoother
-  // for high-contrast K; same weighting rule as the reference FSAI sweeps, multigrid.py:76-81)
-  bool bj_cheb = false;
-  double bj_lo = 0.0, bj_hi = 1.0;
-  double* partials = nullptr;                        // per-CTA norm partials
-  int npart = 0;
-  long long op_bytes = 0;
-  // FSAI smoother (multigrid.py:47-88): G and G' in CSR on the device
-  bool has_fsai = false;
-  bool use_fsai = false;   // active smoother of the cycle: the one attached last
-  int *g_ptr = nullptr, *g_col = nullptr, *gt_ptr = nullptr, *gt_col = nullptr;
-  double *g_val = nullptr, *gt_val = nullptr;
-  double lam_max = 1.0, cheb_frac = 0.15, fsai_omega = 1.0;
-  // facet-structured FSAI (hdg_fsai.cuh): G rows per facet, no column indices, G' by gathers
-  bool fsai_struct = false;
-  double *fGh = nullptr, *fGv = nullptr;
-  unsigned smoother_gen = 0;     // bumped by every smoother setter: cycle graphs captured before are stale
-  double* tail_wd = nullptr;   // fused coarse tail, shared mode: device copy of Wh, Wv, Dh, Dv (n1 = 2)
-  // facet-plane (SoA) device layout, shared mode (hdg_soa.cuh): element block + adapted blocks
-  std::vector<double> blk;     // the 4n1 x 4n1 element block (shared mode)
-  int soa_state = 0;           // 0: not prepared, 1: ready, -1: not available for this level
-  std::vector<double> soaM;
-  int soaW = 0, soaNss = 0;
-};
-
-struct hdg_transfer {
-  bool is_h = false;
-  const hdg_level* fine = nullptr;
-  const hdg_level* coarse = nullptr;
-  PArgs pa{};
-  HArgs ha{};
-  double* dcross = nullptr;
-};
-
-struct GraphEntry {
-  cudaGraphExec_t exec;
-  long long nkern;
-  unsigned long long last_use;
-};
-// cycle graphs are keyed by buffer pointers: callers whose addresses vary would otherwise grow the
-// cache without bound, so the least recently replayed graph is dropped beyond this many
-static const size_t MAX_CYCLE_GRAPHS = 8;
-
-struct hdg_mg {
-  std::vector<hdg_level*> L;
-  std::vector<hdg_transfer*> T;
-  int n = 0;
-  std::vector<double*> X, Tm, B, R;
-  double* Ainv = nullptr;
-  long long nc = 0;
-  cudaStream_t cs = nullptr;
-  std::map<std::tuple<const void*, const void*, void*, int, int, int>, GraphEntry> graphs;
-  int tail_k0 = -1;              // first level of the fused coarse tail (-1: none)
-  bool tail_enabled = true;
-  bool fuse_first = true;        // first two Jacobi steps from x = 0 in one kernel (shared levels)
-  std::vector<unsigned> gens;    // levels' smoother_gen when the cached graphs were captured
-  unsigned long long use_clock = 0;
-  long long graph_captures = 0;  // graphs instantiated so far (tests: re-capture after a smoother change)
-};
 
 // ------------------------------------------------------------------------------ helpers
 
@@ -155,7 +65,7 @@ static int prepare_t() {
   return 0;
 }
 
-static int sm_count() {
+int sm_count() {
   static int n = 0;
   if (n == 0) {
     int dev = 0;
@@ -1144,10 +1054,25 @@ int hdg_mg_destroy(hdg_mg* mg) {
     cudaFree(mg->Tm[k]); cudaFree(mg->B[k]); cudaFree(mg->R[k]);
   }
   cudaFree(mg->Ainv);
+  for (double* q : mg->Xr) cudaFree(q);
+  for (double* q : mg->Tr) cudaFree(q);
+  for (double* q : mg->Br) cudaFree(q);
+  cudaFree(mg->Rr);
   if (mg->cs) cudaStreamDestroy(mg->cs);
   delete mg;
   return 0;
 }
+
+int hdg_mg_set_records(hdg_mg* mg, int mode) {
+  if (!mg || mode < 0 || mode > 3) return fail(HDG_EINVAL, "record mode must be 0 (off), 1 (auto), 2 (on), 3 (on, unfused prolongation)");
+  mg->rec_mode = mode == 3 ? 2 : mode;
+  mg->rec_fuse_prolong = mode != 3;
+  for (auto& kv : mg->graphs) cudaGraphExecDestroy(kv.second.exec);
+  mg->graphs.clear();
+  return 0;
+}
+
+int hdg_mg_record_levels(const hdg_mg* mg) { return mg ? mg->rec_m : -1; }
 
 int hdg_mg_set_fused_tail(hdg_mg* mg, int enable) {
   if (!mg) return fail(HDG_EINVAL, "null mg");
@@ -1405,8 +1330,138 @@ static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1
   return 0;
 }
 
+// ------------------------------------------------------------------ record-layout cycle
+// Levels 0 .. m-1 qualify when they are the constant-coefficient (shared, mirror-symmetric) p-ladder of
+// the finest mesh, smoothed by block-Jacobi, and level m-1 (p = 1) is linked to level m by a whole-mesh
+// h-transfer; the recursion below level m-1 is cycle_rec on the reference layout.
+static long long rec_min_dof() {
+  static long long v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("HDG_REC_MIN_DOF");
+    v = e ? std::atoll(e) : (1LL << 20);
+  }
+  return v;
+}
+
+static int rec_find(hdg_mg* mg) {
+  if (mg->rec_mode == 0 || mg->n < 2) return 0;
+  hdg_level* L0 = mg->L[0];
+  if (mg->rec_mode == 1 && L0->ndof < rec_min_dof()) return 0;
+  int m = 0;
+  for (int k = 0; k + 1 < mg->n; ++k) {
+    hdg_level* L = mg->L[k];
+    if (L->stored || L->blk.empty() || L->n1 > SOA_MAXN1 || !L->has_bj || L->use_fsai || L->nx != L0->nx ||
+        L->ny != L0->ny || L->ndof == 0)
+      return 0;
+    if (soa_prepare(L)) return 0;
+    if (mg->T[k]->is_h) {
+      const HArgs& h = mg->T[k]->ha;
+      if (L->n1 != 2 || h.jf0 != 0 || h.jc0 != 0 || h.nyf != 2 * h.nyc || L->nx != 2 * h.nxc || L->ny != h.nyf)
+        return 0;
+      m = k + 1;
+      break;
+    }
+  }
+  return m;
+}
+
+// allocate the record vectors (outside any stream capture)
+static int rec_prepare(hdg_mg* mg) {
+  const int m = rec_find(mg);
+  if (m == mg->rec_m && (m == 0 || !mg->Xr.empty())) return 0;
+  for (double* q : mg->Xr) cudaFree(q);
+  for (double* q : mg->Tr) cudaFree(q);
+  for (double* q : mg->Br) cudaFree(q);
+  cudaFree(mg->Rr);
+  mg->Xr.clear(); mg->Tr.clear(); mg->Br.clear(); mg->Rr = nullptr;
+  mg->rec_m = m;
+  for (int k = 0; k < m; ++k) {
+    const size_t bytes = sizeof(double) * (size_t)soa_len(mg->L[k]);
+    double *a = nullptr, *b = nullptr, *c = nullptr;
+    CK(cudaMalloc(&a, bytes)); mg->Xr.push_back(a);
+    CK(cudaMalloc(&b, bytes)); mg->Tr.push_back(b);
+    CK(cudaMalloc(&c, bytes)); mg->Br.push_back(c);
+  }
+  if (m > 0) CK(cudaMalloc(&mg->Rr, sizeof(double) * (size_t)soa_len(mg->L[m - 1])));
+  return 0;
+}
+
+static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1, int nu2, int visits,
+                     cudaStream_t s);
+
+// multigrid.py:393-406 on facet records: level-k right-hand side b and iterate x_in (null: zero) are
+// records; the result is left in one of the level's two buffers, returned through x_out
+static int cycle_rec_soa(hdg_mg* mg, int k, const double* b, const double* x_in, double** x_out, int nu1, int nu2,
+                         int visits, cudaStream_t s) {
+  hdg_level* L = mg->L[k];
+  double* const A = mg->Xr[k];
+  double* const Bf = mg->Tr[k];
+  auto other = [&](const double* q) { return q == A ? Bf : A; };
+  const double* cur = x_in;
+  int rc, first = 0;
+  if (!x_in) {
+    if (nu1 >= 1) {
+      // x = 0: x1 = w1 D^-1 b is formed per facet on the streamed b records and the second sweep
+      // runs in the same pass (nu1 = 1: the second step has weight 0)
+      const double w1 = bj_weight(L, 1, nu1), w2 = nu1 >= 2 ? bj_weight(L, 2, nu1) : 0.0;
+      if ((rc = soa_cyc_sweep(L, SOA_EPI_BJ0, b, b, A, w2, w1, nullptr, nullptr, s))) return rc;
+      first = nu1 >= 2 ? 2 : 1;
+    } else {
+      CK(cudaMemsetAsync(A, 0, sizeof(double) * (size_t)soa_len(L), s));
+    }
+    cur = A;
+  }
+  for (int it = first; it < nu1; ++it) {
+    double* out = other(cur);
+    if ((rc = soa_cyc_sweep(L, SOA_EPI_BJ, cur, b, out, bj_weight(L, it + 1, nu1), 0.0, nullptr, nullptr, s))) return rc;
+    cur = out;
+  }
+  hdg_transfer* T = mg->T[k];
+  int post0 = 0;
+  if (!T->is_h) {
+    if ((rc = soa_cyc_sweep(L, SOA_EPI_RESPR, cur, b, mg->Br[k + 1], 0.0, 0.0, T->pa.V, nullptr, s))) return rc;
+    double* xc = nullptr;
+    for (int v = 0; v < visits; ++v)
+      if ((rc = cycle_rec_soa(mg, k + 1, mg->Br[k + 1], xc, &xc, nu1, nu2, visits, s))) return rc;
+    if (nu2 >= 1 && mg->rec_fuse_prolong) {
+      double* out = other(cur);
+      if ((rc = soa_cyc_sweep(L, SOA_EPI_BJ, cur, b, out, bj_weight(L, 1, nu2), 0.0, T->pa.V, xc, s))) return rc;
+      cur = out;
+      post0 = 1;
+    } else if ((rc = soa_cyc_p_prolong(L, mg->L[k + 1], xc, const_cast<double*>(cur), T->pa.V, s))) {
+      return rc;
+    }
+  } else {
+    if ((rc = soa_cyc_sweep(L, SOA_EPI_RES, cur, b, mg->Rr, 0.0, 0.0, nullptr, nullptr, s))) return rc;
+    if ((rc = soa_cyc_h_restrict(L, T->ha, mg->Rr, mg->B[k + 1], s))) return rc;
+    for (int v = 0; v < visits; ++v)
+      if ((rc = cycle_rec(mg, k + 1, mg->B[k + 1], v == 0, nu1, nu2, visits, s))) return rc;
+    if ((rc = soa_cyc_h_prolong(L, T->ha, mg->X[k + 1], const_cast<double*>(cur), s))) return rc;
+  }
+  for (int it = post0; it < nu2; ++it) {
+    double* out = other(cur);
+    if ((rc = soa_cyc_sweep(L, SOA_EPI_BJ, cur, b, out, bj_weight(L, it + 1, nu2), 0.0, nullptr, nullptr, s))) return rc;
+    cur = out;
+  }
+  *x_out = const_cast<double*>(cur);
+  return 0;
+}
+
 static int cycle_issue(hdg_mg* mg, const double* b, const double* x0, double* x, int nu1, int nu2, int visits,
                        cudaStream_t s) {
+  if (mg->rec_m > 0) {
+    hdg_level* L0 = mg->L[0];
+    int rc;
+    if ((rc = hdg_soa_pack(L0, b, mg->Br[0], s))) return rc;
+    const double* xin = nullptr;
+    if (x0) {
+      if ((rc = hdg_soa_pack(L0, x0, mg->Xr[0], s))) return rc;
+      xin = mg->Xr[0];
+    }
+    double* res = nullptr;
+    if ((rc = cycle_rec_soa(mg, 0, mg->Br[0], xin, &res, nu1, nu2, visits, s))) return rc;
+    return hdg_soa_unpack(L0, res, x, s);
+  }
   const size_t bytes = sizeof(double) * (size_t)mg->L[0]->ndof;
   mg->X[0] = x;
   bool zero = (x0 == nullptr);
@@ -1434,6 +1489,7 @@ int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int n
   cudaStream_t s = S(stream);
   int rc0 = tail_prepare(mg);
   if (rc0) return rc0;
+  if ((rc0 = rec_prepare(mg))) return rc0;
   if (!use_graph) return cycle_issue(mg, b, x0, x, nu1, nu2, visits, s);
   auto key = std::make_tuple((const void*)b, (const void*)x0, (void*)x, nu1, nu2, visits);
   auto it = mg->graphs.find(key);
@@ -1547,7 +1603,7 @@ int hdg_pcg(const hdg_level* L, hdg_mg* mg, const double* b, double* x, int use_
     return mg ? cycle_issue(mg, r, nullptr, z, nu1, nu2, 1, st) : 0;
   };
   do {
-    if (mg) { refresh_graphs(mg); if ((rc = tail_prepare(mg))) break; }
+    if (mg) { refresh_graphs(mg); if ((rc = tail_prepare(mg))) break; if ((rc = rec_prepare(mg))) break; }
     // r = b - A x0 (trace.py:147), z = M r, d = z, rz = r.z
     if (use_x0) { if ((rc = hdg_residual(L, b, x, r, nullptr, s))) break; }
     else {
@@ -1693,7 +1749,7 @@ static int soa_occupancy() {
   return occ;
 }
 
-static int soa_prepare(hdg_level* L) {
+int soa_prepare(hdg_level* L) {
   if (L->soa_state == 1) return 0;
   if (L->soa_state == -1 || L->stored || L->blk.empty() || L->n1 > SOA_MAXN1)
     return fail(HDG_EINVAL, "facet-plane layout needs a shared-block (constant coefficient, mirror-symmetric) "
@@ -1722,7 +1778,7 @@ static int soa_prepare(hdg_level* L) {
   return 0;
 }
 
-static long long soa_len(const hdg_level* L) {
+long long soa_len(const hdg_level* L) {
   return (long long)(L->ny + 1) * L->soaW * (L->n1 * 32 + ((L->n1 * 31 + 3) & ~3) + 2 * ((L->n1 + 3) & ~3));   // SoaCfg<N1>::ENT
 }
 

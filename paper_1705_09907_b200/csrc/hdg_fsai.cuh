@@ -294,7 +294,7 @@ __global__ void fsai_gt_kernel(const FsaiApplyArgs a) {
 }
 
 // v <- w / ||w|| given the device norm^2 (power iteration step, multigrid.py:167-172)
-__global__ void fsai_scale_kernel(const double* __restrict__ w, const double* __restrict__ nrm2, double* __restrict__ v,
+static __global__ void fsai_scale_kernel(const double* __restrict__ w, const double* __restrict__ nrm2, double* __restrict__ v,
                                   double* __restrict__ lam_out, long long n) {
   const double lam = sqrt(*nrm2);
   if (blockIdx.x == 0 && threadIdx.x == 0) *lam_out = lam;

@@ -1345,7 +1345,7 @@ __device__ __forceinline__ void h_prolong_add_one(const HArgs& h, const double* 
   *xp = x;
 }
 
-__global__ void h_prolong_add_kernel(const __grid_constant__ HArgs h, const double* __restrict__ ec,
+static __global__ void h_prolong_add_kernel(const __grid_constant__ HArgs h, const double* __restrict__ ec,
                                      double* __restrict__ xf) {
   const long long nvf = (long long)(2 * h.nxc - 1) * h.nyf;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1424,7 +1424,7 @@ __device__ __forceinline__ void h_restrict_one(const HArgs& h, const double* __r
   rc[2 * t + 1] = ok ? acc[1] : 0.0;
 }
 
-__global__ void h_restrict_kernel(const __grid_constant__ HArgs h, const double* __restrict__ rf,
+static __global__ void h_restrict_kernel(const __grid_constant__ HArgs h, const double* __restrict__ rf,
                                   double* __restrict__ rc) {
   const long long nvc = (long long)(h.nxc - 1) * h.nyc;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1435,7 +1435,7 @@ __global__ void h_restrict_kernel(const __grid_constant__ HArgs h, const double*
 
 // ---------------------------------------------------------------------------- small kernels
 // dense y = M b, warp per row (coarsest level, multigrid.py:209-212)
-__global__ void dense_gemv_kernel(const double* __restrict__ M, const double* __restrict__ b,
+static __global__ void dense_gemv_kernel(const double* __restrict__ M, const double* __restrict__ b,
                                   double* __restrict__ y, int n) {
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -1448,7 +1448,7 @@ __global__ void dense_gemv_kernel(const double* __restrict__ M, const double* __
 }
 
 // deterministic dot: fixed grid, per-CTA partials, then one CTA sums them in order
-__global__ void dot_partials_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
+static __global__ void dot_partials_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
                                     double* __restrict__ partials) {
   double s = 0.0;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
@@ -1465,7 +1465,7 @@ __global__ void dot_partials_kernel(const double* __restrict__ a, const double* 
   }
 }
 
-__global__ void sum_partials_kernel(const double* __restrict__ partials, int n, double* __restrict__ out) {
+static __global__ void sum_partials_kernel(const double* __restrict__ partials, int n, double* __restrict__ out) {
   // one warp; fixed order => bitwise deterministic
   double s = 0.0;
   for (int t = threadIdx.x; t < n; t += 32) s += partials[t];
@@ -1528,7 +1528,7 @@ __global__ void csr_spmv_kernel(int n, const int* __restrict__ rowptr, const int
 }
 
 // CG vector updates (trace.py:156-161): x += a d, r -= a ad ;  d = z + beta d
-__global__ void cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ d,
+static __global__ void cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ d,
                                  const double* __restrict__ ad, double alpha, long long n) {
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
     x[t] = fma(alpha, d[t], x[t]);
@@ -1538,7 +1538,7 @@ __global__ void cg_update_kernel(double* __restrict__ x, double* __restrict__ r,
 
 // two dot products in one pass (same per-thread order as dot_partials_kernel, so each result is
 // bitwise the one a separate hdg_dot would give): partials[blk] = a.b, partials[grid + blk] = c.e
-__global__ void dot2_partials_kernel(const double* __restrict__ a, const double* __restrict__ b,
+static __global__ void dot2_partials_kernel(const double* __restrict__ a, const double* __restrict__ b,
                                      const double* __restrict__ c, const double* __restrict__ e, long long n,
                                      double* __restrict__ partials) {
   double s = 0.0, u = 0.0;
@@ -1564,7 +1564,7 @@ __global__ void dot2_partials_kernel(const double* __restrict__ a, const double*
 
 // CG updates with the step lengths read from device scalars (no host round trip):
 // sc[0] = r.z, sc[1] = d.Ad, sc[2] = r_new.z_new  (trace.py:156-161)
-__global__ void cg_update_dev_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ d,
+static __global__ void cg_update_dev_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ d,
                                      const double* __restrict__ ad, const double* __restrict__ sc, long long n) {
   const double alpha = sc[0] / sc[1];
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
@@ -1573,14 +1573,14 @@ __global__ void cg_update_dev_kernel(double* __restrict__ x, double* __restrict_
   }
 }
 
-__global__ void xpby_dev_kernel(const double* __restrict__ z, const double* __restrict__ sc, double* __restrict__ d,
+static __global__ void xpby_dev_kernel(const double* __restrict__ z, const double* __restrict__ sc, double* __restrict__ d,
                                 long long n) {
   const double beta = sc[2] / sc[0];
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
     d[t] = fma(beta, d[t], z[t]);
 }
 
-__global__ void xpby_kernel(const double* __restrict__ z, double beta, double* __restrict__ d, long long n) {
+static __global__ void xpby_kernel(const double* __restrict__ z, double beta, double* __restrict__ d, long long n) {
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x)
     d[t] = fma(beta, d[t], z[t]);
 }
@@ -1722,7 +1722,7 @@ __device__ __forceinline__ int tail_slot(const TailLevel& L, int bk, bool& vert)
   return j * L.nxp + i;
 }
 
-__global__ void __launch_bounds__(TAIL_THREADS, 1) tail_cycle_kernel(const __grid_constant__ TailArgs Ap) {
+static __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_cycle_kernel(const __grid_constant__ TailArgs Ap) {
   extern __shared__ __align__(16) double tsm_raw[];
   const int tid = threadIdx.x;
   // the program and level descriptors are read on every op: copy them from the parameter

@@ -65,6 +65,9 @@
 
 namespace hdg {
 
+// sweeps of the record-layout cycle (hdg_soa_cycle.cuh)
+enum { SOA_EPI_BJ = 1, SOA_EPI_BJ0 = 2, SOA_EPI_RES = 3, SOA_EPI_RESPR = 4 };
+
 template <int N1>
 struct SoaCfg {
   static constexpr int H = (N1 + 1) / 2, L = N1 / 2;

@@ -558,6 +558,18 @@ def set_fused_tail(levels, enable=True):
     check(lib.hdg_mg_set_fused_tail(_native_mg(levels).handle, int(bool(enable))))
 
 
+def set_records(levels, mode=1):
+    """Facet-record cycle on the constant-coefficient p-ladder of the finest mesh (hdgb200.h:
+    hdg_mg_set_records): 0 off, 1 automatic (large levels), 2 whenever the levels qualify, 3 as 2
+    with the p-prolongation as a separate kernel."""
+    check(lib.hdg_mg_set_records(_native_mg(levels).handle, int(mode)))
+
+
+def record_levels(levels):
+    """Number of leading levels the last device cycle ran on facet records (0: reference layout)."""
+    return int(lib.hdg_mg_record_levels(_native_mg(levels).handle))
+
+
 def _native_mg(levels):
     """The native level stack of `levels` (a hierarchy or a suffix / slice of one).  It is cached
     on the hierarchy's first level, so it lives exactly as long as the levels do: dropping the
