@@ -399,15 +399,47 @@ def run_ours(args, rank, ws):
         print(json.dumps(line), flush=True)
 
 
+def vcycle_model_bytes(levels):
+    """Minimum HBM bytes of one V(2,2) block-Jacobi cycle with every facet-local step fused into
+    an operator pass: per non-coarsest level of n dofs with a coarse level of
+    c dofs, p-link: zero-start double sweep 16n, residual + restriction 16n + 8c, prolongation +
+    sweep 24n + 8c, sweep 24n; h-link: 16n + residual 24n + restriction 8n + 8c + prolongation
+    16n + 8c + two sweeps 48n.  Shared (K = I) levels: no operator bytes."""
+    total = 0
+    for k in range(len(levels) - 1):
+        n, c = levels[k].ndof, levels[k + 1].ndof
+        same_mesh = levels[k].mesh.n_x == levels[k + 1].mesh.n_x
+        total += (80 * n + 16 * c) if same_mesh else (112 * n + 16 * c)
+    return total
+
+
 def vcycle_timings(steps=20):
-    """V(2,2) block-Jacobi(0.8) cycle time on the configs[1] hierarchy (1024^2, p=4, K=I, 14
-    levels) and on configs[0] (64^2, p=2, sliced to 4x4), device-resident, graph-replayed."""
+    """V(2,2) block-Jacobi(0.8) cycle time on the configs[1] hierarchy (1024^2, p=4, K=I, 13
+    levels) and on configs[0] (64^2, p=2, sliced to 4x4), graph-replayed: through hdg_mg_cycle on
+    reference-layout vectors (pack / unpack at the boundary when the record cycle is on) and, for
+    configs[1], on record-resident vectors (hdg_mg_cycle_records), with the byte-model roofline."""
     import torch
     from paper_1705_09907_b200 import _lib
     from paper_1705_09907_b200.mesh import build_cartesian
     from paper_1705_09907_b200.multigrid import _native_mg, build_hierarchy
     from paper_1705_09907_b200.problem import config1_problem, constant_problem
     out = {}
+    L = _lib.lib
+    peak, _ = peaks()
+
+    def timed(fn):
+        st = torch.cuda.current_stream()
+        for _ in range(3):
+            fn(st)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            fn(st)
+        e1.record(st)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
     for name, (n, p, spec, cut) in {"cfg2_1024p4": (1024, 4, constant_problem(0.0, 1.0), None),
                                     "cfg1_64p2": (64, 2, config1_problem(), 6)}.items():
         levels = build_hierarchy(build_cartesian(n, n), p, spec, smoother=None)
@@ -417,19 +449,26 @@ def vcycle_timings(steps=20):
         mg = _native_mg(levels)
         b = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, levels[0].ndof)).cuda()
         x = torch.zeros_like(b)
-        st = torch.cuda.current_stream()
-        for _ in range(3):
-            _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), x.data_ptr(), x.data_ptr(), 2, 2, 1, 1,
-                                             st.cuda_stream))
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        for _ in range(steps):
-            _lib.check(_lib.lib.hdg_mg_cycle(mg.handle, b.data_ptr(), x.data_ptr(), x.data_ptr(), 2, 2, 1, 1,
-                                             st.cuda_stream))
-        e1.record(st)
-        torch.cuda.synchronize()
-        out[name] = {"ms_per_cycle": e0.elapsed_time(e1) / steps, "levels": len(levels), "ndof": levels[0].ndof}
+        ms = timed(lambda st: _lib.check(L.hdg_mg_cycle(mg.handle, b.data_ptr(), x.data_ptr(), x.data_ptr(), 2, 2, 1,
+                                                        1, st.cuda_stream)))
+        rec = {"ms_per_cycle": ms, "levels": len(levels), "ndof": levels[0].ndof,
+               "record_levels": int(L.hdg_mg_record_levels(mg.handle))}
+        if rec["record_levels"] > 0:
+            sysf = levels[0].system
+            bp = sysf.facet_planes(b).data
+            xp = torch.zeros_like(bp)
+            rms = timed(lambda st: _lib.check(L.hdg_mg_cycle_records(mg.handle, bp.data_ptr(), xp.data_ptr(),
+                                                                     xp.data_ptr(), 2, 2, 1, 1, st.cuda_stream)))
+            nbytes = vcycle_model_bytes(levels)
+            rec["records_resident_ms_per_cycle"] = rms
+            rec["roofline"] = {"bound": "hbm", "model_bytes_per_cycle": nbytes, "floor_ms": nbytes / peak / 1e6,
+                               "frac": nbytes / peak / 1e6 / rms, "peak": peak, "unit": "GB/s",
+                               "frac_reference_layout_api": nbytes / peak / 1e6 / ms}
+            _lib.check(L.hdg_mg_set_records(mg.handle, 0))
+            rec["reference_layout_cycle_ms"] = timed(lambda st: _lib.check(L.hdg_mg_cycle(
+                mg.handle, b.data_ptr(), x.data_ptr(), x.data_ptr(), 2, 2, 1, 1, st.cuda_stream)))
+            _lib.check(L.hdg_mg_set_records(mg.handle, 1))
+        out[name] = rec
     return out
 
 

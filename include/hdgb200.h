@@ -190,6 +190,11 @@ int hdg_mg_set_fused_tail(hdg_mg* mg, int enable);
  * cycle (0: reference layout). */
 int hdg_mg_set_records(hdg_mg* mg, int mode);
 int hdg_mg_record_levels(const hdg_mg* mg);
+/* hdg_mg_cycle on vectors that already live as facet records of level 0 (hdg_soa_pack): no
+ * pack / unpack at the cycle's boundary; the last sweep writes x_rec directly.  Needs record
+ * levels (HDG_ESTATE otherwise).  x0_rec may be NULL (zero guess) and may alias x_rec. */
+int hdg_mg_cycle_records(hdg_mg* mg, const double* b_rec, const double* x0_rec, double* x_rec, int nu1,
+                         int nu2, int visits, int use_graph, void* stream);
 /* x = cycle(b, x0) with nu1/nu2 smoothing sweeps (FSAI if attached to the level, else
  * block-Jacobi), visits = 1 (V) or 2 (W).
  * x0 may be NULL (zero initial guess, as v_cycle(x0=None)).  x may alias x0.

@@ -62,6 +62,8 @@ SIGNATURES = [
     ("hdg_mg_set_fused_tail", c_int, [c_void_p, c_int]),
     ("hdg_mg_set_records", c_int, [c_void_p, c_int]),
     ("hdg_mg_record_levels", c_int, [c_void_p]),
+    ("hdg_mg_cycle_records", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
+                                     c_void_p]),
     ("hdg_fsai_rows", c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int32,
                               ctypes.POINTER(c_int64), c_void_p]),
     ("hdg_mg_cycle", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,

@@ -1392,7 +1392,7 @@ static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1
 // multigrid.py:393-406 on facet records: level-k right-hand side b and iterate x_in (null: zero) are
 // records; the result is left in one of the level's two buffers, returned through x_out
 static int cycle_rec_soa(hdg_mg* mg, int k, const double* b, const double* x_in, double** x_out, int nu1, int nu2,
-                         int visits, cudaStream_t s) {
+                         int visits, cudaStream_t s, double* final_out = nullptr) {
   hdg_level* L = mg->L[k];
   double* const A = mg->Xr[k];
   double* const Bf = mg->Tr[k];
@@ -1424,7 +1424,7 @@ static int cycle_rec_soa(hdg_mg* mg, int k, const double* b, const double* x_in,
     for (int v = 0; v < visits; ++v)
       if ((rc = cycle_rec_soa(mg, k + 1, mg->Br[k + 1], xc, &xc, nu1, nu2, visits, s))) return rc;
     if (nu2 >= 1 && mg->rec_fuse_prolong) {
-      double* out = other(cur);
+      double* out = (final_out && nu2 == 1 && final_out != cur && final_out != b) ? final_out : other(cur);
       if ((rc = soa_cyc_sweep(L, SOA_EPI_BJ, cur, b, out, bj_weight(L, 1, nu2), 0.0, T->pa.V, xc, s))) return rc;
       cur = out;
       post0 = 1;
@@ -1439,9 +1439,14 @@ static int cycle_rec_soa(hdg_mg* mg, int k, const double* b, const double* x_in,
     if ((rc = soa_cyc_h_prolong(L, T->ha, mg->X[k + 1], const_cast<double*>(cur), s))) return rc;
   }
   for (int it = post0; it < nu2; ++it) {
-    double* out = other(cur);
+    // the caller's result buffer receives the last sweep directly
+    double* out = (final_out && it == nu2 - 1 && final_out != cur && final_out != b) ? final_out : other(cur);
     if ((rc = soa_cyc_sweep(L, SOA_EPI_BJ, cur, b, out, bj_weight(L, it + 1, nu2), 0.0, nullptr, nullptr, s))) return rc;
     cur = out;
+  }
+  if (final_out && cur != final_out) {
+    CK(cudaMemcpyAsync(final_out, cur, sizeof(double) * (size_t)soa_len(L), cudaMemcpyDeviceToDevice, s));
+    cur = final_out;
   }
   *x_out = const_cast<double*>(cur);
   return 0;
@@ -1480,8 +1485,20 @@ static void refresh_graphs(hdg_mg* mg) {
   }
 }
 
-int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int nu1, int nu2, int visits,
-                 int use_graph, void* stream) {
+// records = true: b, x0, x are facet records of level 0 (no pack / unpack at the boundary)
+static int cycle_issue_any(hdg_mg* mg, bool records, const double* b, const double* x0, double* x, int nu1, int nu2,
+                           int visits, cudaStream_t s) {
+  if (!records) return cycle_issue(mg, b, x0, x, nu1, nu2, visits, s);
+  if (x0 && nu1 == 0) {   // no pre-sweep: the correction would be added to the caller's x0 in place
+    CK(cudaMemcpyAsync(mg->Xr[0], x0, sizeof(double) * (size_t)soa_len(mg->L[0]), cudaMemcpyDeviceToDevice, s));
+    x0 = mg->Xr[0];
+  }
+  double* res = nullptr;
+  return cycle_rec_soa(mg, 0, b, x0, &res, nu1, nu2, visits, s, x);
+}
+
+static int run_cycle(hdg_mg* mg, bool records, const double* b, const double* x0, double* x, int nu1, int nu2,
+                     int visits, int use_graph, void* stream) {
   if (!mg || !b || !x) return fail(HDG_EINVAL, "null argument");
   refresh_graphs(mg);
   if (nu1 < 0 || nu2 < 0 || visits < 1) return fail(HDG_EINVAL, "bad cycle parameters");
@@ -1489,14 +1506,23 @@ int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int n
   cudaStream_t s = S(stream);
   int rc0 = tail_prepare(mg);
   if (rc0) return rc0;
+  const int m0 = mg->rec_m;
   if ((rc0 = rec_prepare(mg))) return rc0;
-  if (!use_graph) return cycle_issue(mg, b, x0, x, nu1, nu2, visits, s);
-  auto key = std::make_tuple((const void*)b, (const void*)x0, (void*)x, nu1, nu2, visits);
+  if (m0 != mg->rec_m) {                       // the record levels changed: cached graphs are stale
+    for (auto& kv : mg->graphs) cudaGraphExecDestroy(kv.second.exec);
+    mg->graphs.clear();
+  }
+  if (records) {
+    if (mg->rec_m == 0) return fail(HDG_ESTATE, "this hierarchy has no record levels (hdg_mg_set_records)");
+    if (b == x) return fail(HDG_EINVAL, "record cycle: x must not alias b");
+  }
+  if (!use_graph) return cycle_issue_any(mg, records, b, x0, x, nu1, nu2, visits, s);
+  auto key = std::make_tuple((const void*)b, (const void*)x0, (void*)x, nu1, nu2, records ? -visits : visits);
   auto it = mg->graphs.find(key);
   if (it == mg->graphs.end()) {
     const long long c0 = g_launches.load();
     CK(cudaStreamBeginCapture(mg->cs, cudaStreamCaptureModeThreadLocal));
-    int rc = cycle_issue(mg, b, x0, x, nu1, nu2, visits, mg->cs);
+    int rc = cycle_issue_any(mg, records, b, x0, x, nu1, nu2, visits, mg->cs);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(mg->cs, &g);
     if (rc) { if (g) cudaGraphDestroy(g); return rc; }
@@ -1521,6 +1547,16 @@ int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int n
   CK(cudaGraphLaunch(it->second.exec, s));
   g_launches.fetch_add(it->second.nkern);
   return 0;
+}
+
+int hdg_mg_cycle(hdg_mg* mg, const double* b, const double* x0, double* x, int nu1, int nu2, int visits,
+                 int use_graph, void* stream) {
+  return run_cycle(mg, false, b, x0, x, nu1, nu2, visits, use_graph, stream);
+}
+
+int hdg_mg_cycle_records(hdg_mg* mg, const double* b_rec, const double* x0_rec, double* x_rec, int nu1, int nu2,
+                         int visits, int use_graph, void* stream) {
+  return run_cycle(mg, true, b_rec, x0_rec, x_rec, nu1, nu2, visits, use_graph, stream);
 }
 
 int64_t hdg_mg_graph_captures(const hdg_mg* mg) { return mg ? mg->graph_captures : -1; }
@@ -1821,9 +1857,8 @@ int hdg_soa_pack(hdg_level* L, const double* x, double* xs, void* stream) {
   if (!L || (!x && L->ndof) || !xs) return fail(HDG_EINVAL, "null argument");
   int rc = soa_prepare(L);
   if (rc) return rc;
-  const long long total = soa_len(L);
-  const unsigned grid = (unsigned)((total + 255) / 256);
-#define SOA_PACK(N) { soa_pack_kernel<N><<<grid, 256, 0, S(stream)>>>(x, xs, L->nx, L->ny, L->soaW, L->nh, total); CKL(); return 0; }
+  const unsigned grid = (unsigned)(L->soaW * ((L->ny + 1 + SOA_PB - 1) / SOA_PB));
+#define SOA_PACK(N) { soa_pack_blocked_kernel<N><<<grid, 256, 0, S(stream)>>>(x, xs, L->nx, L->ny, L->soaW, L->nh); CKL(); return 0; }
   switch (L->n1) {
     case 2: SOA_PACK(2) case 3: SOA_PACK(3) case 4: SOA_PACK(4) case 5: SOA_PACK(5)
     case 6: SOA_PACK(6) case 7: SOA_PACK(7) case 8: SOA_PACK(8) case 9: SOA_PACK(9)
@@ -1837,8 +1872,8 @@ int hdg_soa_unpack(hdg_level* L, const double* xs, double* x, void* stream) {
   int rc = soa_prepare(L);
   if (rc) return rc;
   if (L->ndof == 0) return 0;
-  const unsigned grid = (unsigned)((L->ndof + 255) / 256);
-#define SOA_UNPACK(N) { soa_unpack_kernel<N><<<grid, 256, 0, S(stream)>>>(xs, x, L->nx, L->ny, L->soaW, L->nh, L->ndof); CKL(); return 0; }
+  const unsigned grid = (unsigned)(L->soaW * ((L->ny + 1 + SOA_PB - 1) / SOA_PB));
+#define SOA_UNPACK(N) { soa_unpack_blocked_kernel<N><<<grid, 256, 0, S(stream)>>>(xs, x, L->nx, L->ny, L->soaW, L->nh); CKL(); return 0; }
   switch (L->n1) {
     case 2: SOA_UNPACK(2) case 3: SOA_UNPACK(3) case 4: SOA_UNPACK(4) case 5: SOA_UNPACK(5)
     case 6: SOA_UNPACK(6) case 7: SOA_UNPACK(7) case 8: SOA_UNPACK(8) case 9: SOA_UNPACK(9)

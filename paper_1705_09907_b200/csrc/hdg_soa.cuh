@@ -520,4 +520,79 @@ __global__ void soa_unpack_kernel(const double* __restrict__ xs, double* __restr
   x[u] = xs[src];
 }
 
+// Blocked pack / unpack: one CTA moves SOA_PB consecutive records of one tile through shared
+// memory, so the reference-layout side is read / written as contiguous runs (a horizontal line
+// segment of 32 columns = 32 N1 doubles; SOA_PB rows of one vertical line = SOA_PB N1 doubles) and
+// the record side as whole records.
+constexpr int SOA_PB = 8;
+
+template <int N1>
+__global__ void __launch_bounds__(256) soa_pack_blocked_kernel(const double* __restrict__ x, double* __restrict__ xs,
+                                                               int nx, int ny, int W, long long nh) {
+  using C = SoaCfg<N1>;
+  constexpr int ENT = C::ENT, VOFF = C::VOFF, EOFF = C::EOFF, EB = C::EB;
+  __shared__ __align__(16) double S[SOA_PB * ENT];
+  // row blocks fastest: CTAs running together read neighbouring pieces of the same vertical lines
+  const int nrb = (ny + SOA_PB) / SOA_PB;
+  const int w = blockIdx.x / nrb, R0 = (blockIdx.x % nrb) * SOA_PB;
+  const int nr = min(SOA_PB, ny + 1 - R0);
+  for (int t = threadIdx.x; t < SOA_PB * ENT; t += blockDim.x) S[t] = 0.0;
+  __syncthreads();
+  // H: record R0 + rr holds line R0 + rr, columns 31 w .. 31 w + 31: one contiguous source run per line
+  const int ncol = min(32, nx - 31 * w), hl = ncol * N1;
+  for (int t = threadIdx.x; t < nr * hl; t += blockDim.x) {
+    const int rr = t / hl, u = t - rr * hl, R = R0 + rr;
+    if (R < 1 || R > ny - 1) continue;
+    S[rr * ENT + (u % N1) * 32 + u / N1] = __ldg(x + ((long long)(R - 1) * nx + 31 * w) * N1 + u);
+  }
+  // V: lines 31 w .. 31 w + 32 (first / last are the edge-in lines), element rows [ra, rb): one
+  // contiguous source run of (rb - ra) N1 doubles per line
+  const int ra = max(R0 - 1, 0), rb = R0 + nr - 1;
+  const int len = max(rb - ra, 0) * N1;
+  for (int t = threadIdx.x; t < 33 * len; t += blockDim.x) {
+    const int l = t / len, u = t - l * len, line = 31 * w + l;
+    if (line < 1 || line > nx - 1) continue;
+    const int rr = ra + u / N1 + 1 - R0, k = u % N1;
+    const int o = l == 0 ? EOFF + k : (l == 32 ? EOFF + EB + k : VOFF + k * 31 + (l - 1));
+    S[rr * ENT + o] = __ldg(x + (nh + (long long)(line - 1) * ny + ra) * N1 + u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nr * ENT; t += blockDim.x) {
+    const int rr = t / ENT, o = t - rr * ENT;
+    xs[((long long)(R0 + rr) * W + w) * ENT + o] = S[t];
+  }
+}
+
+template <int N1>
+__global__ void __launch_bounds__(256) soa_unpack_blocked_kernel(const double* __restrict__ xs, double* __restrict__ x,
+                                                                 int nx, int ny, int W, long long nh) {
+  using C = SoaCfg<N1>;
+  constexpr int ENT = C::ENT, VOFF = C::VOFF;
+  __shared__ __align__(16) double S[SOA_PB * ENT];
+  // row blocks fastest: CTAs running together read neighbouring pieces of the same vertical lines
+  const int nrb = (ny + SOA_PB) / SOA_PB;
+  const int w = blockIdx.x / nrb, R0 = (blockIdx.x % nrb) * SOA_PB;
+  const int nr = min(SOA_PB, ny + 1 - R0);
+  for (int t = threadIdx.x; t < nr * ENT; t += blockDim.x) {
+    const int rr = t / ENT, o = t - rr * ENT;
+    S[t] = __ldg(xs + ((long long)(R0 + rr) * W + w) * ENT + o);
+  }
+  __syncthreads();
+  // H columns 31 w .. 31 w + 30 (the last tile also its 32nd column)
+  const int ncol = min(w == W - 1 ? 32 : 31, nx - 31 * w), hl = ncol * N1;
+  for (int t = threadIdx.x; t < nr * hl; t += blockDim.x) {
+    const int rr = t / hl, u = t - rr * hl, R = R0 + rr;
+    if (R < 1 || R > ny - 1) continue;
+    x[((long long)(R - 1) * nx + 31 * w) * N1 + u] = S[rr * ENT + (u % N1) * 32 + u / N1];
+  }
+  const int ra = max(R0 - 1, 0), rb = R0 + nr - 1;
+  const int len = max(rb - ra, 0) * N1;
+  for (int t = threadIdx.x; t < 31 * len; t += blockDim.x) {
+    const int l = t / len + 1, u = t - (l - 1) * len, line = 31 * w + l;
+    if (line > nx - 1) continue;
+    const int rr = ra + u / N1 + 1 - R0, k = u % N1;
+    x[(nh + (long long)(line - 1) * ny + ra) * N1 + u] = S[rr * ENT + VOFF + k * 31 + (l - 1)];
+  }
+}
+
 }  // namespace hdg

@@ -609,6 +609,18 @@ def v_cycle(levels, b, x0=None, nu1=2, nu2=2):
     return _run_cycle(levels, b, x0, nu1, nu2, 1)
 
 
+def cycle_records(levels, b, x0=None, nu1=2, nu2=2, visits=1, out=None):
+    """One cycle (multigrid.py:393-406) on vectors held as facet records of the fine level
+    (TraceSystem.facet_planes): FacetPlanes in, FacetPlanes out, no layout change at the boundary
+    (hdgb200.h: hdg_mg_cycle_records).  The hierarchy needs record levels (set_records)."""
+    from .trace import FacetPlanes
+    mg = _native_mg(levels)
+    x = dev.empty(b.data.numel()) if out is None else out.data
+    check(lib.hdg_mg_cycle_records(mg.handle, dev.ptr(b.data), dev.ptr(None if x0 is None else x0.data), dev.ptr(x),
+                                   int(nu1), int(nu2), int(visits), 1, dev.stream()))
+    return FacetPlanes(b.system, x) if out is None else out
+
+
 def w_cycle(levels, b, x0=None, nu1=2, nu2=2):
     """multigrid.py:415-418."""
     return _run_cycle(levels, b, x0, nu1, nu2, 2)

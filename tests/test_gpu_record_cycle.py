@@ -113,3 +113,26 @@ def test_record_cycle_full_size_configs1(P):
     assert err < 1e-12
     r = b - levels[0].system.matvec_free(x)
     assert float(r.norm() / b.norm()) < 0.5
+
+
+@pytest.mark.parametrize("nx,ny,p,nu1,nu2,visits", [(64, 64, 4, 2, 2, 1), (40, 24, 3, 0, 1, 1), (32, 32, 2, 1, 0, 2),
+                                                   (16, 16, 1, 0, 2, 1)])
+def test_cycle_on_resident_records(P, nx, ny, p, nu1, nu2, visits):
+    """hdg_mg_cycle_records: b and x stay facet records; x0 is not mutated, x may alias x0."""
+    levels, lo = _hier(P, nx, ny, p)
+    P.mg.set_records(levels, 2)
+    sysf = levels[0].system
+    rng = np.random.default_rng(11)
+    b, x0 = rng.uniform(-1, 1, sysf.ndof), rng.standard_normal(sysf.ndof)
+    P.mg.v_cycle(levels, b)                                   # sets the record levels up
+    bp, x0p = sysf.facet_planes(b), sysf.facet_planes(x0)
+    x = P.mg.cycle_records(levels, bp, None, nu1, nu2, visits).numpy()
+    assert rel(x, O.cycle(lo, 0, b, np.zeros_like(b), nu1, nu2, visits)) < TOL
+    xo = O.cycle(lo, 0, b, x0.copy(), nu1, nu2, visits)
+    x2 = P.mg.cycle_records(levels, bp, x0p, nu1, nu2, visits)
+    assert rel(x2.numpy(), xo) < TOL
+    np.testing.assert_array_equal(x0p.numpy(), x0)            # x0 untouched
+    P.mg.cycle_records(levels, bp, x0p, nu1, nu2, visits, out=x0p)   # in place
+    assert rel(x0p.numpy(), xo) < TOL
+    np.testing.assert_array_equal(bp.numpy(), b)
+    P.mg.set_records(levels, 1)
