@@ -234,6 +234,46 @@ int hdg_cg_update(double* x, double* r, const double* d, const double* ad, doubl
 /* d = z + beta d  (trace.py:161) */
 int hdg_xpby(const double* z, double beta, double* d, int64_t n, void* stream);
 
+/* ---------------------------------------------------------------- setup / post-solve kernels
+ * the batched steps either side of the solve.  All pointers are
+ * device pointers (fp64, row-major), one CTA per element unless noted.
+ *
+ * hdg_condense_piecewise: local.py:133-237 (local_blocks + assemble_local + condense) for an
+ *   element-wise constant coefficient (isotropic or diagonal: kx, ky per element) and uniform tau,
+ *   by eliminating the flux first: H = Stab + kx Lap0 + ky Lap1 (nb x nb, SPD) is eliminated on
+ *   the augmented matrix [H | B], B = Tu - kx G0 - ky G1, in shared memory and
+ *   S = kx A00 + ky A01 + Ms - B^T H^-1 B  (m = 4 (p+1), nb = (p+1)^2, S_out: E x m x m).
+ *   *status (device int) is set to 1 on a non-positive pivot (NumericalBreakdown, local.py:27).
+ * hdg_piecewise_usolve: rhs_e <- H(K_e)^-1 rhs_e in place (E x nb): the potential solve of
+ *   condensed loads (local.py:236) and of the volume reconstruction (local.py:240-251).
+ * hdg_gemm_nt: C = beta C + alpha diag(rowscale) ((A * colscale / adiv) B^T), A: E x J (lda), B: I x J,
+ *   C: E x I (ldc); rowscale (E), colscale (J), adiv (E x J, ldad) may be NULL.  The shared-matrix
+ *   products of reconstruct_all / postprocess_all (trace.py:171-185, local.py:282-299) and of the
+ *   load condensation.
+ * hdg_class_gemv: out_e = beta out_e + alpha M[cls_e] in_e with class-indexed I x J matrices
+ *   (reconstruct_all with several element classes).
+ * hdg_galerkin_p: S_c = Q^T S Q, Q = I_4 (x) V (multigrid.py:328-334 in element form);
+ *   V: n1 x n1c.  hdg_galerkin_h: S_c = sum_k Q_k^T S_k Q_k over the 4 children at p = 1
+ *   (S_children: C x 4 x 8 x 8; Q: C x 4 x 8 x 8, or one set when shared_q).
+ * hdg_gather_elements: trace.py:81-85 for every element, lam_e: E x 4 (p+1), 0 on Dirichlet sides.
+ * hdg_sum_owners: trace.py:67 / 73-79, rhs_f = cl[E1, side1] + cl[E2, side2] (slot-0 owner first). */
+int hdg_condense_piecewise(int nb, int m, int64_t E, const double* kx, const double* ky, const double* stab,
+                           const double* lap0, const double* lap1, const double* tu, const double* g0,
+                           const double* g1, const double* a00, const double* a01, const double* ms,
+                           double* S_out, int* status, void* stream);
+int hdg_piecewise_usolve(int nb, int64_t E, const double* kx, const double* ky, const double* stab,
+                         const double* lap0, const double* lap1, double* rhs, int* status, void* stream);
+int hdg_gemm_nt(int64_t E, int I, int J, const double* A, int lda, const double* B, double* C, int ldc,
+                const double* rowscale, const double* colscale, const double* adiv, int ldad, double alpha,
+                double beta, void* stream);
+int hdg_class_gemv(int64_t E, int I, int J, const int64_t* cls, const double* M, const double* in, int ldi,
+                   double* out, int ldo, double alpha, double beta, void* stream);
+int hdg_galerkin_p(int64_t E, int n1, int n1c, const double* S, const double* V, double* S_coarse, void* stream);
+int hdg_galerkin_h(int64_t C, const double* S_children, const double* Q, int shared_q, double* S_coarse,
+                   void* stream);
+int hdg_gather_elements(int nx, int ny, int p, const double* lam, double* lam_e, void* stream);
+int hdg_sum_owners(int nx, int ny, int p, const double* cl, double* rhs, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

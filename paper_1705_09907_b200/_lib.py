@@ -77,6 +77,16 @@ SIGNATURES = [
     ("hdg_dot", c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     ("hdg_cg_update", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, ctypes.c_double, c_int64, c_void_p]),
     ("hdg_xpby", c_int, [c_void_p, ctypes.c_double, c_void_p, c_int64, c_void_p]),
+    ("hdg_condense_piecewise", c_int, [c_int, c_int, c_int64] + [c_void_p] * 14),
+    ("hdg_piecewise_usolve", c_int, [c_int, c_int64] + [c_void_p] * 8),
+    ("hdg_gemm_nt", c_int, [c_int64, c_int, c_int, c_void_p, c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
+                            c_void_p, c_int, ctypes.c_double, ctypes.c_double, c_void_p]),
+    ("hdg_class_gemv", c_int, [c_int64, c_int, c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int,
+                               ctypes.c_double, ctypes.c_double, c_void_p]),
+    ("hdg_galerkin_p", c_int, [c_int64, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("hdg_galerkin_h", c_int, [c_int64, c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
+    ("hdg_gather_elements", c_int, [c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    ("hdg_sum_owners", c_int, [c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
 ]
 
 

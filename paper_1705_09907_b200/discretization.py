@@ -197,6 +197,39 @@ class NumericalBreakdown(RuntimeError):
     """local.py:27."""
 
 
+# ------------------------------------------------------------------ device kernel wrappers
+# torch allocates and views; the arithmetic is the hand-written kernels of csrc/hdg_setup.cu.
+
+def gemm_nt(A, B, out=None, rowscale=None, colscale=None, adiv=None, alpha=1.0, beta=0.0):
+    """out = beta out + alpha diag(rowscale) ((A * colscale / adiv) B^T) on the device
+    (hdgb200.h: hdg_gemm_nt).  A (E, J) and out (E, I) may be column slices of wider row-major
+    tensors (unit column stride); B (I, J) contiguous."""
+    import torch
+    from . import _device as dev
+    from ._lib import check, lib
+    E, J = A.shape
+    B = B.contiguous()
+    I = B.shape[0]
+    assert B.shape[1] == J and A.stride(1) == 1
+    if out is None:
+        out = torch.empty((E, I), dtype=torch.float64, device=A.device)
+        beta = 0.0
+    assert out.shape == (E, I) and out.stride(1) == 1
+    if adiv is not None:
+        assert adiv.shape == (E, J) and adiv.stride(1) == 1
+    check(lib.hdg_gemm_nt(E, I, J, A.data_ptr(), A.stride(0) if E > 1 else J, B.data_ptr(), out.data_ptr(),
+                          out.stride(0) if E > 1 else I, dev.ptr(rowscale), dev.ptr(colscale), dev.ptr(adiv),
+                          0 if adiv is None else (adiv.stride(0) if E > 1 else J), float(alpha), float(beta),
+                          dev.stream()))
+    return out
+
+
+def _status_check(status, what):
+    if int(status.item()) != 0:
+        raise NumericalBreakdown(f"{what}: non-positive pivot in an element's potential block")
+
+
+
 class PiecewiseCondenser:
     """Batched condensation on the GPU for elements with an element-wise CONSTANT coefficient
     K_e and uniform tau (configs 3/5-style heterogeneous media).
@@ -256,11 +289,11 @@ class PiecewiseCondenser:
         if not hasattr(self, "_t"):
             T = {}
             for k in ("stab", "Tu", "Fu", "Ms"):
-                T[k] = torch.as_tensor(getattr(self, k), device="cuda")
+                T[k] = torch.as_tensor(np.ascontiguousarray(getattr(self, k)), device="cuda")
             for k in ("Mi", "Tq"):
-                T[k] = torch.as_tensor(getattr(self, k), device="cuda")
+                T[k] = torch.as_tensor(np.ascontiguousarray(getattr(self, k)), device="cuda")
             for k in ("Lapd", "Gd", "A0d", "C0d", "BMid", "FqMid", "MiBt"):
-                T[k] = [torch.as_tensor(m, device="cuda") for m in getattr(self, k)]
+                T[k] = [torch.as_tensor(np.ascontiguousarray(m), device="cuda") for m in getattr(self, k)]
             self._t = T
         return self._t
 
@@ -271,58 +304,95 @@ class PiecewiseCondenser:
         K = np.asarray(K, float)
         return K, K
 
-    def condensed_loads(self, K, load_q, load_u, chunk=1 << 16):
-        """F L(K)^-1 [load_q; load_u] per element (local.py:236), the same elimination."""
+    def _kpair(self, K):
+        import torch
+        kx, ky = (torch.as_tensor(k, dtype=torch.float64, device="cuda").contiguous() for k in self._pair(K))
+        return kx, ky
+
+    def _usolve(self, kx, ky, rhs):
+        """rhs_e <- (Stab + kx Lap_x + ky Lap_y)^-1 rhs_e in place (hdgb200.h: hdg_piecewise_usolve)."""
+        import torch
+        from . import _device as dev
+        from ._lib import check, lib
+        t = self._dev()
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        check(lib.hdg_piecewise_usolve(self.nb, kx.numel(), kx.data_ptr(), ky.data_ptr(), t["stab"].data_ptr(),
+                                       t["Lapd"][0].data_ptr(), t["Lapd"][1].data_ptr(), rhs.data_ptr(),
+                                       status.data_ptr(), dev.stream()))
+        _status_check(status, "potential solve")
+        return rhs
+
+    def condensed_loads(self, K, load_q, load_u):
+        return self.condensed_loads_device(K, load_q, load_u).cpu().numpy()
+
+    def condensed_loads_device(self, K, load_q, load_u):
+        """F L(K)^-1 [load_q; load_u] per element (local.py:236), the same elimination:
+        u = H^-1 (f_u - sum_d K_d B_d M^-1 f_q,d), out = sum_d K_d (F_q,d M^-1 f_q,d + C_d u) + F_u u."""
         import torch
         t = self._dev()
-        kx, ky = (torch.as_tensor(k, device="cuda") for k in self._pair(K))
-        fq = torch.as_tensor(load_q, device="cuda")
-        fu = torch.as_tensor(load_u, device="cuda")
+        k = self._kpair(K)
+        fq = torch.as_tensor(load_q, dtype=torch.float64, device="cuda").contiguous()
+        rhs = torch.as_tensor(load_u, dtype=torch.float64, device="cuda").clone().contiguous()
         nb = self.nb
-        out = torch.empty((kx.numel(), 4 * self.n1), dtype=torch.float64, device="cuda")
-        for s0 in range(0, kx.numel(), chunk):
-            k = (kx[s0:s0 + chunk][:, None], ky[s0:s0 + chunk][:, None])
-            f = (fq[s0:s0 + chunk, :nb], fq[s0:s0 + chunk, nb:])
-            H = t["stab"] + sum(k[d][:, :, None] * t["Lapd"][d] for d in range(2))
-            rhs = fu[s0:s0 + chunk] - sum(k[d] * (f[d] @ t["BMid"][d].T) for d in range(2))
-            u = torch.linalg.solve(H, rhs[:, :, None])[:, :, 0]
-            out[s0:s0 + chunk] = sum(k[d] * (f[d] @ t["FqMid"][d].T) + k[d] * (u @ t["C0d"][d].T)
-                                     for d in range(2)) + u @ t["Fu"].T
-        return out.cpu().numpy()
+        f = (fq[:, :nb], fq[:, nb:])
+        for d in range(2):
+            gemm_nt(f[d], t["BMid"][d], out=rhs, rowscale=k[d], alpha=-1.0, beta=1.0)
+        u = self._usolve(k[0], k[1], rhs)
+        out = gemm_nt(u, t["Fu"])
+        for d in range(2):
+            gemm_nt(f[d], t["FqMid"][d], out=out, rowscale=k[d], beta=1.0)
+            gemm_nt(u, t["C0d"][d], out=out, rowscale=k[d], beta=1.0)
+        return out
 
-    def reconstruct(self, K, load, lam_e, chunk=1 << 16):
+    def reconstruct(self, K, load, lam_e):
         """(q, u) of every element from its trace values (local.py:240-251) by the same
         elimination: f = load - T lam_e, (Stab + sum_d K_d Lap_d) u = f_u - sum_d K_d B_d M^-1 f_q,d,
         q_d = K_d M^-1 (f_q,d + B_d^T u).  load (E, 3nb), lam_e (E, 4n1) CUDA tensors."""
         import torch
         t = self._dev()
-        kx, ky = (torch.as_tensor(k, device="cuda") for k in self._pair(K))
-        nb, E = self.nb, kx.numel()
+        k = self._kpair(K)
+        nb, E = self.nb, k[0].numel()
+        f = load.clone()
+        gemm_nt(lam_e, t["Tq"], out=f[:, :2 * nb], alpha=-1.0, beta=1.0)
+        gemm_nt(lam_e, t["Tu"], out=f[:, 2 * nb:], alpha=-1.0, beta=1.0)
+        fd = (f[:, :nb], f[:, nb:2 * nb])
+        u = f[:, 2 * nb:].contiguous()
+        for d in range(2):
+            gemm_nt(fd[d], t["BMid"][d], out=u, rowscale=k[d], alpha=-1.0, beta=1.0)
+        self._usolve(k[0], k[1], u)
         q = torch.empty((E, 2 * nb), dtype=torch.float64, device="cuda")
-        u = torch.empty((E, nb), dtype=torch.float64, device="cuda")
-        for s0 in range(0, E, chunk):
-            sl = slice(s0, min(E, s0 + chunk))
-            k = (kx[sl][:, None], ky[sl][:, None])
-            lam = lam_e[sl]
-            fq = load[sl, :2 * nb] - lam @ t["Tq"].T
-            fu = load[sl, 2 * nb:] - lam @ t["Tu"].T
-            f = (fq[:, :nb], fq[:, nb:])
-            H = t["stab"] + sum(k[d][:, :, None] * t["Lapd"][d] for d in range(2))
-            rhs = fu - sum(k[d] * (f[d] @ t["BMid"][d].T) for d in range(2))
-            uu = torch.linalg.solve(H, rhs[:, :, None])[:, :, 0]
-            u[sl] = uu
-            for d in range(2):
-                q[sl, d * nb:(d + 1) * nb] = k[d] * (f[d] @ t["Mi"].T + uu @ t["MiBt"][d].T)
+        for d in range(2):
+            qd = q[:, d * nb:(d + 1) * nb]
+            gemm_nt(fd[d], t["Mi"], out=qd, rowscale=k[d])
+            gemm_nt(u, t["MiBt"][d], out=qd, rowscale=k[d], beta=1.0)
         return q, u
 
-    def blocks(self, K, chunk=1 << 15):
-        """S for every element; K: (E,) isotropic or a (Kxx, Kyy) pair of (E,) arrays."""
+    def blocks(self, K):
+        """S for every element; K: (E,) isotropic or a (Kxx, Kyy) pair of (E,) arrays.  One CTA per
+        element eliminates [H | B] in shared memory (hdgb200.h: hdg_condense_piecewise); orders
+        whose augmented matrix exceeds shared memory (p = 12) use the batched library solve."""
+        import torch
+        from . import _device as dev
+        from ._lib import check, lib
+        t = self._dev()
+        kx, ky = self._kpair(K)
+        E, m, nb = kx.numel(), 4 * self.n1, self.nb
+        out = torch.empty((E, m, m), dtype=torch.float64, device="cuda")
+        if 8 * (nb * ((nb + m) | 1) + nb) > 227 * 1024:
+            return self._blocks_library(kx, ky, out)
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        check(lib.hdg_condense_piecewise(nb, m, E, kx.data_ptr(), ky.data_ptr(), t["stab"].data_ptr(),
+                                         t["Lapd"][0].data_ptr(), t["Lapd"][1].data_ptr(), t["Tu"].data_ptr(),
+                                         t["Gd"][0].data_ptr(), t["Gd"][1].data_ptr(), t["A0d"][0].data_ptr(),
+                                         t["A0d"][1].data_ptr(), t["Ms"].data_ptr(), out.data_ptr(),
+                                         status.data_ptr(), dev.stream()))
+        _status_check(status, "local condensation")
+        return out
+
+    def _blocks_library(self, kx, ky, out, chunk=1 << 13):
         import torch
         t = self._dev()
-        kx, ky = (torch.as_tensor(k, device="cuda") for k in self._pair(K))
-        E = kx.numel()
-        out = torch.empty((E, 4 * self.n1, 4 * self.n1), dtype=torch.float64, device="cuda")
-        for s0 in range(0, E, chunk):
+        for s0 in range(0, kx.numel(), chunk):
             k = (kx[s0:s0 + chunk][:, None, None], ky[s0:s0 + chunk][:, None, None])
             H = t["stab"] + sum(k[d] * t["Lapd"][d] for d in range(2))
             U = torch.linalg.solve(H, t["Tu"] - sum(k[d] * t["Gd"][d] for d in range(2)))
@@ -384,10 +454,13 @@ def galerkin_p(S, V):
     Q = np.kron(np.eye(4), V)
     if not isinstance(S, np.ndarray):
         import torch
-        Qt = torch.as_tensor(Q, device=S.device)
-        out = torch.empty((S.shape[0], Q.shape[1], Q.shape[1]), dtype=S.dtype, device=S.device)
-        for s0 in range(0, S.shape[0], 1 << 16):
-            out[s0:s0 + (1 << 16)] = Qt.T @ S[s0:s0 + (1 << 16)] @ Qt
+        from . import _device as dev
+        from ._lib import check, lib
+        S = S.contiguous()
+        n1, n1c = V.shape
+        Vd = torch.as_tensor(np.ascontiguousarray(V, dtype=np.float64), device=S.device)
+        out = torch.empty((S.shape[0], 4 * n1c, 4 * n1c), dtype=torch.float64, device=S.device)
+        check(lib.hdg_galerkin_p(S.shape[0], n1, n1c, S.data_ptr(), Vd.data_ptr(), out.data_ptr(), dev.stream()))
         return out
     return np.einsum("ai,cij,jb->cab", Q.T, S, Q)
 
@@ -440,6 +513,14 @@ def galerkin_h(S_children, Q):
     """S_c = sum_k Q_k^T S_k Q_k.  S_children (C, 4, 8, 8), Q (C, 4, 8, 8)."""
     if not isinstance(S_children, np.ndarray):
         import torch
-        Qt = torch.as_tensor(Q, device=S_children.device)
-        return torch.einsum("ckia,ckij,ckjb->cab", Qt, S_children, Qt)
+        from . import _device as dev
+        from ._lib import check, lib
+        Sc = S_children.contiguous()
+        C = Sc.shape[0]
+        Qt = torch.as_tensor(Q, dtype=torch.float64, device=Sc.device).contiguous()
+        shared = int(Qt.shape[0] == 1 and C != 1)
+        assert shared or Qt.shape[0] == C
+        out = torch.empty((C, 8, 8), dtype=torch.float64, device=Sc.device)
+        check(lib.hdg_galerkin_h(C, Sc.data_ptr(), Qt.data_ptr(), shared, out.data_ptr(), dev.stream()))
+        return out
     return np.einsum("ckia,ckij,ckjb->cab", Q, S_children, Q)

@@ -459,6 +459,13 @@ class TraceSystem:
             load = np.zeros((fs.shape[0], 3 * nb))
             load[:, 2 * nb:] = (fs * wj) @ ref.interp_2d
             yield np.arange(e0, e0 + fs.shape[0]), load
+        yield from self._boundary_loads(spec)
+
+    def _boundary_loads(self, spec):
+        """Dirichlet fold of the boundary datum (local.py:179-184): (boundary elements, loads)."""
+        ref = self.ops.ref
+        n1 = ref.n1
+        m = self.mesh
         inner = self.layout.side_mask()
         bnd_e, bnd_s = np.nonzero(~inner)
         if bnd_e.size:
@@ -484,12 +491,65 @@ class TraceSystem:
                     lam_bc[inv, bnd_s * n1 + k] = proj[:, k]
                 yield ub, -np.einsum("eij,ej->ei", self._trace_cols(ub), lam_bc)
 
+    def _element_loads_device(self, spec, chunk=1 << 16):
+        """_element_loads with the loads built on the device: the source load (f w J) interp_2d is
+        a hdg_gemm_nt product of the sampled source; the Dirichlet fold touches boundary elements
+        only and is uploaded.  Yields (element index CUDA tensor, load (n, 3nb) CUDA tensor)."""
+        import torch
+        from .discretization import gemm_nt
+        ref = self.ops.ref
+        nb = ref.nb
+        m = self.mesh
+        E = m.n_x * m.n_y
+        wj = torch.as_tensor(np.ascontiguousarray(ref.w2 * (m.dx * m.dy / 4.0)), device="cuda")
+        interpT = torch.as_tensor(np.ascontiguousarray(ref.interp_2d.T), device="cuda")
+        for e0 in range(0, E, chunk):
+            qx, qy = self._quad_points(e0, min(E, e0 + chunk))
+            fs = np.asarray(spec.source(qx, qy), float).reshape(qx.shape)
+            if not np.any(fs):
+                continue
+            load = torch.zeros((fs.shape[0], 3 * nb), dtype=torch.float64, device="cuda")
+            gemm_nt(torch.as_tensor(np.ascontiguousarray(fs), device="cuda"), interpT, out=load[:, 2 * nb:], colscale=wj)
+            yield torch.arange(e0, e0 + fs.shape[0], device="cuda"), load
+        for idx, ld in self._boundary_loads(spec):
+            yield torch.as_tensor(idx, device="cuda"), torch.as_tensor(np.ascontiguousarray(ld), device="cuda")
+
+    def _condense_loads_device(self, idx, load):
+        """condensed loads (local.py:236) of elements idx (CUDA index tensor), on the device"""
+        import torch
+        from .discretization import gemm_nt
+        nb, n1 = self.ops.nb, self.ops.n1
+        if self.piecewise is not None:
+            K = self.class_K
+            ih = idx.cpu().numpy()
+            K = (K[0][ih], K[1][ih]) if isinstance(K, tuple) else K[ih]
+            return self.piecewise.condensed_loads_device(K, load[:, :2 * nb], load[:, 2 * nb:])
+        Z = torch.as_tensor(np.ascontiguousarray(self.classes.Z), device="cuda")
+        if self.classes.n == 1:
+            return gemm_nt(load, Z[0])
+        cls = torch.as_tensor(self.elem_class, dtype=torch.int64, device="cuda")[idx].contiguous()
+        out = torch.empty((load.shape[0], 4 * n1), dtype=torch.float64, device="cuda")
+        check(lib.hdg_class_gemv(load.shape[0], 4 * n1, 3 * nb, cls.data_ptr(), Z.data_ptr(), load.data_ptr(), 3 * nb,
+                                 out.data_ptr(), 4 * n1, 1.0, 0.0, dev.stream()))
+        return out
+
     def _condensed_rhs(self, spec):
-        """Loads condensed per element (local.py:236), summed over owners (trace.py:67)."""
+        """Loads condensed per element (local.py:236), summed over owners (trace.py:67).  With a
+        GPU: loads, condensation and the owner sum are device kernels (hdg_gemm_nt /
+        hdg_class_gemv / hdg_piecewise_usolve / hdg_sum_owners); without one (CPU-only setup tests)
+        the same arithmetic runs in numpy."""
         n1 = self.ops.n1
         E = self.mesh.n_x * self.mesh.n_y
         if self.ndof == 0:
             return np.zeros(0)
+        if dev.cuda_available():
+            import torch
+            cl = torch.zeros((E, 4 * n1), dtype=torch.float64, device="cuda")
+            for idx, load in self._element_loads_device(spec):
+                cl.index_add_(0, idx, self._condense_loads_device(idx, load))
+            rhs = dev.empty(self.ndof)
+            check(lib.hdg_sum_owners(self.mesh.n_x, self.mesh.n_y, self.p, cl.data_ptr(), rhs.data_ptr(), dev.stream()))
+            return rhs.cpu().numpy()
         cl = np.zeros((E, 4 * n1))
         for idx, load in self._element_loads(spec):
             cl[idx] += self._condense_loads(idx, load)
@@ -508,39 +568,41 @@ class TraceSystem:
             raise ValueError(f"expected {self.ndof} trace values, got {lam_d.numel()}")
         lam_e = self._gather_device(lam_d)
         load = torch.zeros((E, 3 * nb), dtype=torch.float64, device="cuda")
-        for idx, ld in self._element_loads(self.spec):
-            load[torch.as_tensor(idx, device="cuda")] += torch.as_tensor(ld, device="cuda")
+        for idx, ld in self._element_loads_device(self.spec):
+            load.index_add_(0, idx, ld)
         if self.piecewise is not None:
             q, u = self.piecewise.reconstruct(self.class_K, load, lam_e)
             return dev.back(q, was_np), dev.back(u, was_np)
         if self.classes is None:
             raise NotImplementedError("reconstruction needs the element classes (from_blocks system)")
-        Linv = torch.as_tensor(np.linalg.inv(self.classes.L), device="cuda")
-        T = torch.as_tensor(self.classes.T, device="cuda")
+        from .discretization import gemm_nt
+        # sol = L^-1 (load - T lam_e): Z1 = L^-1 T applied to lam_e and L^-1 to the load
+        Linv = np.linalg.inv(self.classes.L)
         if self.classes.n == 1:
-            sol = (load - lam_e @ T[0].T) @ Linv[0].T
+            LinvT = torch.as_tensor(np.ascontiguousarray(Linv[0] @ self.classes.T[0]), device="cuda")
+            sol = gemm_nt(load, torch.as_tensor(np.ascontiguousarray(Linv[0]), device="cuda"))
+            gemm_nt(lam_e, LinvT, out=sol, alpha=-1.0, beta=1.0)
         else:
-            cls = torch.as_tensor(self.elem_class, device="cuda")
+            cls = torch.as_tensor(self.elem_class, dtype=torch.int64, device="cuda").contiguous()
+            Ld = torch.as_tensor(np.ascontiguousarray(Linv), device="cuda")
+            Td = torch.as_tensor(np.ascontiguousarray(self.classes.T), device="cuda")
+            rhs = load.clone()
+            st = dev.stream()
+            check(lib.hdg_class_gemv(E, 3 * nb, 4 * n1, cls.data_ptr(), Td.data_ptr(), lam_e.data_ptr(), 4 * n1,
+                                     rhs.data_ptr(), 3 * nb, -1.0, 1.0, st))
             sol = torch.empty_like(load)
-            for s0 in range(0, E, 1 << 16):
-                c = cls[s0:s0 + (1 << 16)]
-                rhs = load[s0:s0 + (1 << 16)] - torch.einsum("eij,ej->ei", T[c], lam_e[s0:s0 + (1 << 16)])
-                sol[s0:s0 + (1 << 16)] = torch.einsum("eij,ej->ei", Linv[c], rhs)
+            check(lib.hdg_class_gemv(E, 3 * nb, 3 * nb, cls.data_ptr(), Ld.data_ptr(), rhs.data_ptr(), 3 * nb,
+                                     sol.data_ptr(), 3 * nb, 1.0, 0.0, st))
         return dev.back(sol[:, :2 * nb].contiguous(), was_np), dev.back(sol[:, 2 * nb:].contiguous(), was_np)
 
     def _gather_device(self, lam_d):
-        """(E, 4n1) element trace values, 0 on Dirichlet sides (trace.py:81-85), on the device:
-        the TraceLayout.gather arithmetic on torch views."""
+        """(E, 4n1) element trace values, 0 on Dirichlet sides (trace.py:81-85), on the device
+        (hdgb200.h: hdg_gather_elements)."""
         import torch
         lay = self.layout
-        n1, nx, ny = lay.n1, lay.nx, lay.ny
-        H = torch.zeros((ny + 1, nx, n1), dtype=torch.float64, device="cuda")
-        V = torch.zeros((nx + 1, ny, n1), dtype=torch.float64, device="cuda")
-        if self.ndof:
-            H[1:ny] = lam_d[:lay.nh * n1].reshape(ny - 1, nx, n1)
-            V[1:nx] = lam_d[lay.nh * n1:].reshape(nx - 1, ny, n1)
-        return torch.stack([H[:-1], V[1:].transpose(0, 1), H[1:], V[:-1].transpose(0, 1)],
-                           dim=2).reshape(nx * ny, 4 * n1)
+        out = torch.empty((lay.nx * lay.ny, 4 * lay.n1), dtype=torch.float64, device="cuda")
+        check(lib.hdg_gather_elements(lay.nx, lay.ny, self.p, dev.ptr(lam_d), out.data_ptr(), dev.stream()))
+        return out
 
     def postprocess_all(self, q, u, chunk=1 << 16):
         """trace.py:180-185 / local.py:282-299: superconvergent order-(p+1) potential per element,
@@ -555,10 +617,14 @@ class TraceSystem:
         nb = self.ops.nb
         E = m.n_x * m.n_y
         qd, ud = qd.reshape(E, 2 * nb), ud.reshape(E, nb)
-        T = {k: torch.as_tensor(getattr(pops, k), device="cuda")
-             for k in ("interp_from_p", "w2", "dxi2", "deta2")}
-        lu, piv = torch.linalg.lu_factor(torch.as_tensor(pops.kkt, device="cuda"))
-        out = torch.empty((E, pops.nb), dtype=torch.float64, device="cuda")
+        from .discretization import gemm_nt
+        cu = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device="cuda")   # noqa: E731
+        interp, w2 = cu(pops.interp_from_p), cu(pops.w2)
+        dxi2T, deta2T = cu(pops.dxi2.T), cu(pops.deta2.T)
+        n = pops.nb
+        kinv = cu(np.linalg.inv(pops.kkt)[:n])                          # the potential rows of the KKT inverse
+        mean_w = cu((pops.jac * (pops.w2 @ pops.interp_from_p))[None, :])   # mean_u = jac w2 . (interp u)
+        out = torch.empty((E, n), dtype=torch.float64, device="cuda")
         ref = pops.ref
         for e0 in range(0, E, chunk):
             e1 = min(E, e0 + chunk)
@@ -567,15 +633,15 @@ class TraceSystem:
             kq = self.spec.coefficient(qx, qy)
             aniso = isinstance(kq, tuple)
             kx_h, ky_h = kq if aniso else (kq, kq)
-            kx = torch.as_tensor(np.asarray(kx_h, float).reshape(qx.shape), device="cuda")
-            ky = torch.as_tensor(np.asarray(ky_h, float).reshape(qx.shape), device="cuda") if aniso else kx
-            qh_x = qd[e0:e1, :nb] @ T["interp_from_p"].T
-            qh_y = qd[e0:e1, nb:] @ T["interp_from_p"].T
-            rhs = (-0.5 * m.dy) * ((T["w2"] * qh_x / kx) @ T["dxi2"]) \
-                + (-0.5 * m.dx) * ((T["w2"] * qh_y / ky) @ T["deta2"])
-            mean_u = pops.jac * ((ud[e0:e1] @ T["interp_from_p"].T) @ T["w2"])
-            B = torch.cat([rhs, mean_u[:, None]], dim=1).T.contiguous()
-            out[e0:e1] = torch.linalg.lu_solve(lu, piv, B).T[:, :-1]
+            kx = cu(np.asarray(kx_h, float).reshape(qx.shape))
+            ky = cu(np.asarray(ky_h, float).reshape(qx.shape)) if aniso else kx
+            qh_x = gemm_nt(qd[e0:e1, :nb], interp)                       # order-raising interpolation
+            qh_y = gemm_nt(qd[e0:e1, nb:], interp)
+            B = torch.empty((e1 - e0, n + 1), dtype=torch.float64, device="cuda")
+            gemm_nt(qh_x, dxi2T, out=B[:, :n], colscale=w2, adiv=kx, alpha=-0.5 * m.dy)
+            gemm_nt(qh_y, deta2T, out=B[:, :n], colscale=w2, adiv=ky, alpha=-0.5 * m.dx, beta=1.0)
+            gemm_nt(ud[e0:e1], mean_w, out=B[:, n:])
+            gemm_nt(B, kinv, out=out[e0:e1])                             # KKT solve, all elements at once
         return dev.back(out, was_np)
 
     # -- reference attributes -----------------------------------------------------------------
