@@ -68,6 +68,24 @@ namespace cg = cooperative_groups;
 #define HDG_SYMSTORE 1     // stored mode: each facet-pair coupling block stored once (4 of 7 blocks per facet)
 #endif
 #ifndef HDG_SYMSTORE_EF_MIN_N1
+#ifndef HDG_PAIR_PREFETCH
+#define HDG_PAIR_PREFETCH 0     // L2 prefetch of the next block of the merged stored pass (measured slower: 0.61 -> 0.58 at p = 8)
+#endif
+#ifndef HDG_PAIR_RING
+#define HDG_PAIR_RING 1         // merged stored pass streams its blocks through a per-warp TMA ring
+#endif
+#ifndef HDG_PAIR_RING_MAX_N1
+#define HDG_PAIR_RING_MAX_N1 10
+#endif
+#ifndef HDG_PAIR_AHEAD_MAX_N1
+#define HDG_PAIR_AHEAD_MAX_N1 7
+#endif
+#ifndef HDG_PAIR_STAGES
+#define HDG_PAIR_STAGES 4       // ring stages per warp of the merged stored pass (3 block rows in flight)
+#endif
+#ifndef HDG_PAIR_MIN_N1
+#define HDG_PAIR_MIN_N1 6      // merged h/v pass over the half-stored stream from this n1 (hdg_kernels.cuh: apply_stored_pair)
+#endif
 #define HDG_SYMSTORE_EF_MIN_N1 7   // half-stored stream: evict-first hint on the owner's read from this n1
 #endif                             // (measured: p=8 192 vs 207 us, p=4 118 vs 105 us, p=1 69 vs 62 us)
 #ifndef HDG_SHARED_SYM
@@ -138,8 +156,20 @@ template <int N1, bool ST = false> struct Cfg {
     return EPI != 0 && (base_doubles(ST) + NBUF * BSZ) * 8 <= 113 * 1024;
   }
   template <int EPI> __host__ __device__ static constexpr int bufs() { return BUF + (stage_b<EPI>() ? BSZ : 0); }   // stage stride
-  template <int EPI> __host__ __device__ static constexpr int smem_doubles_epi() {
+  // merged h/v pass over the half-stored stream (apply_stored_pair): every warp streams its block
+  // rows (n1 entries x 32 lanes = n1 * 256 contiguous bytes each) through a private TMA ring
+  static constexpr bool PAIR = ST && HDG_SYMSTORE && F == 1 && N1 >= HDG_PAIR_MIN_N1;
+  static constexpr int RSTAGES = HDG_PAIR_STAGES;
+  static constexpr int RROW = N1 * 32;                                    // doubles per ring stage
+  // the ring version's fully unrolled block rows outgrow the instruction cache above n1 = 10
+  // (p = 12: 0.43 of HBM with the ring, 0.65 with per-thread loads)
+  static constexpr bool PRING = PAIR && HDG_PAIR_RING && N1 <= HDG_PAIR_RING_MAX_N1;
+  static constexpr int RING = PRING ? NW * RSTAGES * RROW : 0;
+  template <int EPI> __host__ __device__ static constexpr int tile_doubles_epi() {
     return NBUF * bufs<EPI>() + (ST ? 0 : (NW + 1) * WSCR);
+  }
+  template <int EPI> __host__ __device__ static constexpr int smem_doubles_epi() {
+    return ((tile_doubles_epi<EPI>() + 3) & ~3) + RING;
   }
   static constexpr int smem_doubles(bool stored) { return base_doubles(stored); }
 };
@@ -692,6 +722,294 @@ __device__ __forceinline__ void apply_stored_half(const double* const (&nb)[7], 
   }
 }
 
+// A horizontal facet h(i,j) and the vertical facet v(i,j) of the same thread in one pass over the
+// half-stored stream, ordered so that both reads of every coupling block are close in time:
+//   * h.q5 = v.q5^T is loaded once and feeds both accumulators;
+//   * h.q6 / v.q2 are read again, transposed, by lane i+1 in the same loop iteration (one 8-byte
+//     shift inside the same 256-byte line: an L1 hit, no second L2 / DRAM read);
+//   * the three blocks owned by row j-1 (h.q2, v.q6, v.q4 of the row below) are read right after
+//     this thread's own copies of the same three, so the warp of row j-1 and this warp touch them
+//     one block apart (at p = 8 the separate h / v passes put ~100 MB of other traffic between
+//     the two reads GPU-wide and the second read missed the L2: 1.55x DRAM bytes).
+// Blocks nobody reads again (diagonals, q5, and the lane-shifted ones) carry the evict-first hint.
+template <int N1>
+__device__ __forceinline__ void apply_stored_pair(const double* const (&nh)[7], const double* const (&nv)[7],
+                                                  const double* hown, const double* vown, const double* hd,
+                                                  const double* vd, const double* vd1, const double* hw,
+                                                  const double* vw, double (&ah)[N1], double (&av)[N1]) {
+  const uint64_t pol = evict_first_policy();
+  constexpr int B = N1 * N1 * 32;
+#pragma unroll
+  for (int k = 0; k < N1; ++k) ah[k] = av[k] = 0.0;
+  // the warp's copy of one block is N1^2 * 256 contiguous bytes: pull the next step's own block into
+  // L2 while this step computes (the loads then cost an L2 hit instead of a DRAM round trip)
+  auto prefetch_block = [&](const double* W) {
+#if HDG_PAIR_PREFETCH
+    const char* base = reinterpret_cast<const char*>(W - (threadIdx.x & 31));
+    constexpr int LINES = (N1 * N1 * 256 + 127) / 128;
+#pragma unroll
+    for (int l = 0; l < LINES; l += 32)
+      if (l + (int)(threadIdx.x & 31) < LINES)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)(l + (threadIdx.x & 31)) * 128));
+#endif
+  };
+  // own block W (acc += W x) followed by a transposed partner block P (acc2 += P^T x2)
+  auto own_then_partner = [&](const double* W, const double* xo, double (&ao)[N1], const double* Pp, const double* xp,
+                              double (&ap)[N1]) {
+    double xa[N1], xb[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) { xa[m] = xo[m]; xb[m] = xp[m]; }
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+#pragma unroll
+      for (int m = 0; m < N1; ++m) ao[k] = fma(__ldg(W + (k * N1 + m) * 32), xa[m], ao[k]);
+#pragma unroll
+    for (int mm = 0; mm < N1; ++mm)
+#pragma unroll
+      for (int k = 0; k < N1; ++k) ap[k] = fma(__ldg(Pp + (mm * N1 + k) * 32), xb[mm], ap[k]);
+  };
+  // own block and the neighbouring lane's copy of the same entries in one loop (L1 hit)
+  auto own_and_shifted = [&](const double* W, const double* xo, double (&ao)[N1], const double* Ws, const double* xs,
+                             double (&as)[N1]) {
+    double xa[N1], xb[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) { xa[m] = xo[m]; xb[m] = xs[m]; }
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        const double w = __ldg(W + (k * N1 + m) * 32);
+        const double ws = __ldg(Ws + (k * N1 + m) * 32);
+        ao[k] = fma(w, xa[m], ao[k]);
+        as[m] = fma(ws, xb[k], as[m]);
+      }
+  };
+  prefetch_block(vown + 3 * B);
+  own_then_partner(hown + 1 * B, nh[2], ah, hd + 1 * B, nh[0], ah);      // h.q2 ; h.q0 <- h(i,j-1).q2
+  prefetch_block(vown + 2 * B);
+  own_then_partner(vown + 3 * B, nv[6], av, vd + 3 * B, nh[3], ah);      // v.q6 ; h.q3 <- v(i,j-1).q6
+  prefetch_block(hown + 2 * B);
+  own_then_partner(vown + 2 * B, nv[4], av, vd1 + 2 * B, nh[4], ah);     // v.q4 ; h.q4 <- v(i+1,j-1).q4
+  prefetch_block(hown + 3 * B);
+  {                                                                      // h.q5 = v.q5^T: one load, two uses
+    double xa[N1], xb[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) { xa[m] = nh[5][m]; xb[m] = nv[5][m]; }
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        const double w = ld_stream(hown + 2 * B + (k * N1 + m) * 32, pol);
+        ah[k] = fma(w, xa[m], ah[k]);
+        av[m] = fma(w, xb[k], av[m]);
+      }
+  }
+  prefetch_block(vown + 1 * B);
+  own_and_shifted(hown + 3 * B, nh[6], ah, hw + 3 * B, nv[3], av);       // h.q6 ; v.q3 <- h(i-1,j).q6
+  prefetch_block(hown);
+  prefetch_block(vown);
+  own_and_shifted(vown + 1 * B, nv[2], av, vw + 1 * B, nv[0], av);       // v.q2 ; v.q0 <- v(i-1,j).q2
+  {                                                                      // diagonal blocks
+    double xa[N1], xb[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) { xa[m] = nh[1][m]; xb[m] = nv[1][m]; }
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        ah[k] = fma(ld_stream(hown + (k * N1 + m) * 32, pol), xa[m], ah[k]);
+        av[k] = fma(ld_stream(vown + (k * N1 + m) * 32, pol), xb[m], av[k]);
+      }
+  }
+}
+
+// Per-warp ring of the merged stored pass.  `count` (chunks issued / consumed so far by this warp)
+// runs on across the tiles of the persistent CTA and gives every chunk its stage and mbarrier parity.
+struct PairRing {
+  double* ring;
+  uint64_t* bars;
+  unsigned count;
+};
+
+// apply_stored_pair with the block rows streamed through the warp's TMA ring instead of per-thread
+// register loads: the bytes in flight no longer depend on the registers left over by the two
+// accumulators (the register version ran at 12 warps/SM with too few loads in flight: 59% of DRAM
+// throughput although its traffic was down to 1.06x the stream).  Chunk sequence (block, row):
+// the 11 blocks in the order of apply_stored_pair, N1 rows each; lane 0 issues chunk c + STAGES - 1
+// when the warp has finished chunk c - 1.  Lane-shifted partner values come from the same staged
+// row at lane - 1 / lane + 1; the one lane whose neighbour sits in the next slot group reads global
+// memory directly.
+template <int N1, int STAGES>
+__device__ __forceinline__ void apply_stored_pair_ring(PairRing& pr, const double* const (&nh)[7],
+                                                       const double* const (&nv)[7], const double* hown,
+                                                       const double* vown, const double* hd, const double* vd,
+                                                       const double* vd1, const double* hw, const double* vw,
+                                                       double (&ah)[N1], double (&av)[N1]) {
+  constexpr int B = N1 * N1 * 32, ROW = N1 * 32, NBLK = 11, NCH = NBLK * N1;
+  // edge-lane values one row ahead, loaded by that lane only (n1 <= 7: p = 5 0.80 -> 0.85 of HBM), or
+  // loaded in place by every lane (n1 >= 8, where the extra registers cost more: p = 8 0.76 vs 0.55)
+  constexpr bool AHEAD = N1 <= HDG_PAIR_AHEAD_MAX_N1;
+  const int lane = threadIdx.x & 31;
+  // warp-uniform block bases (lane 0's slot of the group), in processing order
+  const double* const blk[NBLK] = {hown - lane + 1 * B, hd - lane + 1 * B, vown - lane + 3 * B, vd - lane + 3 * B,
+                                   vown - lane + 2 * B, vd - lane + 2 * B, hown - lane + 2 * B, hown - lane + 3 * B,
+                                   vown - lane + 1 * B, hown - lane, vown - lane};
+  const unsigned c0 = pr.count;
+  auto issue = [&](int c) {
+    if (c >= NCH || lane != 0) return;
+    const unsigned g = c0 + c;
+    uint64_t* bar = pr.bars + g % STAGES;
+    mbar_arrive_expect_tx(bar, ROW * 8u);
+    tma_load_1d(pr.ring + (g % STAGES) * ROW, blk[c / N1] + (c % N1) * ROW, ROW * 8u, bar);
+  };
+  auto wait = [&](int c) -> const double* {
+    __syncwarp();                       // every lane has finished the stage that is refilled now
+    fence_proxy_async();
+    issue(c + STAGES - 1);
+    const unsigned g = c0 + c;
+    mbar_wait(pr.bars + g % STAGES, (g / STAGES) & 1u);
+    return pr.ring + (g % STAGES) * ROW + lane;
+  };
+  __syncwarp();
+  fence_proxy_async();
+#pragma unroll
+  for (int c = 0; c < STAGES - 1; ++c) issue(c);
+#pragma unroll
+  for (int k = 0; k < N1; ++k) ah[k] = av[k] = 0.0;
+  int c = 0;
+  // own block: acc[r] += row_r . x
+  auto own = [&](const double* xo, double (&ao)[N1]) {
+    double xa[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) xa[m] = xo[m];
+#pragma unroll
+    for (int r = 0; r < N1; ++r) {
+      const double* q = wait(c++);
+      double sacc = ao[r];
+#pragma unroll
+      for (int m = 0; m < N1; ++m) sacc = fma(q[m * 32], xa[m], sacc);
+      ao[r] = sacc;
+    }
+  };
+  // partner block (transposed): acc[k] += P[r][k] x[r]; shift = lane offset of the owner's slot.
+  // The one lane whose owner sits in the next slot group loads its row from global memory, one row
+  // ahead of its use (only that lane executes the loads).
+  auto partner = [&](const double* xp, double (&ap)[N1], int shift, const double* edge) {
+    double xb[N1], ev[AHEAD ? N1 : 1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) xb[m] = xp[m];
+    const bool direct = (shift > 0 && lane == 31);
+    if constexpr (!AHEAD) {
+#pragma unroll
+      for (int r = 0; r < N1; ++r) {
+        const double* q = wait(c++);
+#pragma unroll
+        for (int k = 0; k < N1; ++k) {
+          const double v = direct ? __ldg(edge + (r * N1 + k) * 32) : q[k * 32 + shift];
+          ap[k] = fma(v, xb[r], ap[k]);
+        }
+      }
+      return;
+    }
+#pragma unroll
+    for (int m = 0; m < (AHEAD ? N1 : 1); ++m) ev[m] = 0.0;
+    if (direct) {
+#pragma unroll
+      for (int k = 0; k < (AHEAD ? N1 : 1); ++k) ev[k] = __ldg(edge + k * 32);
+    }
+#pragma unroll
+    for (int r = 0; r < N1; ++r) {
+      const double* q = wait(c++);
+      double cur[N1];
+#pragma unroll
+      for (int k = 0; k < N1; ++k) cur[k] = ev[AHEAD ? k : 0];
+      if (direct && r + 1 < N1) {
+#pragma unroll
+        for (int k = 0; k < (AHEAD ? N1 : 1); ++k) ev[k] = __ldg(edge + ((r + 1) * N1 + k) * 32);
+      }
+#pragma unroll
+      for (int k = 0; k < N1; ++k) {
+        const double v = direct ? cur[k] : q[k * 32 + shift];
+        ap[k] = fma(v, xb[r], ap[k]);
+      }
+    }
+  };
+  // own block whose rows the neighbouring lane also needs transposed: ao[r] += row_r . xo and
+  // as[m] += W(lane - 1)[r][m] xs[r]; lane 0's neighbour is in the previous slot group (global loads,
+  // one row ahead)
+  auto own_and_shifted = [&](const double* xo, double (&ao)[N1], const double* xs, double (&as)[N1],
+                             const double* edge) {
+    double xa[N1], xb[N1], ev[AHEAD ? N1 : 1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) { xa[m] = xo[m]; xb[m] = xs[m]; }
+    const bool direct = lane == 0;
+    if constexpr (!AHEAD) {
+#pragma unroll
+      for (int r = 0; r < N1; ++r) {
+        const double* q = wait(c++);
+#pragma unroll
+        for (int m = 0; m < N1; ++m) {
+          ao[r] = fma(q[m * 32], xa[m], ao[r]);
+          const double ws = direct ? __ldg(edge + (r * N1 + m) * 32) : q[m * 32 - 1];
+          as[m] = fma(ws, xb[r], as[m]);
+        }
+      }
+      return;
+    }
+#pragma unroll
+    for (int m = 0; m < (AHEAD ? N1 : 1); ++m) ev[m] = 0.0;
+    if (direct) {
+#pragma unroll
+      for (int m = 0; m < (AHEAD ? N1 : 1); ++m) ev[m] = __ldg(edge + m * 32);
+    }
+#pragma unroll
+    for (int r = 0; r < N1; ++r) {
+      const double* q = wait(c++);
+      double cur[N1];
+#pragma unroll
+      for (int m = 0; m < N1; ++m) cur[m] = ev[AHEAD ? m : 0];
+      if (direct && r + 1 < N1) {
+#pragma unroll
+        for (int m = 0; m < (AHEAD ? N1 : 1); ++m) ev[m] = __ldg(edge + ((r + 1) * N1 + m) * 32);
+      }
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {      // ao and as may be the same accumulator (v.q2 / v.q0): no cached partial sums
+        ao[r] = fma(q[m * 32], xa[m], ao[r]);
+        const double ws = direct ? cur[m] : q[m * 32 - (direct ? 0 : 1)];
+        as[m] = fma(ws, xb[r], as[m]);
+      }
+    }
+  };
+  own(nh[2], ah);                               // h.q2
+  partner(nh[0], ah, 0, nullptr);               // h.q0 <- h(i,j-1).q2
+  own(nv[6], av);                               // v.q6
+  partner(nh[3], ah, 0, nullptr);               // h.q3 <- v(i,j-1).q6
+  own(nv[4], av);                               // v.q4
+  partner(nh[4], ah, 1, vd1 + 2 * B);           // h.q4 <- v(i+1,j-1).q4 (owner = lane + 1)
+  {                                             // h.q5 = v.q5^T: one staged row, two uses
+    double xa[N1], xb[N1];
+#pragma unroll
+    for (int m = 0; m < N1; ++m) { xa[m] = nh[5][m]; xb[m] = nv[5][m]; }
+#pragma unroll
+    for (int r = 0; r < N1; ++r) {
+      const double* q = wait(c++);
+      double sacc = ah[r];
+#pragma unroll
+      for (int m = 0; m < N1; ++m) {
+        const double w = q[m * 32];
+        sacc = fma(w, xa[m], sacc);
+        av[m] = fma(w, xb[r], av[m]);
+      }
+      ah[r] = sacc;
+    }
+  }
+  own_and_shifted(nh[6], ah, nv[3], av, hw + 3 * B);   // h.q6 ; v.q3 <- h(i-1,j).q6
+  own_and_shifted(nv[2], av, nv[0], av, vw + 1 * B);   // v.q2 ; v.q0 <- v(i-1,j).q2
+  own(nh[1], ah);                               // diagonal blocks
+  own(nv[1], av);
+  pr.count = c0 + NCH;
+}
+
 template <int EPI, int N1> struct NOutOf { static constexpr int v = (EPI == EPI_RESPR) ? N1 - 1 : N1; };
 
 // Per-facet epilogue: the facet's output values (y | r | x_out | r_coarse) into `o`.
@@ -768,7 +1086,7 @@ __device__ __forceinline__ void store_h_row(const MvArgs& a, double* scr, int i0
 }
 
 template <int N1, bool STORED, int EPI>
-__device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(STORED ? 1 : N1)>& op,
+__device__ __forceinline__ void compute_tile(PairRing& pring, const MvArgs& a, const SharedOp<(STORED ? 1 : N1)>& op,
                                              double* buf, double* scr, int i0, int j0, double& nrm) {
   using C = Cfg<N1, STORED>;
   constexpr int F = C::F;
@@ -842,6 +1160,9 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
   }
   double ov[F][N1];
   double ohs[STORED ? F : 1][N1];   // stored mode: h outputs wait for the CTA-staged write
+  constexpr bool PAIR = STORED && HDG_SYMSTORE && F == 1 && N1 >= HDG_PAIR_MIN_N1;
+  double accv_pair[PAIR ? N1 : 1];  // vertical facet's operator value from the merged h/v pass
+  bool pair_done = false;
   {
   // ---- horizontal facets: owners (i, j-1) [TOP rows] and (i, j) [BOTTOM rows]
   {
@@ -894,7 +1215,22 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
         if (j >= 1 && j <= a.ny - 1) {  // warp-uniform; lanes i >= nx read zero padding slots
           const long long grp = ((long long)j * a.nxp + i0) >> 5;
           double acc[N1];
-          if constexpr (HDG_SYMSTORE) {
+          if constexpr (PAIR) {
+            // rows 1 .. ny-1 hold both an h and a v facet per slot: one merged pass
+            const int jj = F * w + f + 1;
+            const double* nv[7] = {V(ii - 1, jj), V(ii, jj), V(ii + 1, jj), H(jj, ii - 1), H(jj + 1, ii - 1),
+                                   H(jj, ii), H(jj + 1, ii)};
+            const long long sl = (long long)j * a.nxp + i, sd = sl - a.nxp, sw = sl - 1;
+            if constexpr (C::PRING)
+              apply_stored_pair_ring<N1, C::RSTAGES>(pring, nb[f], nv, wslot<N1>(a.Wh, sl), wslot<N1>(a.Wv, sl),
+                                                     wslot<N1>(a.Wh, sd), wslot<N1>(a.Wv, sd), wslot<N1>(a.Wv, sd + 1),
+                                                     wslot<N1>(a.Wh, sw), wslot<N1>(a.Wv, sw), acc, accv_pair);
+            else
+              apply_stored_pair<N1>(nb[f], nv, wslot<N1>(a.Wh, sl), wslot<N1>(a.Wv, sl), wslot<N1>(a.Wh, sd),
+                                    wslot<N1>(a.Wv, sd), wslot<N1>(a.Wv, sd + 1), wslot<N1>(a.Wh, sw),
+                                    wslot<N1>(a.Wv, sw), acc, accv_pair);
+            pair_done = true;
+          } else if constexpr (HDG_SYMSTORE) {
             constexpr int B = N1 * N1 * 32;
             const long long sl = (long long)j * a.nxp + i, sd = sl - a.nxp;   // row j-1
             apply_stored_half<N1, false>(nb[f], wslot<N1>(a.Wh, sl), wslot<N1>(a.Wh, sd) + 1 * B,
@@ -944,7 +1280,10 @@ __device__ __forceinline__ void compute_tile(const MvArgs& a, const SharedOp<(ST
         if (j < a.ny) {
           const long long grp = ((long long)j * a.nxp + i0) >> 5;
           double acc[N1];
-          if constexpr (HDG_SYMSTORE) {
+          if (PAIR && pair_done) {
+#pragma unroll
+            for (int k = 0; k < N1; ++k) acc[k] = accv_pair[PAIR ? k : 0];
+          } else if constexpr (HDG_SYMSTORE) {
             constexpr int B = N1 * N1 * 32;
             const long long sl = (long long)j * a.nxp + i, sw = sl > 0 ? sl - 1 : 0;   // column i-1
             apply_stored_half<N1, true>(nb[f], wslot<N1>(a.Wv, sl), wslot<N1>(a.Wv, sw) + 1 * B,
@@ -1026,13 +1365,19 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
   constexpr bool SBV = C::template stage_b<EPI>();
   constexpr int BS = C::template bufs<EPI>();
   __shared__ __align__(8) uint64_t bars[NB];
+  __shared__ __align__(8) uint64_t rbars[C::PRING ? C::NW * C::RSTAGES : 1];
   double nrm = 0.0;
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int q = 0; q < NB; ++q) mbar_init(&bars[q], C::NW + C::NTH);  // lane-0 expect_tx + per-thread LDGSTS arrivals
+    if constexpr (C::PRING) {
+      for (int q = 0; q < C::NW * C::RSTAGES; ++q) mbar_init(&rbars[q], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  PairRing pring{smem + ((C::template tile_doubles_epi<EPI>() + 3) & ~3) + (threadIdx.x >> 5) * (C::RSTAGES * C::RROW),
+                 rbars + (C::PRING ? (threadIdx.x >> 5) * C::RSTAGES : 0), 0u};
   // ring of NB stage buffers: tiles blockIdx.x + it*grid; prefetch distance NB-1
 #pragma unroll
   for (int q = 0; q < NB - 1; ++q) {
@@ -1050,7 +1395,7 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
     }
     mbar_wait(&bars[slot], phase);
     __syncthreads();
-    compute_tile<N1, STORED, EPI>(a, op, smem + slot * BS, smem + NB * BS + (threadIdx.x >> 5) * C::WSCR,
+    compute_tile<N1, STORED, EPI>(pring, a, op, smem + slot * BS, smem + NB * BS + (threadIdx.x >> 5) * C::WSCR,
                                   (tile % tiles_x) * TX, (tile / tiles_x) * C::TY, nrm);
     __syncthreads();
     if (++slot == NB) { slot = 0; phase ^= 1u; }
