@@ -632,12 +632,13 @@ def run_config5(args, rank, ws):
 
 # ------------------------------------------------------------------------ configs[3] runner
 
+FP64_PEAK_TFLOPS = 34.2   # measured DFMA peak on this pool's B200 (profiles/fp64_peak_r01.json)
 C4_MESH = {1: 4096, 2: 3328, 4: 2560, 8: 1920, 12: 1536}   # ~64M trace DOFs each
 
 
 def run_config4(args, rank, ws):
     """configs[3]: order sweep at ~64M trace DOFs, K = I, fp64: trace matvec throughput (the
-    facet-record kernel for p <= 8, the reference-layout kernel above) and the V(2,2)
+    facet-record kernel at every order) and the V(2,2)
     block-Jacobi cycle per order.  value = all orders' DOF applies / their total time; per-order
     numbers (GDOF/s, fraction of HBM on 16 B/DOF, reference-formula FP64 rate, V-cycle ms) in
     "orders"."""
@@ -657,7 +658,7 @@ def run_config4(args, rank, ws):
         op = levels[0].block_op
         ndof = levels[0].ndof
         xr = [torch.rand(ndof, dtype=torch.float64, device="cuda") for _ in range(2)]
-        records = p <= 8
+        records = True   # the facet-record kernel covers every order (p <= 12)
         if records:
             xs = [op.to_planes(x) for x in xr]
             ys = [torch.empty_like(xs[0]) for _ in range(2)]
@@ -687,9 +688,14 @@ def run_config4(args, rank, ws):
         e1.record(st)
         torch.cuda.synchronize()
         nb = levels[0].system.n_blocks
+        # t_min = max(algorithmic bytes / HBM, reference-formula FLOPs / measured FP64 peak)
+        fl = nb * (16 * (p + 1) ** 2 - (p + 1))
+        t_hbm, t_fp = 16 * ndof / hbm / 1e3, fl / FP64_PEAK_TFLOPS / 1e6
         orders[str(p)] = {"mesh": n, "ndof": ndof, "kernel": kern, "matvec_us": round(us, 2),
                           "gdofs": round(ndof / us / 1e3, 1), "hbm_frac": round(16 * ndof / us / 1e3 / hbm, 3),
-                          "fp64_tflops_ref_formula": round(nb * (16 * (p + 1) ** 2 - (p + 1)) / us / 1e6, 2),
+                          "fp64_tflops_ref_formula": round(fl / us / 1e6, 2),
+                          "bound": "hbm" if t_hbm >= t_fp else "fp64",
+                          "roofline_frac": round(max(t_hbm, t_fp) / us, 3),
                           "vcycle_ms": round(e0.elapsed_time(e1) / 5, 3), "levels": len(levels)}
         tot_dof += ndof * args.steps
         tot_us += us * args.steps

@@ -1350,7 +1350,7 @@ static int rec_find(hdg_mg* mg) {
   int m = 0;
   for (int k = 0; k + 1 < mg->n; ++k) {
     hdg_level* L = mg->L[k];
-    if (L->stored || L->blk.empty() || L->n1 > SOA_MAXN1 || !L->has_bj || L->use_fsai || L->nx != L0->nx ||
+    if (L->stored || L->blk.empty() || L->n1 > SOA_CYCLE_MAXN1 || !L->has_bj || L->use_fsai || L->nx != L0->nx ||
         L->ny != L0->ny || L->ndof == 0)
       return 0;
     if (soa_prepare(L)) return 0;
@@ -1789,13 +1789,14 @@ int soa_prepare(hdg_level* L) {
   if (L->soa_state == 1) return 0;
   if (L->soa_state == -1 || L->stored || L->blk.empty() || L->n1 > SOA_MAXN1)
     return fail(HDG_EINVAL, "facet-plane layout needs a shared-block (constant coefficient, mirror-symmetric) "
-                            "level with p <= 8");
+                            "level with p <= 12");
   bool ok = false;
   int occ = 1;
 #define SOA_PREP(N) { ok = soa_reduce<N>(L->blk, L->soaM); occ = soa_occupancy<N>(); break; }
   switch (L->n1) {
     case 2: SOA_PREP(2) case 3: SOA_PREP(3) case 4: SOA_PREP(4) case 5: SOA_PREP(5)
     case 6: SOA_PREP(6) case 7: SOA_PREP(7) case 8: SOA_PREP(8) case 9: SOA_PREP(9)
+    case 10: SOA_PREP(10) case 11: SOA_PREP(11) case 12: SOA_PREP(12) case 13: SOA_PREP(13)
     default: break;
   }
 #undef SOA_PREP
@@ -1857,12 +1858,13 @@ int hdg_soa_pack(hdg_level* L, const double* x, double* xs, void* stream) {
   if (!L || (!x && L->ndof) || !xs) return fail(HDG_EINVAL, "null argument");
   int rc = soa_prepare(L);
   if (rc) return rc;
-  const unsigned grid = (unsigned)(L->soaW * ((L->ny + 1 + SOA_PB - 1) / SOA_PB));
+  const unsigned grid = (unsigned)(L->soaW * ((L->ny + 1 + soa_pb(L->n1) - 1) / soa_pb(L->n1)));
 #define SOA_PACK(N) { soa_pack_blocked_kernel<N><<<grid, 256, 0, S(stream)>>>(x, xs, L->nx, L->ny, L->soaW, L->nh); CKL(); return 0; }
   switch (L->n1) {
     case 2: SOA_PACK(2) case 3: SOA_PACK(3) case 4: SOA_PACK(4) case 5: SOA_PACK(5)
     case 6: SOA_PACK(6) case 7: SOA_PACK(7) case 8: SOA_PACK(8) case 9: SOA_PACK(9)
-    default: return fail(HDG_EINVAL, "facet-plane layout: p <= 8");
+    case 10: SOA_PACK(10) case 11: SOA_PACK(11) case 12: SOA_PACK(12) case 13: SOA_PACK(13)
+    default: return fail(HDG_EINVAL, "facet-plane layout: p <= 12");
   }
 #undef SOA_PACK
 }
@@ -1872,12 +1874,13 @@ int hdg_soa_unpack(hdg_level* L, const double* xs, double* x, void* stream) {
   int rc = soa_prepare(L);
   if (rc) return rc;
   if (L->ndof == 0) return 0;
-  const unsigned grid = (unsigned)(L->soaW * ((L->ny + 1 + SOA_PB - 1) / SOA_PB));
+  const unsigned grid = (unsigned)(L->soaW * ((L->ny + 1 + soa_pb(L->n1) - 1) / soa_pb(L->n1)));
 #define SOA_UNPACK(N) { soa_unpack_blocked_kernel<N><<<grid, 256, 0, S(stream)>>>(xs, x, L->nx, L->ny, L->soaW, L->nh); CKL(); return 0; }
   switch (L->n1) {
     case 2: SOA_UNPACK(2) case 3: SOA_UNPACK(3) case 4: SOA_UNPACK(4) case 5: SOA_UNPACK(5)
     case 6: SOA_UNPACK(6) case 7: SOA_UNPACK(7) case 8: SOA_UNPACK(8) case 9: SOA_UNPACK(9)
-    default: return fail(HDG_EINVAL, "facet-plane layout: p <= 8");
+    case 10: SOA_UNPACK(10) case 11: SOA_UNPACK(11) case 12: SOA_UNPACK(12) case 13: SOA_UNPACK(13)
+    default: return fail(HDG_EINVAL, "facet-plane layout: p <= 12");
   }
 #undef SOA_UNPACK
 }
@@ -1891,7 +1894,8 @@ int hdg_matvec_soa(hdg_level* L, const double* xs, double* ys, void* stream) {
   switch (L->n1) {
     case 2: SOA_APPLY(2) case 3: SOA_APPLY(3) case 4: SOA_APPLY(4) case 5: SOA_APPLY(5)
     case 6: SOA_APPLY(6) case 7: SOA_APPLY(7) case 8: SOA_APPLY(8) case 9: SOA_APPLY(9)
-    default: return fail(HDG_EINVAL, "facet-plane layout: p <= 8");
+    case 10: SOA_APPLY(10) case 11: SOA_APPLY(11) case 12: SOA_APPLY(12) case 13: SOA_APPLY(13)
+    default: return fail(HDG_EINVAL, "facet-plane layout: p <= 12");
   }
 #undef SOA_APPLY
 }

@@ -59,6 +59,9 @@
                                // (constant bank for p <= 4: 36.7 vs 37.3 us at 1024^2; at p = 8
                                // the 326 entries overflow the uniform registers: 264 vs 220 us)
 #endif
+#ifndef HDG_SOA_MINB3_MAXN1
+#define HDG_SOA_MINB3_MAXN1 7   // 3 CTAs/SM (168 registers) up to this n1; n1 = 8, 9 spill there
+#endif
 #ifndef HDG_SOA_MINB_HI
 #define HDG_SOA_MINB_HI 3      // CTAs per SM for p >= 3 (154 registers at p = 4 without a cap)
 #endif
@@ -75,7 +78,7 @@ struct SoaCfg {
   static constexpr int MSZ = A0 * A0 + A1 * A1 + A2 * A2 + A3 * A3;
   static constexpr int NTH = 128;
   static constexpr int WPB = NTH / 32;                   // warps (= stacked segments) per CTA
-  static constexpr int MINB = N1 <= 3 ? 4 : HDG_SOA_MINB_HI;
+  static constexpr int MINB = N1 <= 3 ? 4 : (N1 <= HDG_SOA_MINB3_MAXN1 ? HDG_SOA_MINB_HI : 2);   // high orders: 255 registers, 2 CTAs/SM (no spills)
   static constexpr int RING = HDG_SOA_RING;              // ring entries per warp (RING-1 rows in flight)
   static constexpr int VOFF = N1 * 32;                   // V rows, 31 slots each, packed
   static constexpr int VB = (N1 * 31 + 3) & ~3;          // doubles of the V block (whole sectors)
@@ -524,13 +527,14 @@ __global__ void soa_unpack_kernel(const double* __restrict__ xs, double* __restr
 // memory, so the reference-layout side is read / written as contiguous runs (a horizontal line
 // segment of 32 columns = 32 N1 doubles; SOA_PB rows of one vertical line = SOA_PB N1 doubles) and
 // the record side as whole records.
-constexpr int SOA_PB = 8;
+__host__ __device__ constexpr int soa_pb(int n1) { return n1 <= 9 ? 8 : 4; }   // records per CTA (48 KB of static shared memory)
 
 template <int N1>
 __global__ void __launch_bounds__(256) soa_pack_blocked_kernel(const double* __restrict__ x, double* __restrict__ xs,
                                                                int nx, int ny, int W, long long nh) {
   using C = SoaCfg<N1>;
   constexpr int ENT = C::ENT, VOFF = C::VOFF, EOFF = C::EOFF, EB = C::EB;
+  constexpr int SOA_PB = soa_pb(N1);
   __shared__ __align__(16) double S[SOA_PB * ENT];
   // row blocks fastest: CTAs running together read neighbouring pieces of the same vertical lines
   const int nrb = (ny + SOA_PB) / SOA_PB;
@@ -568,6 +572,7 @@ __global__ void __launch_bounds__(256) soa_unpack_blocked_kernel(const double* _
                                                                  int nx, int ny, int W, long long nh) {
   using C = SoaCfg<N1>;
   constexpr int ENT = C::ENT, VOFF = C::VOFF;
+  constexpr int SOA_PB = soa_pb(N1);
   __shared__ __align__(16) double S[SOA_PB * ENT];
   // row blocks fastest: CTAs running together read neighbouring pieces of the same vertical lines
   const int nrb = (ny + SOA_PB) / SOA_PB;

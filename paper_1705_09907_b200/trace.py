@@ -672,7 +672,7 @@ class TraceSystem:
     def facet_planes(self, x):
         """Keep a trace vector resident on the device in the facet-plane layout (node k of every
         facet line contiguous): repeated matvec_free calls on it stream coalesced rows.  Shared-block
-        (constant coefficient) systems with p <= 8; raises otherwise."""
+        (constant coefficient) systems; raises otherwise."""
         return FacetPlanes(self, self.operator.to_planes(x))
 
     def gather_element(self, x, e):

@@ -26,7 +26,7 @@ def oracle_for(s, nx, ny, p):
     return o
 
 
-@pytest.mark.parametrize("p", list(range(1, 9)))
+@pytest.mark.parametrize("p", list(range(1, 13)))
 @pytest.mark.parametrize("shape", [(37, 21), (64, 64), (31, 5), (32, 7), (62, 9), (63, 2), (2, 40), (93, 3)])
 def test_planes_matvec_vs_oracle(P, p, shape):
     """Every order the facet-plane kernel is built for; meshes around the 31-column warp
@@ -39,7 +39,7 @@ def test_planes_matvec_vs_oracle(P, p, shape):
     assert rel(y, oracle_for(s, nx, ny, p).matvec(x)) < TOL
 
 
-@pytest.mark.parametrize("p", [1, 4, 8])
+@pytest.mark.parametrize("p", [1, 4, 8, 12])
 def test_planes_roundtrip_and_every_slot_written(P, p):
     import torch
     s = P.tr.TraceSystem(P.mesh(70, 45), p, specs.constant(P.pb.ProblemSpec))
@@ -120,7 +120,3 @@ def test_planes_refuses_stored_levels(P):
         s.facet_planes(np.zeros(s.ndof))
 
 
-def test_planes_refuses_high_order(P):
-    s = P.tr.TraceSystem(P.mesh(8, 8), 9, specs.constant(P.pb.ProblemSpec))
-    with pytest.raises(HDGError):
-        s.facet_planes(np.zeros(s.ndof))
