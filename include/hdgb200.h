@@ -274,6 +274,25 @@ int hdg_galerkin_h(int64_t C, const double* S_children, const double* Q, int sha
 int hdg_gather_elements(int nx, int ny, int p, const double* lam, double* lam_e, void* stream);
 int hdg_sum_owners(int nx, int ny, int p, const double* cl, double* rhs, void* stream);
 
+/* ---------------------------------------------------------------- multi-GPU strips
+ * element-row strips, one process (or context) per GPU.  Each rank holds a
+ * WINDOW of the mesh (a level created on nx x nyl elements: its owned rows [r0, r1) of the global
+ * mesh plus ghost rows, window row 0 = global row lo) and applies the single-GPU kernels to it;
+ * hdg_dist_halo refreshes the ghost facet rows from the neighbouring ranks over the caller's NCCL
+ * communicator (nccl_comm is an ncclComm_t; NCCL is resolved at run time from the process'
+ * libnccl.so.2), packed / sent / received / unpacked on `stream` with no host wait:
+ *   kind 0 (before an operator apply, trace.py:87-94 on the window): down: send h(r0), receive
+ *          h(r0-1), v(r0-1); up: send h(r1-1), v(r1-1), receive h(r1);
+ *   kind 1 (before an h-restriction, multigrid.py:276-281): send up v(r1-2), v(r1-1), h(r1-1).
+ * (kind | 0x100: loopback self-test, the rank acts as its own lower and upper neighbour.)
+ * hdg_dist_allreduce_sum: the owned-dof dot products / norms (one ncclAllReduce, in place). */
+typedef struct hdg_dist hdg_dist;
+int hdg_dist_init(void* nccl_comm, int rank, int nranks, hdg_dist** out);
+int hdg_dist_destroy(hdg_dist* d);
+int hdg_dist_halo(hdg_dist* d, const hdg_level* window_level, int lo, int r0, int r1, int ny_global, int kind,
+                  double* x, void* stream);
+int hdg_dist_allreduce_sum(hdg_dist* d, double* v, int count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

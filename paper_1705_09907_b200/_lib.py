@@ -87,6 +87,10 @@ SIGNATURES = [
     ("hdg_galerkin_h", c_int, [c_int64, c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
     ("hdg_gather_elements", c_int, [c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     ("hdg_sum_owners", c_int, [c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    ("hdg_dist_init", c_int, [c_void_p, c_int, c_int, ctypes.POINTER(c_void_p)]),
+    ("hdg_dist_destroy", c_int, [c_void_p]),
+    ("hdg_dist_halo", c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
+    ("hdg_dist_allreduce_sum", c_int, [c_void_p, c_void_p, c_int, c_void_p]),
 ]
 
 
