@@ -250,7 +250,7 @@ def run_ours(args, rank, ws):
         xs = [op.to_planes(x) for x in xs]
         ys = [torch.empty_like(xs[0]) for _ in range(NB)]
         apply_fn, kname = lib.hdg_matvec_soa, "soa_apply_kernel<5> (facet records)"
-        ncu_keys = "ncu_soa_apply_p4_r02_key_metrics.txt"
+        ncu_keys = "ncu_soa_apply_p4_r02b_key_metrics.txt"
     else:
         apply_fn, kname = lib.hdg_matvec, "trace_apply_kernel<5,shared,EPI_Y>"
         ncu_keys = "ncu_trace_apply_p4_r01_key_metrics.txt"
