@@ -25,6 +25,15 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+bool hdg_pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("HDG_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // ------------------------------------------------------------------------------ helpers
 
 static void host_invert(std::vector<double>& a, int n) {  // SPD Gauss-Jordan, no pivoting
@@ -121,7 +130,7 @@ static int apply_t(const hdg_level* L, MvArgs& a, cudaStream_t s) {
   } else {
     std::memset(&op, 0, sizeof(op));
   }
-  kernel_ptr<N1, STORED, EPI>()<<<grid, C::NTH, smem, s>>>(a, op);
+  launch_pdl(kernel_ptr<N1, STORED, EPI>(), dim3(grid), dim3(C::NTH), smem, s, a, op);
   CKL();
   return 0;
 }
@@ -939,7 +948,7 @@ int hdg_prolong_add(const hdg_transfer* t, const double* ec, double* xf, void* s
   const int bs = 256;
   const unsigned grid = (unsigned)((nf + bs - 1) / bs);
   if (t->is_h) {
-    h_prolong_add_kernel<<<grid, bs, 0, S(stream)>>>(t->ha, ec, xf);
+    launch_pdl(h_prolong_add_kernel, dim3(grid), dim3(bs), 0, S(stream), t->ha, ec, xf);
     CKL();
     return 0;
   }
@@ -954,7 +963,7 @@ int hdg_restrict(const hdg_transfer* t, const double* rf, double* rc, void* stre
   if (t->is_h) {
     const long long nc = t->coarse->n_blocks;
     if (nc == 0) return 0;
-    h_restrict_kernel<<<(unsigned)((nc + bs - 1) / bs), bs, 0, S(stream)>>>(t->ha, rf, rc);
+    launch_pdl(h_restrict_kernel, dim3((unsigned)((nc + bs - 1) / bs)), dim3(bs), 0, S(stream), t->ha, rf, rc);
     CKL();
     return 0;
   }
@@ -1244,7 +1253,7 @@ static int tail_issue(hdg_mg* mg, const double* b, bool zero_init, int nu1, int 
   TailGen g{mg, A, k0, nu1, nu2, visits};
   g.gen(k0, zero_init);
   if (g.overflow) { delete A; return 0; }
-  tail_cycle_kernel<<<1, TAIL_THREADS, (size_t)(off + TAIL_ARGS_DOUBLES + 64 * TAIL_MAXL) * sizeof(double), s>>>(*A);
+  launch_pdl(tail_cycle_kernel, dim3(1), dim3(TAIL_THREADS), (size_t)(off + TAIL_ARGS_DOUBLES + 64 * TAIL_MAXL) * sizeof(double), s, *A);
   delete A;
   CKL();
   return 1;

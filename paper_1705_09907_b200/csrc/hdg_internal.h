@@ -8,6 +8,7 @@
 #include <map>
 #include <string>
 #include <tuple>
+#include <utility>
 #include <vector>
 
 using namespace hdg;
@@ -32,6 +33,27 @@ int fail(int code, const std::string& msg);   // sets hdg_last_error, returns co
   } while (0)
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Launch with programmatic stream serialization: the grid may be scheduled while the kernel before
+// it in the stream drains, and runs its prologue up to its `griddepcontrol.wait` (every kernel
+// launched this way executes one before its first global access).  The cycle's small levels are
+// chains of 5 us kernels, where the launch gap is a large part of the time.  HDG_PDL=0 turns it off.
+bool hdg_pdl_enabled();
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = hdg_pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 struct hdg_level {
   int nx = 0, ny = 0, p = 0, n1 = 0, nxp = 0;

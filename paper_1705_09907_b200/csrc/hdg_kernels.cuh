@@ -235,6 +235,10 @@ template <int N1> __device__ __forceinline__ int v_run_start(const MvArgs& a, in
   return (a.nh + (i0 - 2 + c) * a.ny + j0 - 1) * N1;
 }
 
+// programmatic dependent launch: wait for the kernel before this one in the stream (hdg_internal.h:
+// launch_pdl); a no-op for a normally launched grid
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------- mbarrier / TMA (bulk)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -1376,6 +1380,7 @@ trace_apply_kernel(const MvArgs a, const __grid_constant__ SharedOp<(STORED ? 1 
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  grid_dependency_wait();
   PairRing pring{smem + ((C::template tile_doubles_epi<EPI>() + 3) & ~3) + (threadIdx.x >> 5) * (C::RSTAGES * C::RROW),
                  rbars + (C::PRING ? (threadIdx.x >> 5) * C::RSTAGES : 0), 0u};
   // ring of NB stage buffers: tiles blockIdx.x + it*grid; prefetch distance NB-1
@@ -1694,6 +1699,7 @@ static __global__ void h_prolong_add_kernel(const __grid_constant__ HArgs h, con
                                      double* __restrict__ xf) {
   const long long nvf = (long long)(2 * h.nxc - 1) * h.nyf;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  grid_dependency_wait();
   if (t >= h.nhf + nvf) return;
   if (h.shared_cross) h_prolong_add_one<false, true>(h, ec, xf, t);
   else h_prolong_add_one<false, false>(h, ec, xf, t);
@@ -1773,6 +1779,7 @@ static __global__ void h_restrict_kernel(const __grid_constant__ HArgs h, const 
                                   double* __restrict__ rc) {
   const long long nvc = (long long)(h.nxc - 1) * h.nyc;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  grid_dependency_wait();
   if (t >= h.nhc + nvc) return;
   if (h.shared_cross) h_restrict_one<false, true>(h, rf, rc, t);
   else h_restrict_one<false, false>(h, rf, rc, t);
@@ -2079,6 +2086,7 @@ static __global__ void __launch_bounds__(TAIL_THREADS, 1) tail_cycle_kernel(cons
     uint4* dst = reinterpret_cast<uint4*>(tsm_raw);
     for (int t = tid; t < NW; t += TAIL_THREADS) dst[t] = src[t];
   }
+  grid_dependency_wait();   // the program copy above overlaps the previous kernel's tail
   __syncthreads();
   // shared-mode operators (64 doubles per level) next to the program; stored streams stay global
   double* opsm = tsm_raw + TAIL_ARGS_DOUBLES;

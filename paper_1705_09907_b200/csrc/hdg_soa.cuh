@@ -60,7 +60,10 @@
                                // the 326 entries overflow the uniform registers: 264 vs 220 us)
 #endif
 #ifndef HDG_SOA_MINB3_MAXN1
-#define HDG_SOA_MINB3_MAXN1 7   // 3 CTAs/SM (168 registers) up to this n1; n1 = 8, 9 spill there
+#define HDG_SOA_MINB3_MAXN1 9   // 3 CTAs/SM (168 registers) up to this n1
+#endif
+#ifndef HDG_SOA_HOLD_SMEM_MIN_N1
+#define HDG_SOA_HOLD_SMEM_MIN_N1 8
 #endif
 #ifndef HDG_SOA_MINB_HI
 #define HDG_SOA_MINB_HI 3      // CTAs per SM for p >= 3 (154 registers at p = 4 without a cap)
@@ -85,7 +88,10 @@ struct SoaCfg {
   static constexpr int EOFF = VOFF + VB;                 // edge-in blocks: left-in | right-in
   static constexpr int EB = (N1 + 3) & ~3;               // doubles per edge block (whole sectors)
   static constexpr int ENT = EOFF + 2 * EB;              // doubles per record (multiple of 4)
-  static constexpr int WSTRIDE = (RING * ENT + RING + 3) & ~3;   // doubles per warp (32-byte multiple)
+  // high orders keep the deferred first line's bottom part in shared memory (18 registers at n1 = 9)
+  static constexpr bool HOLD_SMEM = N1 >= HDG_SOA_HOLD_SMEM_MIN_N1;
+  static constexpr int HOLD = HOLD_SMEM ? N1 * 32 : 0;
+  static constexpr int WSTRIDE = (RING * ENT + RING + HOLD + 3) & ~3;   // doubles per warp (32-byte multiple)
   static constexpr int SMEM_RING = WPB * WSTRIDE * 8;
 };
 
@@ -346,9 +352,12 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
   const int oL = lane == 0 ? EOFF : VOFF + lane - 1, sL = lane == 0 ? 1 : 31;
   const int oR = lane == 31 ? EOFF + EB : VOFF + lane, sR = lane == 31 ? 1 : 31;
   // tp: the T part of the row below (facet-sum partner); xC: its top H line = this row's bottom
-  double tp[N1], xC[N1], hold[N1];
+  double tp[N1], xC[N1], hold[C::HOLD_SMEM ? 1 : N1];
+  double* holds = ring + RING * ENT + RING + lane;     // HOLD_SMEM: [k * 32 + lane], behind the barriers
 #pragma unroll
-  for (int k = 0; k < N1; ++k) tp[k] = hold[k] = 0.0;
+  for (int k = 0; k < N1; ++k) tp[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < (C::HOLD_SMEM ? 1 : N1); ++k) hold[k] = 0.0;
 
   if (active) {
 #pragma unroll 1
@@ -386,7 +395,10 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
       if (r >= r0) {
         if (t == 0 && defer) {                         // line r0 waits for the warp below
 #pragma unroll
-          for (int k = 0; k < N1; ++k) hold[k] = yB[k];
+          for (int k = 0; k < N1; ++k) {
+            if constexpr (C::HOLD_SMEM) holds[k * 32] = yB[k];
+            else hold[k] = yB[k];
+          }
         } else {                                       // H line r = T(r-1) + B(r)
           const bool hint = hcol && r >= 1;
           double* hrec = Y + rec(r, w);
@@ -455,7 +467,8 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
     const bool hint = hcol && r0 >= 1;
     double* hrec = Y + rec(r0, w);
 #pragma unroll
-    for (int k = 0; k < N1; ++k) hrec[k * 32 + lane] = hint ? src[k * 32 + lane] + hold[k] : 0.0;
+    for (int k = 0; k < N1; ++k)
+      hrec[k * 32 + lane] = hint ? src[k * 32 + lane] + (C::HOLD_SMEM ? holds[k * 32] : hold[C::HOLD_SMEM ? 0 : k]) : 0.0;
   }
   if (active && r1 == a.ny) {                          // top boundary line
     double* hrec = Y + rec(a.ny, w);

@@ -99,8 +99,8 @@ int soa_cyc_h_restrict(const hdg_level* Lf, const HArgs& h, const double* rf, do
   const long long n = h.nhc + (long long)(h.nxc - 1) * h.nyc;
   if (n == 0) return 0;
   const unsigned grid = (unsigned)((n + 127) / 128);
-  if (h.shared_cross) soa_h_restrict_kernel<true><<<grid, 128, 0, s>>>(h, Lf->soaW, rf, rc);
-  else soa_h_restrict_kernel<false><<<grid, 128, 0, s>>>(h, Lf->soaW, rf, rc);
+  if (h.shared_cross) launch_pdl(soa_h_restrict_kernel<true>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, rf, rc);
+  else launch_pdl(soa_h_restrict_kernel<false>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, rf, rc);
   CKL();
   return 0;
 }
@@ -110,8 +110,8 @@ int soa_cyc_h_prolong(const hdg_level* Lf, const HArgs& h, const double* ec, dou
   if (rc0) return rc0;
   const long long n = (long long)(Lf->ny + 1) * Lf->soaW * 65;
   const unsigned grid = (unsigned)((n + 255) / 256);
-  if (h.shared_cross) soa_h_prolong_kernel<true><<<grid, 256, 0, s>>>(h, Lf->soaW, Lf->nx, Lf->ny, ec, xf);
-  else soa_h_prolong_kernel<false><<<grid, 256, 0, s>>>(h, Lf->soaW, Lf->nx, Lf->ny, ec, xf);
+  if (h.shared_cross) launch_pdl(soa_h_prolong_kernel<true>, dim3(grid), dim3(256), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf);
+  else launch_pdl(soa_h_prolong_kernel<false>, dim3(grid), dim3(256), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf);
   CKL();
   return 0;
 }

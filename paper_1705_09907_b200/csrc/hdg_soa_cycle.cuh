@@ -46,6 +46,9 @@ struct SoaCycCfg {
   static constexpr int WSTRIDE = (C::RING * (C::ENT + ENT2) + 2 * C::RING + 3) & ~3;
   static constexpr int SMEM = SoaSmem<N1>::TOTAL * 8 + C::WPB * WSTRIDE * 8;
   static constexpr bool MCONST = N1 <= 5;
+  // the fused epilogues need more registers than the plain apply: from n1 = 8 two CTAs per SM
+  // without spills beat three with (configs[3] p = 8 cycle: 7.8 vs 8.9 ms)
+  static constexpr int MINB = N1 >= 8 ? 2 : SoaCfg<N1>::MINB;
 };
 
 template <int N1>
@@ -87,7 +90,7 @@ __device__ __forceinline__ void soa_epi(const SoaCycArgs<N1>& a, const double* D
 }
 
 template <int N1, int EPI, bool PROL>
-__global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCfg<N1>::MINB)
+__global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCycCfg<N1, EPI, PROL>::MINB)
     soa_cycle_kernel(const __grid_constant__ SoaCycArgs<N1> a) {
   using C = SoaCfg<N1>;
   using K = SoaCycCfg<N1, EPI, PROL>;
@@ -459,6 +462,7 @@ __global__ void soa_h_restrict_kernel(const __grid_constant__ HArgs h, int W, co
                                       double* __restrict__ rc) {
   const long long nvc = (long long)(h.nxc - 1) * h.nyc;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  grid_dependency_wait();
   if (t >= h.nhc + nvc) return;
   double acc[2] = {0.0, 0.0};
   if (t < h.nhc) {   // coarse h(I, J): children fine h(2I, 2J), h(2I+1, 2J)
@@ -492,6 +496,7 @@ __global__ void soa_h_prolong_kernel(const __grid_constant__ HArgs h, int W, int
   using C = SoaCfg<2>;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long nrec = (long long)(nyf + 1) * W;
+  grid_dependency_wait();
   if (t >= nrec * 65) return;
   const long long rw = t / 65;
   const int s = (int)(t % 65), R = (int)(rw / W), w = (int)(rw % W);
