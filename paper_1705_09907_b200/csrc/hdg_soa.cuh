@@ -54,6 +54,12 @@
 #ifndef HDG_SOA_RING
 #define HDG_SOA_RING 3
 #endif
+#ifndef HDG_SOA_RING_P1
+#define HDG_SOA_RING_P1 8
+#endif
+#ifndef HDG_SOA_RING_P2
+#define HDG_SOA_RING_P2 3
+#endif
 #ifndef HDG_SOA_MCONST
 #define HDG_SOA_MCONST -1      // blocks from the constant bank (1) or shared memory (0); -1: by order
                                // (constant bank for p <= 4: 36.7 vs 37.3 us at 1024^2; at p = 8
@@ -82,7 +88,9 @@ struct SoaCfg {
   static constexpr int NTH = 128;
   static constexpr int WPB = NTH / 32;                   // warps (= stacked segments) per CTA
   static constexpr int MINB = N1 <= 3 ? 4 : (N1 <= HDG_SOA_MINB3_MAXN1 ? HDG_SOA_MINB_HI : 2);   // high orders: 255 registers, 2 CTAs/SM (no spills)
-  static constexpr int RING = HDG_SOA_RING;              // ring entries per warp (RING-1 rows in flight)
+  // ring entries per warp (RING-1 rows in flight): the short records of the lowest orders need more
+  // rows in flight to cover the HBM latency (p = 1: 1088-byte records, 16 warps/SM)
+  static constexpr int RING = N1 == 2 ? HDG_SOA_RING_P1 : (N1 == 3 ? HDG_SOA_RING_P2 : HDG_SOA_RING);
   static constexpr int VOFF = N1 * 32;                   // V rows, 31 slots each, packed
   static constexpr int VB = (N1 * 31 + 3) & ~3;          // doubles of the V block (whole sectors)
   static constexpr int EOFF = VOFF + VB;                 // edge-in blocks: left-in | right-in

@@ -3,6 +3,7 @@
 #include "hdg_internal.h"
 #include "hdg_soa_cycle.cuh"
 
+#include <algorithm>
 #include <cstring>
 
 template <int N1, int EPI, bool PROL>
@@ -17,6 +18,8 @@ static int cyc_launch(const hdg_level* L, const double* x, const double* b, doub
   SoaCycArgs<N1> a{};
   a.x = x; a.b = b; a.y = y; a.ec = ec;
   a.nx = L->nx; a.ny = L->ny; a.W = L->soaW; a.nss = L->soaNss;
+  // one wave: the level's segment count was sized for the apply kernel's CTAs per SM
+  if (K::MINB < SoaCfg<N1>::MINB) a.nss = std::max(1, L->soaNss * K::MINB / SoaCfg<N1>::MINB);
   a.w = w; a.w0 = w0;
   std::memcpy(a.M, L->soaM.data(), sizeof(a.M));
   std::memcpy(a.Dh, L->Dh.data(), sizeof(a.Dh));
