@@ -1076,6 +1076,7 @@ int hdg_mg_set_records(hdg_mg* mg, int mode) {
   if (!mg || mode < 0 || mode > 3) return fail(HDG_EINVAL, "record mode must be 0 (off), 1 (auto), 2 (on), 3 (on, unfused prolongation)");
   mg->rec_mode = mode == 3 ? 2 : mode;
   mg->rec_fuse_prolong = mode != 3;
+  mg->rec_fold_first = mode != 3;
   for (auto& kv : mg->graphs) cudaGraphExecDestroy(kv.second.exec);
   mg->graphs.clear();
   return 0;
@@ -1363,6 +1364,7 @@ static int rec_find(hdg_mg* mg) {
         L->ny != L0->ny || L->ndof == 0)
       return 0;
     if (soa_prepare(L)) return 0;
+    soa_prepare_bj0(L);
     if (mg->T[k]->is_h) {
       const HArgs& h = mg->T[k]->ha;
       if (L->n1 != 2 || h.jf0 != 0 || h.jc0 != 0 || h.nyf != 2 * h.nyc || L->nx != 2 * h.nxc || L->ny != h.nyf)
@@ -1413,7 +1415,8 @@ static int cycle_rec_soa(hdg_mg* mg, int k, const double* b, const double* x_in,
       // x = 0: x1 = w1 D^-1 b is formed per facet on the streamed b records and the second sweep
       // runs in the same pass (nu1 = 1: the second step has weight 0)
       const double w1 = bj_weight(L, 1, nu1), w2 = nu1 >= 2 ? bj_weight(L, 2, nu1) : 0.0;
-      if ((rc = soa_cyc_sweep(L, SOA_EPI_BJ0, b, b, A, w2, w1, nullptr, nullptr, s))) return rc;
+      const int epi0 = (!L->soaM0.empty() && mg->rec_fold_first) ? SOA_EPI_BJ0F : SOA_EPI_BJ0;
+      if ((rc = soa_cyc_sweep(L, epi0, b, b, A, w2, w1, nullptr, nullptr, s))) return rc;
       first = nu1 >= 2 ? 2 : 1;
     } else {
       CK(cudaMemsetAsync(A, 0, sizeof(double) * (size_t)soa_len(L), s));
@@ -1721,7 +1724,7 @@ int hdg_pcg(const hdg_level* L, hdg_mg* mg, const double* b, double* x, int use_
 // commutes with both element mirrors, and symmetric when S is (the kernel stores the upper
 // triangles).  Off-block entries or asymmetry above 1e-11 max|M| -> not available.
 template <int N1>
-static bool soa_reduce(const std::vector<double>& S, std::vector<double>& out) {
+static bool soa_reduce(const std::vector<double>& S, std::vector<double>& out, bool symmetric = true) {
   using C = SoaCfg<N1>;
   constexpr int NT = 4 * N1;
   std::vector<double> T(NT * NT), TT(NT * NT);
@@ -1769,13 +1772,44 @@ static bool soa_reduce(const std::vector<double>& S, std::vector<double>& out) {
   for (int i = 0; i < NT; ++i)
     for (int m = 0; m < NT; ++m)
       defect = std::fmax(defect, cls(i) != cls(m) ? std::fabs(M[i * NT + m])
-                                                  : std::fabs(M[i * NT + m] - M[m * NT + i]));
+                                                  : (symmetric ? std::fabs(M[i * NT + m] - M[m * NT + i]) : 0.0));
   if (!(defect <= 1e-11 * mx)) return false;
   out.clear();
   for (int c = 0; c < 4; ++c)
     for (int i = off[c]; i < off[c + 1]; ++i)
-      for (int m = off[c]; m < off[c + 1]; ++m) out.push_back(0.5 * (M[i * NT + m] + M[m * NT + i]));
+      for (int m = off[c]; m < off[c + 1]; ++m)
+        out.push_back(symmetric ? 0.5 * (M[i * NT + m] + M[m * NT + i]) : M[i * NT + m]);
   return (int)out.size() == C::MSZ;
+}
+
+// class blocks of S' = S blockdiag(Dh^-1, Dv^-1, Dh^-1, Dv^-1) (sides bottom, right, top, left): the
+// zero-start double sweep x2 = D^-1((w0 + w) b - w w0 S' b) applies them to the raw right-hand side
+int soa_prepare_bj0(hdg_level* L) {
+  if (L->soaM0_gen == L->smoother_gen && !L->soaM0.empty()) return 0;
+  L->soaM0.clear();
+  if (L->n1 > 5 || !L->has_bj || L->blk.empty() || L->Dh.empty() || L->Dv.empty()) return 0;
+  const int n1 = L->n1, NT = 4 * n1;
+  std::vector<double> Sp((size_t)NT * NT, 0.0);
+  for (int r = 0; r < NT; ++r)
+    for (int sd = 0; sd < 4; ++sd) {
+      const std::vector<double>& Dm = (sd & 1) ? L->Dv : L->Dh;
+      for (int c = 0; c < n1; ++c) {
+        double acc = 0.0;
+        for (int k = 0; k < n1; ++k) acc += L->blk[(size_t)r * NT + sd * n1 + k] * Dm[k * n1 + c];
+        Sp[(size_t)r * NT + sd * n1 + c] = acc;
+      }
+    }
+  bool ok = false;
+  switch (n1) {
+    case 2: ok = soa_reduce<2>(Sp, L->soaM0, false); break;
+    case 3: ok = soa_reduce<3>(Sp, L->soaM0, false); break;
+    case 4: ok = soa_reduce<4>(Sp, L->soaM0, false); break;
+    case 5: ok = soa_reduce<5>(Sp, L->soaM0, false); break;
+    default: break;
+  }
+  if (!ok) L->soaM0.clear();   // D^-1 does not commute with the element mirrors: keep the unfolded sweep
+  L->soaM0_gen = L->smoother_gen;
+  return 0;
 }
 
 template <int N1>

@@ -87,6 +87,8 @@ struct hdg_level {
   std::vector<double> blk;     // the 4n1 x 4n1 element block (shared mode)
   int soa_state = 0;           // 0: not prepared, 1: ready, -1: not available for this level
   std::vector<double> soaM;
+  std::vector<double> soaM0;   // class blocks of S D^-1 (general, full rows): the folded zero-start double sweep
+  unsigned soaM0_gen = ~0u;    // smoother_gen they were formed at
   int soaW = 0, soaNss = 0;
 };
 
@@ -128,6 +130,7 @@ struct hdg_mg {
   int rec_mode = 1;              // 0: off, 1: automatic (large levels), 2: whenever the levels qualify
   int rec_m = 0;
   bool rec_fuse_prolong = true;  // p-prolongation inside the first post-smoothing sweep
+  bool rec_fold_first = true;    // zero-start double sweep in its folded form (p <= 4)
   std::vector<double*> Xr, Tr, Br;
   double* Rr = nullptr;
 };
@@ -136,6 +139,7 @@ struct hdg_mg {
 int sm_count();
 int soa_prepare(hdg_level* L);
 long long soa_len(const hdg_level* L);
+int soa_prepare_bj0(hdg_level* L);   // soaM0 from the element block and the block-Jacobi inverses (n1 <= 5)
 
 // record-layout cycle pieces (hdg_soa_cycle.cu)
 int soa_cyc_sweep(const hdg_level* L, int epi, const double* x, const double* b, double* y, double w, double w0,

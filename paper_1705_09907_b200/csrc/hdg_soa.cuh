@@ -78,7 +78,7 @@
 namespace hdg {
 
 // sweeps of the record-layout cycle (hdg_soa_cycle.cuh)
-enum { SOA_EPI_BJ = 1, SOA_EPI_BJ0 = 2, SOA_EPI_RES = 3, SOA_EPI_RESPR = 4 };
+enum { SOA_EPI_BJ = 1, SOA_EPI_BJ0 = 2, SOA_EPI_RES = 3, SOA_EPI_RESPR = 4, SOA_EPI_BJ0F = 5 };
 
 template <int N1>
 struct SoaCfg {
@@ -242,6 +242,28 @@ __device__ __forceinline__ void soa_block_c(const double* M, const double* t, do
       z[TOFF + i] = fma(v, t[TOFF + j], z[TOFF + i]);
       z[TOFF + j] = fma(v, t[TOFF + i], z[TOFF + j]);
     }
+}
+
+// general (non-symmetric) class blocks from the constant bank: z = M t, every entry one FMA
+template <int SZ, int MOFF, int TOFF>
+__device__ __forceinline__ void soa_block_cg(const double* M, const double* t, double* z) {
+#pragma unroll
+  for (int i = 0; i < SZ; ++i) {
+    double s = M[MOFF + i * SZ] * t[TOFF];
+#pragma unroll
+    for (int j = 1; j < SZ; ++j) s = fma(M[MOFF + i * SZ + j], t[TOFF + j], s);
+    z[TOFF + i] = s;
+  }
+}
+
+template <int N1>
+__device__ __forceinline__ void soa_blocks_cg(const double* M, const double* t, double* z) {
+  using C = SoaCfg<N1>;
+  constexpr int M1 = C::A0 * C::A0, M2 = M1 + C::A1 * C::A1, M3 = M2 + C::A2 * C::A2;
+  soa_block_cg<C::A0, 0, 0>(M, t, z);
+  soa_block_cg<C::A1, M1, C::A0>(M, t, z);
+  soa_block_cg<C::A2, M2, C::A0 + C::A1>(M, t, z);
+  soa_block_cg<C::A3, M3, C::A0 + C::A1 + C::A2>(M, t, z);
 }
 
 template <int N1>

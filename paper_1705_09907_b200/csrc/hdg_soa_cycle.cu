@@ -21,7 +21,12 @@ static int cyc_launch(const hdg_level* L, const double* x, const double* b, doub
   // one wave: the level's segment count was sized for the apply kernel's CTAs per SM
   if (K::MINB < SoaCfg<N1>::MINB) a.nss = std::max(1, L->soaNss * K::MINB / SoaCfg<N1>::MINB);
   a.w = w; a.w0 = w0;
-  std::memcpy(a.M, L->soaM.data(), sizeof(a.M));
+  if (EPI == SOA_EPI_BJ0F) {
+    if (L->soaM0.size() * sizeof(double) != sizeof(a.M)) return fail(HDG_ESTATE, "record cycle: folded blocks not prepared");
+    std::memcpy(a.M, L->soaM0.data(), sizeof(a.M));
+  } else {
+    std::memcpy(a.M, L->soaM.data(), sizeof(a.M));
+  }
   std::memcpy(a.Dh, L->Dh.data(), sizeof(a.Dh));
   std::memcpy(a.Dv, L->Dv.data(), sizeof(a.Dv));
   if (V) std::memcpy(a.V, V, sizeof(a.V));
@@ -44,6 +49,9 @@ template <int N1>
 static int cyc_sweep_t(const hdg_level* L, int epi, const double* x, const double* b, double* y, double w,
                        double w0, const double* V, const double* ec, cudaStream_t s) {
   if (epi == SOA_EPI_BJ0) return cyc_launch<N1, SOA_EPI_BJ0, false>(L, x, b, y, w, w0, V, ec, s);
+  if constexpr (N1 <= 5) {
+    if (epi == SOA_EPI_BJ0F) return cyc_launch<N1, SOA_EPI_BJ0F, false>(L, x, b, y, w, w0, V, ec, s);
+  }
   if (epi == SOA_EPI_RES) return cyc_launch<N1, SOA_EPI_RES, false>(L, x, b, y, w, w0, V, ec, s);
   if constexpr (N1 >= 3) {
     if (epi == SOA_EPI_RESPR) return cyc_launch<N1, SOA_EPI_RESPR, false>(L, x, b, y, w, w0, V, ec, s);

@@ -9,6 +9,9 @@
 //   SEPI_BJ0    x1 = w0 D^-1 b ; y = x1 + w D^-1 (b - A x1) the first two sweeps of a visit that starts
 //                                                          from x = 0 (multigrid.py:400): the ring
 //                                                          streams b, x1 is formed per facet on the fly
+//   SEPI_BJ0F   the same double sweep folded (p <= 4): y = D^-1 ((w0 + w) b - w w0 (S D^-1) b), the element
+//               product runs on the raw b with the class blocks of S D^-1 (one D^-1 per written facet
+//               instead of one per read facet plus one per written facet: 152 instead of 227 FMAs at p = 4)
 //   SEPI_RES    y = b - A x                                residual before an h-restriction
 //   SEPI_RESPR  y_c = V^T (b - A x)                        residual + p-restriction (multigrid.py:399),
 //                                                          written as records of order p - 1
@@ -67,6 +70,16 @@ template <int N1, int EPI>
 __device__ __forceinline__ void soa_epi(const SoaCycArgs<N1>& a, const double* D, const double* ax,
                                         const double* xf, const double* bf, bool valid, double* out) {
   double r[N1];
+  if constexpr (EPI == SOA_EPI_BJ0F) {
+    const double c1 = a.w0 + a.w, c2 = a.w * a.w0;      // ax holds (S D^-1 b) summed over the owners
+    double z[N1];
+#pragma unroll
+    for (int k = 0; k < N1; ++k) r[k] = c1 * bf[k] - c2 * ax[k];
+    soa_dmul<N1>(D, r, z);
+#pragma unroll
+    for (int k = 0; k < N1; ++k) out[k] = valid ? z[k] : 0.0;
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < N1; ++k) r[k] = bf[k] - ax[k];
   if constexpr (EPI == SOA_EPI_RES) {
@@ -99,8 +112,11 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCycCfg<N1, EPI, PROL>::MIN
   constexpr int NT = 4 * N1, RING = C::RING, D = RING - 1, WPB = C::WPB, NO = K::NO, NC = K::NC;
   constexpr int ENT = C::ENT, VOFF = C::VOFF, EOFF = C::EOFF, EB = C::EB;
   constexpr bool MCONST = K::MCONST;
-  constexpr bool BJ0 = EPI == SOA_EPI_BJ0;
-  static_assert(!(PROL && BJ0), "a prolongation never meets a zero iterate");
+  constexpr bool BJ0 = EPI == SOA_EPI_BJ0;            // ring streams b, x1 = w0 D^-1 b formed per facet
+  constexpr bool BJ0F = EPI == SOA_EPI_BJ0F;          // ring streams b, folded form (a.M = blocks of S D^-1)
+  constexpr bool BRING = BJ0 || BJ0F;                 // the right-hand side of the written facets is in the ring
+  static_assert(!(PROL && BRING), "a prolongation never meets a zero iterate");
+  static_assert(!BJ0F || MCONST, "the folded double sweep reads its blocks from the constant bank");
   extern __shared__ __align__(32) double smem_soa[];
   double* Ms = smem_soa;
   if (!MCONST) {
@@ -241,7 +257,7 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCycCfg<N1, EPI, PROL>::MIN
       // right-hand side of the facets this row writes (H line r, V of element row r), one row
       // ahead of their use; SOA_EPI_BJ0 takes them from the ring (the ring streams b)
       double bH[N1], bV[N1];
-      if constexpr (!BJ0) {
+      if constexpr (!BRING) {
         const bool ld = r >= r0;
         const double* bh = B + rec(r, w) + lane;
         const double* bv = B + rec(r + 1, w) + VOFF + lane;
@@ -270,12 +286,13 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCycCfg<N1, EPI, PROL>::MIN
       {
         double tv[NT], z[NT];
         soa_forward<N1>(xB, xR, xT, xL, tv);
-        if (MCONST) soa_blocks_c<N1>(a.M, tv, z);
+        if constexpr (BJ0F) soa_blocks_cg<N1>(a.M, tv, z);
+        else if (MCONST) soa_blocks_c<N1>(a.M, tv, z);
         else soa_blocks<N1>(Ms, tv, z);
         soa_backward<N1>(z, yB, yR, yT, yL);
       }
       if (r >= r0) {
-        if constexpr (BJ0) {                            // the raw ring values are the right-hand side
+        if constexpr (BRING) {                          // the raw ring values are the right-hand side
 #pragma unroll
           for (int k = 0; k < N1; ++k) {
             bH[k] = e0[k * 32 + lane];
@@ -354,7 +371,10 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCycCfg<N1, EPI, PROL>::MIN
 #pragma unroll
     for (int k = 0; k < N1; ++k) ax[k] = src[k * 32 + lane] + hold[k];
     const double* xh = X + rec(r0, w) + lane;
-    if constexpr (BJ0) {
+    if constexpr (BJ0F) {
+#pragma unroll
+      for (int k = 0; k < N1; ++k) { bf[k] = xh[k * 32]; xf[k] = 0.0; }
+    } else if constexpr (BJ0) {
 #pragma unroll
       for (int k = 0; k < N1; ++k) bf[k] = xh[k * 32];
       soa_dmul<N1>(a.Dh, bf, xf);
@@ -461,7 +481,7 @@ template <bool SC>
 __global__ void soa_h_restrict_kernel(const __grid_constant__ HArgs h, int W, const double* __restrict__ rf,
                                       double* __restrict__ rc) {
   const long long nvc = (long long)(h.nxc - 1) * h.nyc;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   grid_dependency_wait();
   if (t >= h.nhc + nvc) return;
   double acc[2] = {0.0, 0.0};
@@ -475,8 +495,11 @@ __global__ void soa_h_restrict_kernel(const __grid_constant__ HArgs h, int W, co
     rec2_cross_restrict<SC>(h, W, rf, I, J - 1, 2, acc);
     rec2_cross_restrict<SC>(h, W, rf, I, J, 0, acc);
   } else {           // coarse v(I, J): children fine v(2I, 2J), v(2I, 2J+1)
+    // consecutive threads walk I (neighbouring slots of the same fine records: coalesced reads); the
+    // coarse vector is vertical-line-major, so the two 8-byte stores are the scattered side
     const long long u = t - h.nhc;
-    const int I = (int)(u / h.nyc) + 1, J = (int)(u % h.nyc);
+    const int J = (int)(u / (h.nxc - 1)), I = (int)(u % (h.nxc - 1)) + 1;
+    t = h.nhc + (long long)(I - 1) * h.nyc + J;
     for (int hf = 0; hf < 2; ++hf) {
       const long long ad = rec2_v(W, 2 * I, 2 * J + hf);
       const double r0 = __ldg(rf + ad), r1 = __ldg(rf + ad + 31);
