@@ -459,10 +459,14 @@ def vcycle_timings(steps=20):
             xp = torch.zeros_like(bp)
             rms = timed(lambda st: _lib.check(L.hdg_mg_cycle_records(mg.handle, bp.data_ptr(), xp.data_ptr(),
                                                                      xp.data_ptr(), 2, 2, 1, 1, st.cuda_stream)))
+            rms0 = timed(lambda st: _lib.check(L.hdg_mg_cycle_records(mg.handle, bp.data_ptr(), 0, xp.data_ptr(), 2, 2,
+                                                                      1, 1, st.cuda_stream)))
             nbytes = vcycle_model_bytes(levels)
             rec["records_resident_ms_per_cycle"] = rms
+            rec["records_resident_zero_guess_ms_per_cycle"] = rms0   # the preconditioner's cycle (x0 = 0)
             rec["roofline"] = {"bound": "hbm", "model_bytes_per_cycle": nbytes, "floor_ms": nbytes / peak / 1e6,
-                               "frac": nbytes / peak / 1e6 / rms, "peak": peak, "unit": "GB/s",
+                               "frac": nbytes / peak / 1e6 / rms, "frac_zero_guess": nbytes / peak / 1e6 / rms0,
+                               "peak": peak, "unit": "GB/s",
                                "frac_reference_layout_api": nbytes / peak / 1e6 / ms}
             _lib.check(L.hdg_mg_set_records(mg.handle, 0))
             rec["reference_layout_cycle_ms"] = timed(lambda st: _lib.check(L.hdg_mg_cycle(
