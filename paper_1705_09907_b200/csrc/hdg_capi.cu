@@ -742,12 +742,17 @@ int hdg_fsai_apply(const hdg_level* L, const double* r, double* z, void* stream)
   return rc;
 }
 
+// x_zero: x is all zeros on entry (a cycle visit from x = 0, multigrid.py:400): the first step's residual
+// is b itself, so its operator apply - a full pass over the level's block stream - is skipped
+// (b - A 0 = b exactly: the iterates are bitwise the same)
 static int fsai_sweeps(const hdg_level* L, const double* b, double* x, double* r, double* t, int steps,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool x_zero = false) {
   for (int k = 1; k <= steps; ++k) {
     int rc;
-    if ((rc = hdg_residual(L, b, x, r, nullptr, s))) return rc;               // r = b - A x
-    if ((rc = spmv(L, false, r, t, nullptr, 0.0, s))) return rc;             // t = G r
+    const double* rk = r;
+    if (k == 1 && x_zero) rk = b;
+    else if ((rc = hdg_residual(L, b, x, r, nullptr, s))) return rc;         // r = b - A x
+    if ((rc = spmv(L, false, rk, t, nullptr, 0.0, s))) return rc;            // t = G r
     if ((rc = spmv(L, true, t, x, x, fsai_weight(L, k, steps), s))) return rc;  // x += w G't
   }
   return 0;
@@ -1296,7 +1301,7 @@ static int cycle_rec(hdg_mg* mg, int k, const double* b, bool zero_init, int nu1
     }
   }
   if (fsai) {
-    if ((rc = fsai_sweeps(L, b, cur, mg->R[k], oth, nu1, s))) return rc;
+    if ((rc = fsai_sweeps(L, b, cur, mg->R[k], oth, nu1, s, zero_init && L->ndof > 0))) return rc;
   } else {
     for (int it = first; it < nu1; ++it) {
       if ((rc = bj_sweep_w(L, b, cur, oth, bj_weight(L, it + 1, nu1), s))) return rc;
