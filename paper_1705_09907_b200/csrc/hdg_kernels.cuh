@@ -84,7 +84,7 @@ namespace cg = cooperative_groups;
 #define HDG_PAIR_STAGES 4       // ring stages per warp of the merged stored pass (3 block rows in flight)
 #endif
 #ifndef HDG_PAIR_MIN_N1
-#define HDG_PAIR_MIN_N1 6      // merged h/v pass over the half-stored stream from this n1 (hdg_kernels.cuh: apply_stored_pair)
+#define HDG_PAIR_MIN_N1 6      // merged h/v pass over the half-stored stream from this n1 (apply_stored_pair; at n1 = 5 it loses: 0.88 -> 0.77)
 #endif
 #define HDG_SYMSTORE_EF_MIN_N1 7   // half-stored stream: evict-first hint on the owner's read from this n1
 #endif                             // (measured: p=8 192 vs 207 us, p=4 118 vs 105 us, p=1 69 vs 62 us)
