@@ -98,6 +98,12 @@ class ClockSampler:
 
             self.t = threading.Thread(target=run, daemon=True)
             self.t.start()
+            # the timed region is tens of ms: hand control back only once the sampler is running,
+            # then drop what it saw while the GPU was still idle
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 1.0:
+                time.sleep(0.001)
+            del self.rows[:]
         except Exception:
             self.t = None
         return self
