@@ -185,7 +185,7 @@ int hdg_mg_set_fused_tail(hdg_mg* mg, int enable);
  * record kernel with the update fused (first two sweeps from x = 0, residual + p-restriction,
  * p-prolongation + first post-sweep are single passes); b is packed and x unpacked at the
  * cycle's boundary, the levels below m use the reference layout.  mode 0: off, 1 (default):
- * when level 0 has >= 2^20 dofs (env HDG_REC_MIN_DOF), 2: whenever the levels qualify, 3: as 2
+ * when level 0 has p >= 2 and >= 2^13 dofs (env HDG_REC_MIN_DOF), 2: whenever the levels qualify, 3: as 2
  * with the p-prolongation as its own kernel.  hdg_mg_record_levels returns m of the last
  * cycle (0: reference layout). */
 int hdg_mg_set_records(hdg_mg* mg, int mode);

@@ -1353,7 +1353,7 @@ static long long rec_min_dof() {
   static long long v = -1;
   if (v < 0) {
     const char* e = std::getenv("HDG_REC_MIN_DOF");
-    v = e ? std::atoll(e) : (1LL << 20);
+    v = e ? std::atoll(e) : (1LL << 13);
   }
   return v;
 }
@@ -1361,7 +1361,9 @@ static long long rec_min_dof() {
 static int rec_find(hdg_mg* mg) {
   if (mg->rec_mode == 0 || mg->n < 2) return 0;
   hdg_level* L0 = mg->L[0];
-  if (mg->rec_mode == 1 && L0->ndof < rec_min_dof()) return 0;
+  // automatic mode: hierarchies with a p-ladder from ~8k fine dofs (measured faster from 32^2, p = 4 up to
+  // 1024^2, p = 4; a p = 1 hierarchy has a single record level and only pays the layout changes)
+  if (mg->rec_mode == 1 && (L0->ndof < rec_min_dof() || L0->n1 < 3)) return 0;
   int m = 0;
   for (int k = 0; k + 1 < mg->n; ++k) {
     hdg_level* L = mg->L[k];
