@@ -1591,30 +1591,54 @@ static int fetch(const double* dsrc, double* h, int count, cudaStream_t s) {
   return 0;
 }
 
+static int run_cycle(hdg_mg* mg, bool records, const double* b, const double* x0, double* x, int nu1, int nu2,
+                     int visits, int use_graph, void* stream);
+
 int hdg_solve_mg(hdg_mg* mg, const double* b, double* x, int nu1, int nu2, int visits, double tol,
                  int max_cycles, double* res_hist, int* ncycles, void* stream) {
   if (!mg || !b || !x || !res_hist || !ncycles) return fail(HDG_EINVAL, "null argument");
   if (max_cycles < 0) return fail(HDG_EINVAL, "max_cycles must be >= 0");
   cudaStream_t s = S(stream);
-  const hdg_level* L0 = mg->L[0];
+  hdg_level* L0 = mg->L[0];
   const long long n = L0->ndof;
   *ncycles = 0;
   if (n == 0) { res_hist[0] = 0.0; return 0; }
-  double* scal = nullptr;
-  double* partials = nullptr;
+  refresh_graphs(mg);
+  int rc = tail_prepare(mg);
+  if (!rc) rc = rec_prepare(mg);
+  if (rc) return rc;
+  // with record levels the whole loop keeps b, x and the residual as facet records: one pack of b and
+  // x0, one unpack of x, no layout change per cycle
+  const bool rec = mg->rec_m > 0;
+  const int nb = vec_blocks();
+  double *scal = nullptr, *partials = nullptr, *bR = nullptr, *xR = nullptr, *rR = nullptr;
   CK(cudaMallocAsync((void**)&scal, sizeof(double) * 2, s));
-  CK(cudaMallocAsync((void**)&partials, sizeof(double) * vec_blocks(), s));
-  int rc = dot_into(b, b, n, scal, partials, s);
+  CK(cudaMallocAsync((void**)&partials, sizeof(double) * nb, s));
+  if (rec) {
+    const size_t rb = sizeof(double) * (size_t)soa_len(L0);
+    CK(cudaMallocAsync((void**)&bR, rb, s));
+    CK(cudaMallocAsync((void**)&xR, rb, s));
+    CK(cudaMallocAsync((void**)&rR, rb, s));
+    rc = hdg_soa_pack(L0, b, bR, s);
+    if (!rc) rc = hdg_soa_pack(L0, x, xR, s);
+  }
+  auto resnorm = [&]() -> int {                                   // scal[1] = ||b - A x||^2
+    if (!rec) return hdg_residual(L0, b, x, nullptr, scal + 1, s);
+    int r2 = soa_cyc_sweep(L0, SOA_EPI_RES, xR, bR, rR, 0.0, 0.0, nullptr, nullptr, s);
+    return r2 ? r2 : soa_cyc_norm2(L0, rR, scal + 1, partials, nb, s);
+  };
+  if (!rc) rc = dot_into(b, b, n, scal, partials, s);
   double h[2];
-  if (!rc) rc = hdg_residual(L0, b, x, nullptr, scal + 1, s);
+  if (!rc) rc = resnorm();
   if (!rc) rc = fetch(scal, h, 2, s);
   const double bnorm = (rc || h[0] == 0.0) ? 1.0 : std::sqrt(h[0]);
   if (!rc) res_hist[0] = std::sqrt(h[1]);
   int k = 0;
   while (!rc && k < max_cycles) {
     if (res_hist[k] <= tol * bnorm) break;                     // multigrid.py:433
-    rc = hdg_mg_cycle(mg, b, x, x, nu1, nu2, visits, 1, stream);
-    if (!rc) rc = hdg_residual(L0, b, x, nullptr, scal + 1, s);
+    rc = rec ? run_cycle(mg, true, bR, xR, xR, nu1, nu2, visits, 1, stream)
+             : hdg_mg_cycle(mg, b, x, x, nu1, nu2, visits, 1, stream);
+    if (!rc) rc = resnorm();
     if (!rc) rc = fetch(scal + 1, h + 1, 1, s);
     if (rc) break;
     res_hist[++k] = std::sqrt(h[1]);
@@ -1627,6 +1651,8 @@ int hdg_solve_mg(hdg_mg* mg, const double* b, double* x, int nu1, int nu2, int v
       if (div) break;
     }
   }
+  if (rec && !rc) rc = hdg_soa_unpack(L0, xR, x, s);
+  if (rec) { cudaFreeAsync(rR, s); cudaFreeAsync(xR, s); cudaFreeAsync(bR, s); }
   cudaFreeAsync(partials, s);
   cudaFreeAsync(scal, s);
   *ncycles = k;

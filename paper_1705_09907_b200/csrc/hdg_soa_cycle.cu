@@ -126,3 +126,19 @@ int soa_cyc_h_prolong(const hdg_level* Lf, const HArgs& h, const double* ec, dou
   CKL();
   return 0;
 }
+
+// *out = ||r||^2 of a record vector (device scalar), `partials` holds at least `nblocks` doubles
+int soa_cyc_norm2(const hdg_level* L, const double* r, double* out, double* partials, int nblocks, cudaStream_t s) {
+  if (L->soa_state != 1) return fail(HDG_ESTATE, "record norm: level not prepared");
+  const long long nrec = (long long)(L->ny + 1) * L->soaW;
+#define NRM(N) case N: soa_norm2_kernel<N><<<nblocks, 256, 0, s>>>(r, nrec, L->soaW, partials); break;
+  switch (L->n1) {
+    NRM(2) NRM(3) NRM(4) NRM(5) NRM(6) NRM(7) NRM(8) NRM(9)
+    default: return fail(HDG_EINVAL, "record norm: order not built");
+  }
+#undef NRM
+  CKL();
+  sum_partials_kernel<<<1, 32, 0, s>>>(partials, nblocks, out);
+  CKL();
+  return 0;
+}

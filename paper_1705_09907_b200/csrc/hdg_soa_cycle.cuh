@@ -571,4 +571,35 @@ __global__ void soa_h_prolong_kernel(const __grid_constant__ HArgs h, int W, int
   x[st] += add[1];
 }
 
+// sum of squares of a record vector over the trace dofs (every dof once: slot 31 of an H row repeats
+// the next tile's slot 0 and the edge blocks repeat V lines of the neighbouring tiles; pads are zeros).
+// Per-CTA partials in a fixed order; sum_partials_kernel finishes (deterministic).
+template <int N1>
+__global__ void __launch_bounds__(256) soa_norm2_kernel(const double* __restrict__ r, long long nrec, int W,
+                                                        double* __restrict__ partials) {
+  using C = SoaCfg<N1>;
+  double s = 0.0;
+  const long long total = nrec * 63;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    const long long rw = t / 63;
+    const int sl = (int)(t - rw * 63);
+    if (sl == 31 && (int)(rw % W) != W - 1) continue;
+    int off, st;
+    soa_slot<N1>(sl, off, st);
+    const double* q = r + rw * C::ENT + off;
+#pragma unroll
+    for (int k = 0; k < N1; ++k) { const double v = q[k * st]; s = fma(v, v, s); }
+  }
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    partials[blockIdx.x] = t;
+  }
+}
+
 }  // namespace hdg
