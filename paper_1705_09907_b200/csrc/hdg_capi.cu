@@ -1669,49 +1669,75 @@ int hdg_pcg(const hdg_level* L, hdg_mg* mg, const double* b, double* x, int use_
   *iters = 0;
   if (n == 0) { if (res_hist) res_hist[0] = 0.0; return 0; }
   const int nb = vec_blocks();
-  const size_t vb = sizeof(double) * (size_t)n;
+  int rc = 0;
+  if (mg) { refresh_graphs(mg); if ((rc = tail_prepare(mg))) return rc; if ((rc = rec_prepare(mg))) return rc; }
+  // preconditioner with record levels on the operator's own level: every CG vector is a facet record for
+  // the whole solve (operator apply = the record kernel, dots masked to the trace dofs, updates
+  // slot-wise: pads and duplicate slots stay consistent); b and x0 are packed once, x unpacked once
+  hdg_level* L0 = mg ? mg->L[0] : nullptr;
+  const bool rec = mg && mg->rec_m > 0 && L0 == L;
+  const long long N = rec ? soa_len(L0) : n;                     // vector length of the loop
+  const size_t vb = sizeof(double) * (size_t)N;
   double *r = nullptr, *z = nullptr, *d = nullptr, *ad = nullptr, *scal = nullptr, *part = nullptr;
+  double *xw = x, *bw = nullptr;                                 // working iterate / packed right-hand side
   CK(cudaMallocAsync((void**)&r, vb, s));
   CK(cudaMallocAsync((void**)&d, vb, s));
   CK(cudaMallocAsync((void**)&ad, vb, s));
   if (mg) CK(cudaMallocAsync((void**)&z, vb, s)); else z = r;
+  if (rec) { CK(cudaMallocAsync((void**)&xw, vb, s)); CK(cudaMallocAsync((void**)&bw, vb, s)); }
   CK(cudaMallocAsync((void**)&scal, sizeof(double) * 8, s));
   CK(cudaMallocAsync((void**)&part, sizeof(double) * 2 * nb, s));
   cudaStream_t cs = nullptr;
   cudaGraphExec_t body = nullptr;
-  int rc = 0;
   auto precond = [&](cudaStream_t st) -> int {                   // z = M r (one V-cycle from zero)
-    return mg ? cycle_issue(mg, r, nullptr, z, nu1, nu2, 1, st) : 0;
+    if (!mg) return 0;
+    return rec ? cycle_issue_any(mg, true, r, nullptr, z, nu1, nu2, 1, st) : cycle_issue(mg, r, nullptr, z, nu1, nu2, 1, st);
+  };
+  auto dot = [&](const double* u, const double* v, double* out, cudaStream_t st) -> int {
+    return rec ? soa_cyc_dot2(L0, u, v, out, nullptr, nullptr, nullptr, part, nb, st) : dot_into(u, v, n, out, part, st);
   };
   do {
-    if (mg) { refresh_graphs(mg); if ((rc = tail_prepare(mg))) break; if ((rc = rec_prepare(mg))) break; }
     // r = b - A x0 (trace.py:147), z = M r, d = z, rz = r.z
-    if (use_x0) { if ((rc = hdg_residual(L, b, x, r, nullptr, s))) break; }
-    else {
-      if (cudaMemsetAsync(x, 0, vb, s) != cudaSuccess || cudaMemcpyAsync(r, b, vb, cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+    if (rec && (rc = hdg_soa_pack(L0, b, bw, s))) break;
+    if (use_x0) {
+      if (rec) {
+        if ((rc = hdg_soa_pack(L0, x, xw, s))) break;
+        if ((rc = soa_cyc_sweep(L0, SOA_EPI_RES, xw, bw, r, 0.0, 0.0, nullptr, nullptr, s))) break;
+      } else if ((rc = hdg_residual(L, b, x, r, nullptr, s))) break;
+    } else {
+      if (cudaMemsetAsync(xw, 0, vb, s) != cudaSuccess ||
+          cudaMemcpyAsync(r, rec ? bw : b, vb, cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
         rc = fail(HDG_ECUDA, "pcg init copies"); break;
       }
     }
     if ((rc = precond(s))) break;
     if (cudaMemcpyAsync(d, z, vb, cudaMemcpyDeviceToDevice, s) != cudaSuccess) { rc = fail(HDG_ECUDA, "pcg copy"); break; }
-    if ((rc = dot_into(r, z, n, scal + 0, part, s))) break;
+    if ((rc = dot(r, z, scal + 0, s))) break;
     if ((rc = dot_into(b, b, n, scal + 4, part, s))) break;
-    if ((rc = dot_into(r, r, n, scal + 3, part, s))) break;
+    if ((rc = dot(r, r, scal + 3, s))) break;
     // one iteration body (trace.py:153-162) captured once, replayed per iteration
     if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) { rc = fail(HDG_ECUDA, "stream"); break; }
     const long long c0 = g_launches.load();
     if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { rc = fail(HDG_ECUDA, "capture"); break; }
     {
-      MvArgs a{};
-      a.x = d; a.out = ad;
-      rc = apply(L, EPI_Y, a, cs);                                            // ad = A d
-      if (!rc) rc = dot_into(d, ad, n, scal + 1, part, cs);                   // d.Ad
-      if (!rc) { cg_update_dev_kernel<<<nb, 256, 0, cs>>>(x, r, d, ad, scal, n); CKL(); }
+      if (rec) {
+        rc = hdg_matvec_soa(L0, d, ad, cs);                                   // ad = A d
+      } else {
+        MvArgs a{};
+        a.x = d; a.out = ad;
+        rc = apply(L, EPI_Y, a, cs);
+      }
+      if (!rc) rc = dot(d, ad, scal + 1, cs);                                 // d.Ad
+      if (!rc) { cg_update_dev_kernel<<<nb, 256, 0, cs>>>(xw, r, d, ad, scal, N); CKL(); }
       if (!rc) rc = precond(cs);                                              // z = M r
-      if (!rc) { dot2_partials_kernel<<<nb, 256, 0, cs>>>(r, z, r, r, n, part); CKL(); }
-      if (!rc) { sum_partials_kernel<<<1, 32, 0, cs>>>(part, nb, scal + 2); CKL(); }       // r.z
-      if (!rc) { sum_partials_kernel<<<1, 32, 0, cs>>>(part + nb, nb, scal + 3); CKL(); }  // r.r
-      if (!rc) { xpby_dev_kernel<<<nb, 256, 0, cs>>>(z, scal, d, n); CKL(); }              // d = z + beta d
+      if (rec) {
+        if (!rc) rc = soa_cyc_dot2(L0, r, z, scal + 2, r, r, scal + 3, part, nb, cs);        // r.z, r.r
+      } else {
+        if (!rc) { dot2_partials_kernel<<<nb, 256, 0, cs>>>(r, z, r, r, n, part); CKL(); }
+        if (!rc) { sum_partials_kernel<<<1, 32, 0, cs>>>(part, nb, scal + 2); CKL(); }       // r.z
+        if (!rc) { sum_partials_kernel<<<1, 32, 0, cs>>>(part + nb, nb, scal + 3); CKL(); }  // r.r
+      }
+      if (!rc) { xpby_dev_kernel<<<nb, 256, 0, cs>>>(z, scal, d, N); CKL(); }              // d = z + beta d
       if (!rc && cudaMemcpyAsync(scal, scal + 2, sizeof(double), cudaMemcpyDeviceToDevice, cs) != cudaSuccess)
         rc = fail(HDG_ECUDA, "pcg scalar copy");
     }
@@ -1739,10 +1765,12 @@ int hdg_pcg(const hdg_level* L, hdg_mg* mg, const double* b, double* x, int use_
     }
     if (!rc && it == maxiter && res_hist) res_hist[maxiter] = std::sqrt(rr);
     *iters = it;
+    if (!rc && rec) rc = hdg_soa_unpack(L0, xw, x, s);
   } while (false);
   if (body) cudaGraphExecDestroy(body);
   if (cs) cudaStreamDestroy(cs);
   cudaFreeAsync(part, s); cudaFreeAsync(scal, s);
+  if (rec) { cudaFreeAsync(bw, s); cudaFreeAsync(xw, s); }
   cudaFreeAsync(ad, s); cudaFreeAsync(d, s); cudaFreeAsync(r, s);
   if (mg) cudaFreeAsync(z, s);
   return rc;

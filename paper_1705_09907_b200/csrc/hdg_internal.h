@@ -149,3 +149,5 @@ int soa_cyc_p_prolong(const hdg_level* Lf, const hdg_level* Lc, const double* ec
 int soa_cyc_h_restrict(const hdg_level* Lf, const HArgs& h, const double* rf, double* rc, cudaStream_t s);
 int soa_cyc_h_prolong(const hdg_level* Lf, const HArgs& h, const double* ec, double* xf, cudaStream_t s);
 int soa_cyc_norm2(const hdg_level* L, const double* r, double* out, double* partials, int nblocks, cudaStream_t s);
+int soa_cyc_dot2(const hdg_level* L, const double* a, const double* b, double* out, const double* c, const double* e,
+                 double* out2, double* partials, int nblocks, cudaStream_t s);

@@ -127,18 +127,28 @@ int soa_cyc_h_prolong(const hdg_level* Lf, const HArgs& h, const double* ec, dou
   return 0;
 }
 
-// *out = ||r||^2 of a record vector (device scalar), `partials` holds at least `nblocks` doubles
-int soa_cyc_norm2(const hdg_level* L, const double* r, double* out, double* partials, int nblocks, cudaStream_t s) {
-  if (L->soa_state != 1) return fail(HDG_ESTATE, "record norm: level not prepared");
+// out[0] = a.b, and out2[0] = c.e when c is given, over the trace dofs of record vectors (device scalars);
+// `partials` holds at least 2 * nblocks doubles
+int soa_cyc_dot2(const hdg_level* L, const double* a, const double* b, double* out, const double* c, const double* e,
+                 double* out2, double* partials, int nblocks, cudaStream_t s) {
+  if (L->soa_state != 1) return fail(HDG_ESTATE, "record dot: level not prepared");
   const long long nrec = (long long)(L->ny + 1) * L->soaW;
-#define NRM(N) case N: soa_norm2_kernel<N><<<nblocks, 256, 0, s>>>(r, nrec, L->soaW, partials); break;
+#define DOT(N) case N: soa_dot2_kernel<N><<<nblocks, 256, 0, s>>>(a, b, c, e, nrec, L->soaW, partials); break;
   switch (L->n1) {
-    NRM(2) NRM(3) NRM(4) NRM(5) NRM(6) NRM(7) NRM(8) NRM(9)
-    default: return fail(HDG_EINVAL, "record norm: order not built");
+    DOT(2) DOT(3) DOT(4) DOT(5) DOT(6) DOT(7) DOT(8) DOT(9)
+    default: return fail(HDG_EINVAL, "record dot: order not built");
   }
-#undef NRM
+#undef DOT
   CKL();
   sum_partials_kernel<<<1, 32, 0, s>>>(partials, nblocks, out);
   CKL();
+  if (c) {
+    sum_partials_kernel<<<1, 32, 0, s>>>(partials + nblocks, nblocks, out2);
+    CKL();
+  }
   return 0;
+}
+
+int soa_cyc_norm2(const hdg_level* L, const double* r, double* out, double* partials, int nblocks, cudaStream_t s) {
+  return soa_cyc_dot2(L, r, r, out, nullptr, nullptr, nullptr, partials, nblocks, s);
 }

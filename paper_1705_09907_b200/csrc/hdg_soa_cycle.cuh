@@ -571,14 +571,16 @@ __global__ void soa_h_prolong_kernel(const __grid_constant__ HArgs h, int W, int
   x[st] += add[1];
 }
 
-// sum of squares of a record vector over the trace dofs (every dof once: slot 31 of an H row repeats
-// the next tile's slot 0 and the edge blocks repeat V lines of the neighbouring tiles; pads are zeros).
-// Per-CTA partials in a fixed order; sum_partials_kernel finishes (deterministic).
+// a.b (and c.e when c != nullptr) of record vectors over the trace dofs, every dof once: slot 31 of an H
+// row repeats the next tile's slot 0 and the edge blocks repeat V lines of the neighbouring tiles; pads
+// are zeros.  Per-CTA partials in a fixed order (partials[blk], partials[grid + blk]);
+// sum_partials_kernel finishes (deterministic).
 template <int N1>
-__global__ void __launch_bounds__(256) soa_norm2_kernel(const double* __restrict__ r, long long nrec, int W,
-                                                        double* __restrict__ partials) {
+__global__ void __launch_bounds__(256) soa_dot2_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                                       const double* __restrict__ c, const double* __restrict__ e,
+                                                       long long nrec, int W, double* __restrict__ partials) {
   using C = SoaCfg<N1>;
-  double s = 0.0;
+  double s = 0.0, s2 = 0.0;
   const long long total = nrec * 63;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     const long long rw = t / 63;
@@ -586,19 +588,26 @@ __global__ void __launch_bounds__(256) soa_norm2_kernel(const double* __restrict
     if (sl == 31 && (int)(rw % W) != W - 1) continue;
     int off, st;
     soa_slot<N1>(sl, off, st);
-    const double* q = r + rw * C::ENT + off;
+    const long long o = rw * C::ENT + off;
 #pragma unroll
-    for (int k = 0; k < N1; ++k) { const double v = q[k * st]; s = fma(v, v, s); }
+    for (int k = 0; k < N1; ++k) {
+      s = fma(a[o + k * st], b[o + k * st], s);
+      if (c != nullptr) s2 = fma(c[o + k * st], e[o + k * st], s2);
+    }
   }
-  __shared__ double red[8];
+  __shared__ double red[2][8];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = s; red[1][threadIdx.x >> 5] = s2; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += red[w];
+    double t = 0.0, t2 = 0.0;
+    for (int w = 0; w < 8; ++w) { t += red[0][w]; t2 += red[1][w]; }
     partials[blockIdx.x] = t;
+    if (c != nullptr) partials[gridDim.x + blockIdx.x] = t2;
   }
 }
 
