@@ -14,7 +14,7 @@
 using namespace hdg;
 
 static const int SOA_MAXN1 = 13;        // facet-record apply (hdg_soa.cuh)
-static const int SOA_CYCLE_MAXN1 = 9;   // record-layout cycle kernels (hdg_soa_cycle.cuh)
+static const int SOA_CYCLE_MAXN1 = 13;   // record-layout cycle kernels (hdg_soa_cycle.cuh)
 
 extern std::atomic<long long> g_launches;
 int fail(int code, const std::string& msg);   // sets hdg_last_error, returns code

@@ -75,6 +75,10 @@ int soa_cyc_sweep(const hdg_level* L, int epi, const double* x, const double* b,
     case 7: return cyc_sweep_t<7>(L, epi, x, b, y, w, w0, V, ec, s);
     case 8: return cyc_sweep_t<8>(L, epi, x, b, y, w, w0, V, ec, s);
     case 9: return cyc_sweep_t<9>(L, epi, x, b, y, w, w0, V, ec, s);
+    case 10: return cyc_sweep_t<10>(L, epi, x, b, y, w, w0, V, ec, s);
+    case 11: return cyc_sweep_t<11>(L, epi, x, b, y, w, w0, V, ec, s);
+    case 12: return cyc_sweep_t<12>(L, epi, x, b, y, w, w0, V, ec, s);
+    case 13: return cyc_sweep_t<13>(L, epi, x, b, y, w, w0, V, ec, s);
 #endif
     default: return fail(HDG_EINVAL, "record cycle: order not built");
   }
@@ -90,7 +94,7 @@ int soa_cyc_p_prolong(const hdg_level* Lf, const hdg_level* Lc, const double* ec
   const unsigned grid = (unsigned)((nrec * 65 + 255) / 256);
 #define PP(N) case N: soa_p_prolong_kernel<N><<<grid, 256, 0, s>>>(ec, xf, nrec, pa); break;
   switch (Lf->n1) {
-    PP(3) PP(4) PP(5) PP(6) PP(7) PP(8) PP(9)
+    PP(3) PP(4) PP(5) PP(6) PP(7) PP(8) PP(9) PP(10) PP(11) PP(12) PP(13)
     default: return fail(HDG_EINVAL, "record p-prolongation: order not built");
   }
 #undef PP
@@ -135,7 +139,7 @@ int soa_cyc_dot2(const hdg_level* L, const double* a, const double* b, double* o
   const long long nrec = (long long)(L->ny + 1) * L->soaW;
 #define DOT(N) case N: soa_dot2_kernel<N><<<nblocks, 256, 0, s>>>(a, b, c, e, nrec, L->soaW, partials); break;
   switch (L->n1) {
-    DOT(2) DOT(3) DOT(4) DOT(5) DOT(6) DOT(7) DOT(8) DOT(9)
+    DOT(2) DOT(3) DOT(4) DOT(5) DOT(6) DOT(7) DOT(8) DOT(9) DOT(10) DOT(11) DOT(12) DOT(13)
     default: return fail(HDG_EINVAL, "record dot: order not built");
   }
 #undef DOT

@@ -24,7 +24,7 @@ def _hier(P, nx, ny, p):
 
 
 @pytest.mark.parametrize("nx,ny,p", [(16, 16, 1), (32, 32, 2), (40, 24, 3), (64, 64, 4), (36, 44, 5), (24, 24, 8),
-                                     (66, 8, 2), (8, 70, 4), (2, 2, 3), (4, 2, 2)])
+                                     (66, 8, 2), (8, 70, 4), (2, 2, 3), (4, 2, 2), (16, 16, 10), (20, 12, 12)])
 def test_record_vcycle_matches_oracle(P, nx, ny, p):
     levels, lo = _hier(P, nx, ny, p)
     rng = np.random.default_rng(nx * 100 + p)
