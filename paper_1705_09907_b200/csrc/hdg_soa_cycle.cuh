@@ -23,6 +23,10 @@
 #pragma once
 #include "hdg_soa.cuh"
 
+#ifndef HDG_SOA_BAHEAD_MAX_N1
+#define HDG_SOA_BAHEAD_MAX_N1 5    // right-hand side fetched one row ahead up to this n1 (above: spills, p = 8 cycle 7.8 -> 8.1 ms)
+#endif
+
 namespace hdg {
 
 template <int N1>
@@ -248,6 +252,25 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCycCfg<N1, EPI, PROL>::MIN
     }
   };
 
+  // right-hand side of the facets a row writes (H line r, V of element row r), straight from global
+  // memory; at the lowest orders a row's arithmetic is too short to cover the load, so the values of
+  // the coming row are fetched one row ahead (BAHEAD)
+  constexpr bool BAHEAD = !BRING && N1 <= HDG_SOA_BAHEAD_MAX_N1;
+  auto loadb = [&](int r, double* bh_out, double* bv_out) {
+    const bool ld = r >= r0;
+    const double* bh = B + rec(r, w) + lane;
+    const double* bv = B + rec(r + 1, w) + VOFF + lane;
+#pragma unroll
+    for (int k = 0; k < N1; ++k) {
+      bh_out[k] = ld ? __ldg(bh + k * 32) : 0.0;
+      bv_out[k] = (ld && lane < 31) ? __ldg(bv + k * 31) : 0.0;
+    }
+  };
+  double bHn[BAHEAD ? N1 : 1], bVn[BAHEAD ? N1 : 1];
+  if constexpr (BAHEAD) {
+    if (active) loadb(rs, bHn, bVn);
+  }
+
   if (active) {
 #pragma unroll 1
     for (int t = 0; t < nrows; ++t) {
@@ -258,13 +281,12 @@ __global__ void __launch_bounds__(SoaCfg<N1>::NTH, SoaCycCfg<N1, EPI, PROL>::MIN
       // ahead of their use; SOA_EPI_BJ0 takes them from the ring (the ring streams b)
       double bH[N1], bV[N1];
       if constexpr (!BRING) {
-        const bool ld = r >= r0;
-        const double* bh = B + rec(r, w) + lane;
-        const double* bv = B + rec(r + 1, w) + VOFF + lane;
+        if constexpr (BAHEAD) {                          // loaded during the previous row
 #pragma unroll
-        for (int k = 0; k < N1; ++k) {
-          bH[k] = ld ? __ldg(bh + k * 32) : 0.0;
-          bV[k] = (ld && lane < 31) ? __ldg(bv + k * 31) : 0.0;
+          for (int k = 0; k < N1; ++k) { bH[k] = bHn[k]; bV[k] = bVn[k]; }
+          if (t + 1 < nrows) loadb(r + 1, bHn, bVn);
+        } else {
+          loadb(r, bH, bV);
         }
       }
       if (t == 0) mbar_wait(bars, 0);
