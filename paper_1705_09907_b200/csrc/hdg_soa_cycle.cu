@@ -123,10 +123,11 @@ int soa_cyc_h_restrict(const hdg_level* Lf, const HArgs& h, const double* rf, do
 int soa_cyc_h_prolong(const hdg_level* Lf, const HArgs& h, const double* ec, double* xf, cudaStream_t s) {
   int rc0 = h_check(Lf, h);
   if (rc0) return rc0;
-  const long long n = (long long)(Lf->ny + 1) * Lf->soaW * 65;
-  const unsigned grid = (unsigned)((n + 255) / 256);
-  if (h.shared_cross) launch_pdl(soa_h_prolong_kernel<true>, dim3(grid), dim3(256), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf);
-  else launch_pdl(soa_h_prolong_kernel<false>, dim3(grid), dim3(256), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf);
+  const long long n = (long long)h.nxc * h.nyc;           // one thread per coarse element
+  if (n == 0) return 0;
+  const unsigned grid = (unsigned)((n + 127) / 128);
+  if (h.shared_cross) launch_pdl(soa_h_prolong_kernel<true>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf);
+  else launch_pdl(soa_h_prolong_kernel<false>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf);
   CKL();
   return 0;
 }

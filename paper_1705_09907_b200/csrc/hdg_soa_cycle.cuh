@@ -82,27 +82,27 @@ __device__ __forceinline__ void soa_epi(const SoaCycArgs<N1>& a, const double* D
     soa_dmul<N1>(D, r, z);
 #pragma unroll
     for (int k = 0; k < N1; ++k) out[k] = valid ? z[k] : 0.0;
-    return;
-  }
-#pragma unroll
-  for (int k = 0; k < N1; ++k) r[k] = bf[k] - ax[k];
-  if constexpr (EPI == SOA_EPI_RES) {
-#pragma unroll
-    for (int k = 0; k < N1; ++k) out[k] = valid ? r[k] : 0.0;
-  } else if constexpr (EPI == SOA_EPI_RESPR) {
-    constexpr int NC = N1 - 1;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      double s = a.V[c] * r[0];
-#pragma unroll
-      for (int k = 1; k < N1; ++k) s = fma(a.V[k * NC + c], r[k], s);
-      out[c] = valid ? s : 0.0;
-    }
   } else {
-    double z[N1];
-    soa_dmul<N1>(D, r, z);
 #pragma unroll
-    for (int k = 0; k < N1; ++k) out[k] = valid ? fma(a.w, z[k], xf[k]) : 0.0;
+    for (int k = 0; k < N1; ++k) r[k] = bf[k] - ax[k];
+    if constexpr (EPI == SOA_EPI_RES) {
+#pragma unroll
+      for (int k = 0; k < N1; ++k) out[k] = valid ? r[k] : 0.0;
+    } else if constexpr (EPI == SOA_EPI_RESPR) {
+      constexpr int NC = N1 - 1;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        double s = a.V[c] * r[0];
+#pragma unroll
+        for (int k = 1; k < N1; ++k) s = fma(a.V[k * NC + c], r[k], s);
+        out[c] = valid ? s : 0.0;
+      }
+    } else {
+      double z[N1];
+      soa_dmul<N1>(D, r, z);
+#pragma unroll
+      for (int k = 0; k < N1; ++k) out[k] = valid ? fma(a.w, z[k], xf[k]) : 0.0;
+    }
   }
 }
 
@@ -534,63 +534,78 @@ __global__ void soa_h_restrict_kernel(const __grid_constant__ HArgs h, int W, co
   rc[2 * t + 1] = acc[1];
 }
 
-// every slot of the fine records (duplicates included) += its prolongation from the coarse level
+// x_f += P_h e_c on p = 1 facet records (multigrid.py:229-298, 403), one thread per coarse element (I, J):
+// it loads the element's four coarse sides once and updates the eight fine facets they determine - the
+// four cross facets inside the element and the two halves each of its bottom and left coarse facets
+// (every fine facet belongs to exactly one coarse element this way).  A fine facet that is stored twice
+// (H column on a tile seam; V line that is a neighbouring tile's edge-in line) is updated in every copy.
+__device__ __forceinline__ void rec2_add_h(double* __restrict__ xf, int W, int c, int j, const double* add) {
+  const int w = min(c / 31, W - 1);
+  double* p = xf + ((long long)j * W + w) * SoaCfg<2>::ENT + (c - 31 * w);
+  p[0] += add[0]; p[32] += add[1];
+  if (c == 31 * w && w > 0) {                    // slot 0 of tile w = slot 31 of tile w - 1
+    double* q = p - SoaCfg<2>::ENT + 31;
+    q[0] += add[0]; q[32] += add[1];
+  }
+}
+__device__ __forceinline__ void rec2_add_v(double* __restrict__ xf, int W, int i, int j, const double* add) {
+  using C = SoaCfg<2>;
+  const int w = (i - 1) / 31;
+  double* rec = xf + ((long long)(j + 1) * W) * C::ENT;
+  double* p = rec + (long long)w * C::ENT + C::VOFF + (i - 31 * w - 1);
+  p[0] += add[0]; p[31] += add[1];
+  if (i % 31 == 0 && i / 31 < W) {               // left-in line of tile i / 31
+    double* q = rec + (long long)(i / 31) * C::ENT + C::EOFF;
+    q[0] += add[0]; q[1] += add[1];
+  }
+  if (i >= 32 && (i - 32) % 31 == 0) {           // right-in line of tile (i - 32) / 31
+    double* q = rec + (long long)((i - 32) / 31) * C::ENT + C::EOFF + C::EB;
+    q[0] += add[0]; q[1] += add[1];
+  }
+}
+
 template <bool SC>
 __global__ void soa_h_prolong_kernel(const __grid_constant__ HArgs h, int W, int nxf, int nyf,
                                      const double* __restrict__ ec, double* __restrict__ xf) {
-  using C = SoaCfg<2>;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nrec = (long long)(nyf + 1) * W;
   grid_dependency_wait();
-  if (t >= nrec * 65) return;
-  const long long rw = t / 65;
-  const int s = (int)(t % 65), R = (int)(rw / W), w = (int)(rw % W);
-  int off, st;
-  soa_slot<2>(s, off, st);
-  bool is_h = s < 32;
-  int i, j;   // fine h(i, j): column i, line j; fine v(i, j): line i, row j
-  if (is_h) {
-    i = 31 * w + s; j = R;
-    if (j < 1 || j > nyf - 1 || i >= nxf) return;
-  } else {
-    i = s < 63 ? 31 * w + 1 + (s - 32) : (s == 63 ? 31 * w : 31 * w + 32);
-    j = R - 1;
-    if (j < 0 || i < 1 || i > nxf - 1) return;
-  }
-  double add[2] = {0.0, 0.0};
-  bool half;
-  int I, J, hf = 0, cf = 0;
-  long long cb = 0;
-  if (is_h) {
-    I = i >> 1;
-    half = (j & 1) == 0;
-    if (half) { J = j >> 1; hf = i & 1; cb = (long long)(J - 1) * h.nxc + I; }
-    else { J = (j - 1) >> 1; cf = (i & 1) ? 3 : 2; }
-  } else {
-    J = j >> 1;
-    half = (i & 1) == 0;
-    if (half) { I = i >> 1; hf = j & 1; cb = h.nhc + (long long)(I - 1) * h.nyc + J; }
-    else { I = (i - 1) >> 1; cf = (j & 1) ? 1 : 0; }
-  }
-  if (half) {
-    const double2 e = __ldg(reinterpret_cast<const double2*>(ec) + cb);
-    for (int k = 0; k < 2; ++k) add[k] = h.halves[hf * 4 + k * 2] * e.x + h.halves[hf * 4 + k * 2 + 1] * e.y;
-  } else {
-    const double* tm = hcross<SC>(h, I, J, cf);
+  if (t >= (long long)h.nxc * h.nyc) return;
+  const int J = (int)(t / h.nxc), I = (int)(t - (long long)J * h.nxc);
+  double sd[4][2];
 #pragma unroll
-    for (int sd = 0; sd < 4; ++sd) {
-      double v[2];
-      coarse_side<false>(h, ec, I, J, sd, v);
+  for (int s = 0; s < 4; ++s) coarse_side<false>(h, ec, I, J, s, sd[s]);
+  // cross facets: right of SW = v(2I+1, 2J), right of NW = v(2I+1, 2J+1), top of SW = h(2I, 2J+1),
+  // top of SE = h(2I+1, 2J+1)
+#pragma unroll
+  for (int cf = 0; cf < 4; ++cf) {
+    const double* tm = hcross<SC>(h, I, J, cf);
+    double add[2] = {0.0, 0.0};
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
-        if constexpr (SC) add[k] += tm[k * 8 + sd * 2] * v[0] + tm[k * 8 + sd * 2 + 1] * v[1];
-        else add[k] += __ldg(tm + k * 8 + sd * 2) * v[0] + __ldg(tm + k * 8 + sd * 2 + 1) * v[1];
+        if constexpr (SC) add[k] += tm[k * 8 + s * 2] * sd[s][0] + tm[k * 8 + s * 2 + 1] * sd[s][1];
+        else add[k] += __ldg(tm + k * 8 + s * 2) * sd[s][0] + __ldg(tm + k * 8 + s * 2 + 1) * sd[s][1];
       }
+    if (cf < 2) rec2_add_v(xf, W, 2 * I + 1, 2 * J + cf, add);
+    else rec2_add_h(xf, W, 2 * I + (cf - 2), 2 * J + 1, add);
+  }
+  // halves of the bottom coarse facet h(I, J) (J >= 1) and of the left one v(I, J) (I >= 1)
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+    double add[2];
+    if (J >= 1) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) add[k] = h.halves[hf * 4 + k * 2] * sd[0][0] + h.halves[hf * 4 + k * 2 + 1] * sd[0][1];
+      rec2_add_h(xf, W, 2 * I + hf, 2 * J, add);
+    }
+    if (I >= 1) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) add[k] = h.halves[hf * 4 + k * 2] * sd[3][0] + h.halves[hf * 4 + k * 2 + 1] * sd[3][1];
+      rec2_add_v(xf, W, 2 * I, 2 * J + hf, add);
     }
   }
-  double* x = xf + rw * C::ENT + off;
-  x[0] += add[0];
-  x[st] += add[1];
+  (void)nxf; (void)nyf;
 }
 
 // a.b (and c.e when c != nullptr) of record vectors over the trace dofs, every dof once: slot 31 of an H
