@@ -186,8 +186,9 @@ int hdg_mg_set_fused_tail(hdg_mg* mg, int enable);
  * p-prolongation + first post-sweep are single passes); b is packed and x unpacked at the
  * cycle's boundary, the levels below m use the reference layout.  mode 0: off, 1 (default):
  * when level 0 has p >= 2 and >= 2^13 dofs (env HDG_REC_MIN_DOF), 2: whenever the levels qualify, 3: as 2
- * with the p-prolongation as its own kernel.  hdg_mg_record_levels returns m of the last
- * cycle (0: reference layout). */
+ * with the p-prolongation as its own kernel, 4: as 2 with every qualifying h-coarsened level on
+ * records too (automatically: those with >= 50k dofs, env HDG_REC_H_MIN_DOF; record-to-record
+ * h-transfers).  hdg_mg_record_levels returns m of the last cycle (0: reference layout). */
 int hdg_mg_set_records(hdg_mg* mg, int mode);
 int hdg_mg_record_levels(const hdg_mg* mg);
 /* hdg_mg_cycle on vectors that already live as facet records of level 0 (hdg_soa_pack): no

@@ -1078,8 +1078,10 @@ int hdg_mg_destroy(hdg_mg* mg) {
 }
 
 int hdg_mg_set_records(hdg_mg* mg, int mode) {
-  if (!mg || mode < 0 || mode > 3) return fail(HDG_EINVAL, "record mode must be 0 (off), 1 (auto), 2 (on), 3 (on, unfused prolongation)");
-  mg->rec_mode = mode == 3 ? 2 : mode;
+  if (!mg || mode < 0 || mode > 4)
+    return fail(HDG_EINVAL, "record mode must be 0 (off), 1 (auto), 2 (on), 3 (on, unfused), 4 (on, every h-level)");
+  mg->rec_mode = mode >= 3 ? 2 : mode;
+  mg->rec_h_all = mode == 4;
   mg->rec_fuse_prolong = mode != 3;
   mg->rec_fold_first = mode != 3;
   for (auto& kv : mg->graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -1358,6 +1360,16 @@ static long long rec_min_dof() {
   return v;
 }
 
+static long long rec_h_min_dof() {
+  static long long v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("HDG_REC_H_MIN_DOF");
+    v = e ? std::atoll(e) : 50000;   // measured on the configs[1] hierarchy: 0.746 ms without, 0.728 / 0.725 / 0.722 ms
+                                     // with the levels down to 512^2 / 256^2 / 128^2 on records
+  }
+  return v;
+}
+
 static int rec_find(hdg_mg* mg) {
   if (mg->rec_mode == 0 || mg->n < 2) return 0;
   hdg_level* L0 = mg->L[0];
@@ -1380,6 +1392,19 @@ static int rec_find(hdg_mg* mg) {
       break;
     }
   }
+  // h-coarsened p = 1 levels that are still large keep their vectors as records too (record-to-record
+  // h-transfers); the first level below them is the reference-layout one
+  while (m >= 1 && m + 1 < mg->n) {
+    hdg_level* L = mg->L[m];
+    const HArgs& h = mg->T[m]->ha;
+    if (L->stored || L->blk.empty() || L->n1 != 2 || !L->has_bj || L->use_fsai ||
+        (!mg->rec_h_all && L->ndof < rec_h_min_dof()) ||
+        !mg->T[m]->is_h || h.jf0 != 0 || h.jc0 != 0 || h.nyf != 2 * h.nyc || L->nx != 2 * h.nxc || L->ny != h.nyf)
+      break;
+    if (soa_prepare(L)) break;
+    soa_prepare_bj0(L);
+    ++m;
+  }
   return m;
 }
 
@@ -1399,8 +1424,10 @@ static int rec_prepare(hdg_mg* mg) {
     CK(cudaMalloc(&a, bytes)); mg->Xr.push_back(a);
     CK(cudaMalloc(&b, bytes)); mg->Tr.push_back(b);
     CK(cudaMalloc(&c, bytes)); mg->Br.push_back(c);
+    CK(cudaMemset(c, 0, bytes));   // a record-to-record restriction writes facet slots only
   }
-  if (m > 0) CK(cudaMalloc(&mg->Rr, sizeof(double) * (size_t)soa_len(mg->L[m - 1])));
+  for (int k = 0; k < m && !mg->Rr; ++k)   // residual records of the h-linked levels: the first is the largest
+    if (mg->T[k]->is_h) CK(cudaMalloc(&mg->Rr, sizeof(double) * (size_t)soa_len(mg->L[k])));
   return 0;
 }
 
@@ -1450,6 +1477,15 @@ static int cycle_rec_soa(hdg_mg* mg, int k, const double* b, const double* x_in,
     } else if ((rc = soa_cyc_p_prolong(L, mg->L[k + 1], xc, const_cast<double*>(cur), T->pa.V, s))) {
       return rc;
     }
+  } else if (k + 1 < mg->rec_m) {
+    // h-link between two record levels
+    hdg_level* Lc = mg->L[k + 1];
+    if ((rc = soa_cyc_sweep(L, SOA_EPI_RES, cur, b, mg->Rr, 0.0, 0.0, nullptr, nullptr, s))) return rc;
+    if ((rc = soa_cyc_h_restrict(L, T->ha, mg->Rr, mg->Br[k + 1], s, Lc))) return rc;
+    double* xc = nullptr;
+    for (int v = 0; v < visits; ++v)
+      if ((rc = cycle_rec_soa(mg, k + 1, mg->Br[k + 1], xc, &xc, nu1, nu2, visits, s))) return rc;
+    if ((rc = soa_cyc_h_prolong(L, T->ha, xc, const_cast<double*>(cur), s, Lc))) return rc;
   } else {
     if ((rc = soa_cyc_sweep(L, SOA_EPI_RES, cur, b, mg->Rr, 0.0, 0.0, nullptr, nullptr, s))) return rc;
     if ((rc = soa_cyc_h_restrict(L, T->ha, mg->Rr, mg->B[k + 1], s))) return rc;

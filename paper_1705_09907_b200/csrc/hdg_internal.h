@@ -131,6 +131,7 @@ struct hdg_mg {
   int rec_m = 0;
   bool rec_fuse_prolong = true;  // p-prolongation inside the first post-smoothing sweep
   bool rec_fold_first = true;    // zero-start double sweep in its folded form (p <= 4)
+  bool rec_h_all = false;        // every qualifying h-coarsened level on records, whatever its size (tests)
   std::vector<double*> Xr, Tr, Br;
   double* Rr = nullptr;
 };
@@ -146,8 +147,10 @@ int soa_cyc_sweep(const hdg_level* L, int epi, const double* x, const double* b,
                   const double* V, const double* ec, cudaStream_t s);
 int soa_cyc_p_prolong(const hdg_level* Lf, const hdg_level* Lc, const double* ec, double* xf, const double* V,
                       cudaStream_t s);
-int soa_cyc_h_restrict(const hdg_level* Lf, const HArgs& h, const double* rf, double* rc, cudaStream_t s);
-int soa_cyc_h_prolong(const hdg_level* Lf, const HArgs& h, const double* ec, double* xf, cudaStream_t s);
+int soa_cyc_h_restrict(const hdg_level* Lf, const HArgs& h, const double* rf, double* rc, cudaStream_t s,
+                       const hdg_level* Lc = nullptr);
+int soa_cyc_h_prolong(const hdg_level* Lf, const HArgs& h, const double* ec, double* xf, cudaStream_t s,
+                      const hdg_level* Lc = nullptr);
 int soa_cyc_norm2(const hdg_level* L, const double* r, double* out, double* partials, int nblocks, cudaStream_t s);
 int soa_cyc_dot2(const hdg_level* L, const double* a, const double* b, double* out, const double* c, const double* e,
                  double* out2, double* partials, int nblocks, cudaStream_t s);

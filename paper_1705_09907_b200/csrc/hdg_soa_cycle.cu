@@ -108,26 +108,41 @@ static int h_check(const hdg_level* Lf, const HArgs& h) {
   return 0;
 }
 
-int soa_cyc_h_restrict(const hdg_level* Lf, const HArgs& h, const double* rf, double* rc, cudaStream_t s) {
+// Lc != nullptr: the coarse vector is a record vector of level Lc (its non-facet slots must be zero)
+int soa_cyc_h_restrict(const hdg_level* Lf, const HArgs& h, const double* rf, double* rc, cudaStream_t s,
+                       const hdg_level* Lc) {
   int rc0 = h_check(Lf, h);
   if (rc0) return rc0;
   const long long n = h.nhc + (long long)(h.nxc - 1) * h.nyc;
   if (n == 0) return 0;
   const unsigned grid = (unsigned)((n + 127) / 128);
-  if (h.shared_cross) launch_pdl(soa_h_restrict_kernel<true>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, rf, rc);
-  else launch_pdl(soa_h_restrict_kernel<false>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, rf, rc);
+  const int Wc = Lc ? Lc->soaW : 0;
+  if (Lc) {
+    if (h.shared_cross) launch_pdl(soa_h_restrict_kernel<true, true>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, rf, rc, Wc);
+    else launch_pdl(soa_h_restrict_kernel<false, true>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, rf, rc, Wc);
+  } else {
+    if (h.shared_cross) launch_pdl(soa_h_restrict_kernel<true, false>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, rf, rc, Wc);
+    else launch_pdl(soa_h_restrict_kernel<false, false>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, rf, rc, Wc);
+  }
   CKL();
   return 0;
 }
 
-int soa_cyc_h_prolong(const hdg_level* Lf, const HArgs& h, const double* ec, double* xf, cudaStream_t s) {
+int soa_cyc_h_prolong(const hdg_level* Lf, const HArgs& h, const double* ec, double* xf, cudaStream_t s,
+                      const hdg_level* Lc) {
   int rc0 = h_check(Lf, h);
   if (rc0) return rc0;
   const long long n = (long long)h.nxc * h.nyc;           // one thread per coarse element
   if (n == 0) return 0;
   const unsigned grid = (unsigned)((n + 127) / 128);
-  if (h.shared_cross) launch_pdl(soa_h_prolong_kernel<true>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf);
-  else launch_pdl(soa_h_prolong_kernel<false>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf);
+  const int Wc = Lc ? Lc->soaW : 0;
+  if (Lc) {
+    if (h.shared_cross) launch_pdl(soa_h_prolong_kernel<true, true>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf, Wc);
+    else launch_pdl(soa_h_prolong_kernel<false, true>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf, Wc);
+  } else {
+    if (h.shared_cross) launch_pdl(soa_h_prolong_kernel<true, false>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf, Wc);
+    else launch_pdl(soa_h_prolong_kernel<false, false>, dim3(grid), dim3(128), 0, s, h, Lf->soaW, Lf->nx, Lf->ny, ec, xf, Wc);
+  }
   CKL();
   return 0;
 }

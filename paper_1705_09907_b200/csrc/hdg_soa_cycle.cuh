@@ -499,9 +499,37 @@ __device__ __forceinline__ void rec2_cross_restrict(const HArgs& h, int W, const
   }
 }
 
-template <bool SC>
+// store helpers for p = 1 records: every copy of a facet (see rec2_add_h / rec2_add_v)
+__device__ __forceinline__ void rec2_set_h(double* __restrict__ x, int W, int c, int j, double v0, double v1) {
+  const int w = min(c / 31, W - 1);
+  double* p = x + ((long long)j * W + w) * SoaCfg<2>::ENT + (c - 31 * w);
+  p[0] = v0; p[32] = v1;
+  if (c == 31 * w && w > 0) {
+    double* q = p - SoaCfg<2>::ENT + 31;
+    q[0] = v0; q[32] = v1;
+  }
+}
+__device__ __forceinline__ void rec2_set_v(double* __restrict__ x, int W, int i, int j, double v0, double v1) {
+  using C = SoaCfg<2>;
+  const int w = (i - 1) / 31;
+  double* rec = x + ((long long)(j + 1) * W) * C::ENT;
+  double* p = rec + (long long)w * C::ENT + C::VOFF + (i - 31 * w - 1);
+  p[0] = v0; p[31] = v1;
+  if (i % 31 == 0 && i / 31 < W) {
+    double* q = rec + (long long)(i / 31) * C::ENT + C::EOFF;
+    q[0] = v0; q[1] = v1;
+  }
+  if (i >= 32 && (i - 32) % 31 == 0) {
+    double* q = rec + (long long)((i - 32) / 31) * C::ENT + C::EOFF + C::EB;
+    q[0] = v0; q[1] = v1;
+  }
+}
+
+// CREC: the coarse vector is a p = 1 record vector too (Wc tiles; every slot that is not a facet stays
+// the zero it was allocated with), else the reference layout
+template <bool SC, bool CREC = false>
 __global__ void soa_h_restrict_kernel(const __grid_constant__ HArgs h, int W, const double* __restrict__ rf,
-                                      double* __restrict__ rc) {
+                                      double* __restrict__ rc, int Wc = 0) {
   const long long nvc = (long long)(h.nxc - 1) * h.nyc;
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   grid_dependency_wait();
@@ -516,6 +544,7 @@ __global__ void soa_h_restrict_kernel(const __grid_constant__ HArgs h, int W, co
     }
     rec2_cross_restrict<SC>(h, W, rf, I, J - 1, 2, acc);
     rec2_cross_restrict<SC>(h, W, rf, I, J, 0, acc);
+    if constexpr (CREC) { rec2_set_h(rc, Wc, I, J, acc[0], acc[1]); return; }
   } else {           // coarse v(I, J): children fine v(2I, 2J), v(2I, 2J+1)
     // consecutive threads walk I (neighbouring slots of the same fine records: coalesced reads); the
     // coarse vector is vertical-line-major, so the two 8-byte stores are the scattered side
@@ -529,6 +558,7 @@ __global__ void soa_h_restrict_kernel(const __grid_constant__ HArgs h, int W, co
     }
     rec2_cross_restrict<SC>(h, W, rf, I - 1, J, 1, acc);
     rec2_cross_restrict<SC>(h, W, rf, I, J, 3, acc);
+    if constexpr (CREC) { rec2_set_v(rc, Wc, I, J, acc[0], acc[1]); return; }
   }
   rc[2 * t] = acc[0];
   rc[2 * t + 1] = acc[1];
@@ -564,16 +594,32 @@ __device__ __forceinline__ void rec2_add_v(double* __restrict__ xf, int W, int i
   }
 }
 
-template <bool SC>
+// side s of coarse element (I, J) from a coarse p = 1 record vector (zero on Dirichlet sides)
+__device__ __forceinline__ void coarse_side_rec(const HArgs& h, const double* __restrict__ ec, int Wc, int I, int J,
+                                                int s, double* v) {
+  long long ad = -1;
+  int st = 32;
+  if (s == 0 && J >= 1) ad = rec2_h(Wc, I, J);
+  if (s == 2 && J + 1 <= h.nyc - 1) ad = rec2_h(Wc, I, J + 1);
+  if (s == 3 && I >= 1) { ad = rec2_v(Wc, I, J); st = 31; }
+  if (s == 1 && I + 1 <= h.nxc - 1) { ad = rec2_v(Wc, I + 1, J); st = 31; }
+  v[0] = ad >= 0 ? __ldg(ec + ad) : 0.0;
+  v[1] = ad >= 0 ? __ldg(ec + ad + st) : 0.0;
+}
+
+template <bool SC, bool CREC = false>
 __global__ void soa_h_prolong_kernel(const __grid_constant__ HArgs h, int W, int nxf, int nyf,
-                                     const double* __restrict__ ec, double* __restrict__ xf) {
+                                     const double* __restrict__ ec, double* __restrict__ xf, int Wc = 0) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   grid_dependency_wait();
   if (t >= (long long)h.nxc * h.nyc) return;
   const int J = (int)(t / h.nxc), I = (int)(t - (long long)J * h.nxc);
   double sd[4][2];
 #pragma unroll
-  for (int s = 0; s < 4; ++s) coarse_side<false>(h, ec, I, J, s, sd[s]);
+  for (int s = 0; s < 4; ++s) {
+    if constexpr (CREC) coarse_side_rec(h, ec, Wc, I, J, s, sd[s]);
+    else coarse_side<false>(h, ec, I, J, s, sd[s]);
+  }
   // cross facets: right of SW = v(2I+1, 2J), right of NW = v(2I+1, 2J+1), top of SW = h(2I, 2J+1),
   // top of SE = h(2I+1, 2J+1)
 #pragma unroll

@@ -560,8 +560,8 @@ def set_fused_tail(levels, enable=True):
 
 def set_records(levels, mode=1):
     """Facet-record cycle on the constant-coefficient p-ladder of the finest mesh (hdgb200.h:
-    hdg_mg_set_records): 0 off, 1 automatic (large levels), 2 whenever the levels qualify, 3 as 2
-    with the p-prolongation as a separate kernel."""
+    hdg_mg_set_records): 0 off, 1 automatic, 2 whenever the levels qualify, 3 as 2 with the
+    p-prolongation as a separate kernel, 4 as 2 with every qualifying h-coarsened level on records too."""
     check(lib.hdg_mg_set_records(_native_mg(levels).handle, int(mode)))
 
 

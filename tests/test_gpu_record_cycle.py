@@ -105,7 +105,7 @@ def test_record_cycle_full_size_configs1(P):
     import torch
     b = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, levels[0].ndof)).cuda()
     x = P.mg.v_cycle(levels, b)
-    assert P.mg.record_levels(levels) == 4
+    assert P.mg.record_levels(levels) == 7                 # the p-ladder and the 512^2, 256^2, 128^2 levels (>= 50k dofs)
     P.mg.set_records(levels, 0)
     xr = P.mg.v_cycle(levels, b)
     assert P.mg.record_levels(levels) == 0
@@ -135,4 +135,20 @@ def test_cycle_on_resident_records(P, nx, ny, p, nu1, nu2, visits):
     P.mg.cycle_records(levels, bp, x0p, nu1, nu2, visits, out=x0p)   # in place
     assert rel(x0p.numpy(), xo) < TOL
     np.testing.assert_array_equal(bp.numpy(), b)
+    P.mg.set_records(levels, 1)
+
+
+@pytest.mark.parametrize("nx,ny,p,visits", [(64, 64, 2, 1), (32, 32, 1, 1), (96, 40, 3, 1), (64, 32, 4, 2)])
+def test_record_cycle_with_h_levels_on_records(P, nx, ny, p, visits):
+    """Mode 4: the h-coarsened p = 1 levels keep their vectors as records too (record-to-record
+    h-transfers, hdg_soa_cycle.cuh: soa_h_restrict_kernel / soa_h_prolong_kernel with CREC)."""
+    levels, lo = _hier(P, nx, ny, p)
+    rng = np.random.default_rng(5 * nx + p)
+    b, x0 = rng.uniform(-1, 1, levels[0].ndof), rng.standard_normal(levels[0].ndof)
+    P.mg.set_records(levels, 4)
+    run = P.mg.v_cycle if visits == 1 else P.mg.w_cycle
+    x = run(levels, b)
+    assert P.mg.record_levels(levels) > p                  # at least one h-level beyond the p-ladder
+    assert rel(x, O.cycle(lo, 0, b, np.zeros_like(b), 2, 2, visits)) < TOL
+    assert rel(run(levels, b, x0), O.cycle(lo, 0, b, x0.copy(), 2, 2, visits)) < TOL
     P.mg.set_records(levels, 1)
