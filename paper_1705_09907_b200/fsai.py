@@ -14,6 +14,7 @@ SpMV kernels (the second fused with the update) per sweep (hdg_fsai_sweeps).
 from __future__ import annotations
 
 import ctypes
+import warnings
 
 import numpy as np
 import scipy.sparse as sp
@@ -95,6 +96,9 @@ def _rows_solve_device(A, pattern):
     counts = np.diff(pattern.indptr)
     max_len = int(counts.max()) if n else 0
     if max_len > 96 or A.nnz >= 2 ** 31 or pattern.nnz >= 2 ** 31:
+        # not silent: the device kernel holds one gathered block of <= 96 x 96 per thread
+        warnings.warn(f"FSAI row solves on the host: pattern rows up to {max_len} entries "
+                      f"(device kernel limit 96) or nnz >= 2^31", RuntimeWarning, stacklevel=2)
         return _rows_solve(A, pattern)
     Acsr = A.tocsr()
     Acsr.sort_indices()
