@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--smoother", default="baseline", help="baseline (the reference FSAI, device setup) | blockjacobi")
     ap.add_argument("--nu", type=int, default=2, help="pre- and post-smoothing sweeps")
     ap.add_argument("--hist", default=None, help="write the PCG residual history here")
+    ap.add_argument("--true-residual", action="store_true",
+                    help="after the reference stopping test (recursive residual, trace.py:153) passes, recompute "
+                         "b - A x and restart PCG from x while the TRUE residual is above tol (at most 3 restarts)")
     a = ap.parse_args()
     rng = np.random.default_rng(2)
     Kg = np.exp(rng.uniform(np.log(1e-2), np.log(1e2), (a.n, a.n)))
@@ -71,6 +74,20 @@ def main():
     t_solve = time.time() - t1
     r = b - levels[0].matvec(xs)
     relres = float(torch.linalg.vector_norm(r) / torch.linalg.vector_norm(b))
+    first_relres, restarts, restart_iters = relres, 0, 0
+    first_hist = getattr(levels[0].system, "cg_residuals", None)
+    while a.true_residual and relres > a.tol and restarts < 3:
+        del r
+        # restart: hdg_pcg with x0 recomputes r = b - A x0, so its stopping test starts from the true residual
+        xs, it2 = levels[0].system.solve_cg(tol=a.tol, maxiter=a.maxiter, precond=mg_preconditioner(levels, a.nu, a.nu),
+                                            b=b, x0=xs)
+        torch.cuda.synchronize()
+        restarts, restart_iters = restarts + 1, restart_iters + it2
+        r = b - levels[0].matvec(xs)
+        relres = float(torch.linalg.vector_norm(r) / torch.linalg.vector_norm(b))
+    t_total = time.time() - t1
+    if first_hist is not None:
+        levels[0].system.cg_residuals = first_hist
     hist = getattr(levels[0].system, "cg_residuals", None)
     if a.hist and hist is not None:
         np.savetxt(a.hist, np.asarray(hist) / float(torch.linalg.vector_norm(b)), header="||r_k|| / ||b||, k = 0..iters")
@@ -78,7 +95,9 @@ def main():
                       "ndof": ndof, "levels": len(levels), "setup_s": round(t_setup, 2),
                       "fsai_setup_s": round(fsai_s, 2),
                       "vcycle_ms": round(vms, 3), "pcg_iterations": iters, "solve_s": round(t_solve, 3),
-                      "final_rel_residual": relres, "gpu_mem_used_GB": round((total - free) / 1e9, 1),
+                      "final_rel_residual": relres, "true_residual_restarts": restarts,
+                      "restart_iterations": restart_iters, "rel_residual_at_reference_stop": first_relres,
+                      "solve_with_restarts_s": round(t_total, 3), "gpu_mem_used_GB": round((total - free) / 1e9, 1),
                       "torch_reserved_GB": round(torch.cuda.memory_reserved() / 1e9, 1),
                       "operator_stream_GB": round(sum(lev.block_op.operator_bytes() for lev in levels) / 1e9, 1)}))
 
