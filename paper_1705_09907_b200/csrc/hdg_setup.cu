@@ -14,19 +14,28 @@ namespace {
 // H(K) = Stab + kx Lap0 + ky Lap1 (nb x nb, SPD) eliminated without pivoting on the augmented
 // matrix [H | B] held in shared memory, one CTA per element; threads (ty, tx): tx walks a row
 // (conflict-free), ty the rows below the pivot.  Returns false on a non-positive pivot.
+// PK = true keeps only the upper triangle of H (row i: columns j >= i, then B), which is all the
+// elimination of a symmetric matrix needs (multiplier l_ik = A_ki / d_k): nb ncol - nb (nb - 1) / 2
+// doubles instead of nb ncol, so p = 12 (169 x 221) fits in 227 KB.
+template <bool PK>
+__device__ __forceinline__ int row_base(int i, int ld, int ncol) {
+  return PK ? i * ncol - (i * (i + 1)) / 2 : i * ld;
+}
+
+template <bool PK>
 __device__ __forceinline__ bool eliminate(double* A, int nb, int ncol, int ld, double* dinv) {
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, nty = blockDim.x >> 5;
   bool ok = true;
   for (int k = 0; k < nb; ++k) {
-    const double d = A[k * ld + k];
+    const double* rk = A + row_base<PK>(k, ld, ncol);
+    const double d = rk[k];
     if (!(d > 0.0)) ok = false;
     const double inv = 1.0 / d;
     if (threadIdx.x == 0) dinv[k] = inv;
-    const double* rk = A + k * ld;
     for (int i = k + 1 + ty; i < nb; i += nty) {
-      double* ri = A + i * ld;
-      const double l = ri[k] * inv;
-      for (int j = k + 1 + tx; j < ncol; j += 32) ri[j] = fma(-l, rk[j], ri[j]);
+      double* ri = A + row_base<PK>(i, ld, ncol);
+      const double l = (PK ? rk[i] : ri[k]) * inv;
+      for (int j = (PK ? i : k + 1) + tx; j < ncol; j += 32) ri[j] = fma(-l, rk[j], ri[j]);
     }
     __syncthreads();
   }
@@ -34,6 +43,7 @@ __device__ __forceinline__ bool eliminate(double* A, int nb, int ncol, int ld, d
 }
 
 // S_e = kx A00 + ky A01 + Ms - B^T H^-1 B,  B = Tu - kx G0 - ky G1   (C = -B^T: Fq = Tq^T, Fu = -Tu^T)
+template <bool PK>
 __global__ void __launch_bounds__(256) condense_kernel(int nb, int m, long long E, const double* __restrict__ kx,
                                                        const double* __restrict__ ky, const double* __restrict__ stab,
                                                        const double* __restrict__ lap0, const double* __restrict__ lap1,
@@ -44,24 +54,27 @@ __global__ void __launch_bounds__(256) condense_kernel(int nb, int m, long long 
   extern __shared__ __align__(16) double sm[];
   const int ncol = nb + m, ld = ncol | 1;
   double* A = sm;
-  double* dinv = sm + (size_t)nb * ld;
+  double* dinv = sm + (PK ? (size_t)nb * ncol - (size_t)nb * (nb - 1) / 2 : (size_t)nb * ld);
   for (long long e = blockIdx.x; e < E; e += gridDim.x) {
     const double a = kx[e], b = ky[e];
     for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
       const int i = t / nb, j = t - i * nb;
-      A[i * ld + j] = stab[t] + a * lap0[t] + b * lap1[t];
+      if (!PK || j >= i) A[row_base<PK>(i, ld, ncol) + j] = stab[t] + a * lap0[t] + b * lap1[t];
     }
     for (int t = threadIdx.x; t < nb * m; t += blockDim.x) {
       const int i = t / m, j = t - i * m;
-      A[i * ld + nb + j] = tu[t] - a * g0[t] - b * g1[t];
+      A[row_base<PK>(i, ld, ncol) + nb + j] = tu[t] - a * g0[t] - b * g1[t];
     }
     __syncthreads();
-    if (!eliminate(A, nb, ncol, ld, dinv) && threadIdx.x == 0) atomicExch(status, 1);
+    if (!eliminate<PK>(A, nb, ncol, ld, dinv) && threadIdx.x == 0) atomicExch(status, 1);
     double* out = S + e * (long long)m * m;
     for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
       const int r = t / m, c = t - r * m;
       double acc = 0.0;
-      for (int k = 0; k < nb; ++k) acc = fma(A[k * ld + nb + r] * dinv[k], A[k * ld + nb + c], acc);
+      for (int k = 0; k < nb; ++k) {
+        const double* bk = A + row_base<PK>(k, ld, ncol) + nb;
+        acc = fma(bk[r] * dinv[k], bk[c], acc);
+      }
       out[t] = a * a00[t] + b * a01[t] + ms[t] - acc;
     }
     __syncthreads();
@@ -69,6 +82,7 @@ __global__ void __launch_bounds__(256) condense_kernel(int nb, int m, long long 
 }
 
 // u_e = H(K_e)^-1 rhs_e in place (rhs: E x nb)
+template <bool PK>
 __global__ void __launch_bounds__(256) usolve_kernel(int nb, long long E, const double* __restrict__ kx,
                                                      const double* __restrict__ ky, const double* __restrict__ stab,
                                                      const double* __restrict__ lap0, const double* __restrict__ lap1,
@@ -76,29 +90,30 @@ __global__ void __launch_bounds__(256) usolve_kernel(int nb, long long E, const 
   extern __shared__ __align__(16) double sm[];
   const int ncol = nb + 1, ld = ncol | 1;
   double* A = sm;
-  double* dinv = sm + (size_t)nb * ld;
+  double* dinv = sm + (PK ? (size_t)nb * ncol - (size_t)nb * (nb - 1) / 2 : (size_t)nb * ld);
   for (long long e = blockIdx.x; e < E; e += gridDim.x) {
     const double a = kx[e], b = ky[e];
     for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
       const int i = t / nb, j = t - i * nb;
-      A[i * ld + j] = stab[t] + a * lap0[t] + b * lap1[t];
+      if (!PK || j >= i) A[row_base<PK>(i, ld, ncol) + j] = stab[t] + a * lap0[t] + b * lap1[t];
     }
-    for (int t = threadIdx.x; t < nb; t += blockDim.x) A[t * ld + nb] = rhs[e * nb + t];
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) A[row_base<PK>(t, ld, ncol) + nb] = rhs[e * nb + t];
     __syncthreads();
-    if (!eliminate(A, nb, ncol, ld, dinv) && threadIdx.x == 0) atomicExch(status, 1);
+    if (!eliminate<PK>(A, nb, ncol, ld, dinv) && threadIdx.x == 0) atomicExch(status, 1);
     // back substitution on the upper triangle, one warp: u_k = (y_k - sum_{j > k} U_kj u_j) / U_kk
     if (threadIdx.x < 32) {
       for (int k = nb - 1; k >= 0; --k) {
+        double* rk = A + row_base<PK>(k, ld, ncol);
         double s = 0.0;
-        for (int j = k + 1 + (int)threadIdx.x; j < nb; j += 32) s = fma(A[k * ld + j], A[j * ld + nb], s);
+        for (int j = k + 1 + (int)threadIdx.x; j < nb; j += 32) s = fma(rk[j], A[row_base<PK>(j, ld, ncol) + nb], s);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (threadIdx.x == 0) A[k * ld + nb] = (A[k * ld + nb] - s) * dinv[k];
+        if (threadIdx.x == 0) rk[nb] = (rk[nb] - s) * dinv[k];
         __syncwarp();
       }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < nb; t += blockDim.x) rhs[e * nb + t] = A[t * ld + nb];
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) rhs[e * nb + t] = A[row_base<PK>(t, ld, ncol) + nb];
     __syncthreads();
   }
 }
@@ -294,12 +309,15 @@ int hdg_condense_piecewise(int nb, int m, int64_t E, const double* kx, const dou
   if (nb < 1 || m < 1 || E < 0 || !kx || !ky || !S_out || !status) return fail(HDG_EINVAL, "condense: bad argument");
   if (E == 0) return 0;
   const int ld = (nb + m) | 1;
-  const size_t smem = sizeof(double) * ((size_t)nb * ld + nb);
-  if (smem > 227 * 1024) return fail(HDG_EINVAL, "condense: the augmented element matrix exceeds shared memory (p > 11)");
-  CK(cudaFuncSetAttribute(condense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  size_t smem = sizeof(double) * ((size_t)nb * ld + nb);
+  const bool packed = smem > 227 * 1024;                     // p = 12: upper triangle of H only
+  if (packed) smem = sizeof(double) * ((size_t)nb * (nb + m) - (size_t)nb * (nb - 1) / 2 + nb);
+  if (smem > 227 * 1024) return fail(HDG_EINVAL, "condense: the augmented element matrix exceeds shared memory (p > 12)");
+  auto kern = packed ? condense_kernel<true> : condense_kernel<false>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, condense_kernel, 256, smem);
-  condense_kernel<<<grid_for_elements(E, occ < 1 ? 1 : occ), 256, smem, S(stream)>>>(
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+  kern<<<grid_for_elements(E, occ < 1 ? 1 : occ), 256, smem, S(stream)>>>(
       nb, m, E, kx, ky, stab, lap0, lap1, tu, g0, g1, a00, a01, ms, S_out, status);
   CKL();
   return 0;
@@ -310,13 +328,15 @@ int hdg_piecewise_usolve(int nb, int64_t E, const double* kx, const double* ky, 
   if (nb < 1 || E < 0 || !kx || !ky || !rhs || !status) return fail(HDG_EINVAL, "usolve: bad argument");
   if (E == 0) return 0;
   const int ld = (nb + 1) | 1;
-  const size_t smem = sizeof(double) * ((size_t)nb * ld + nb);
-  if (smem > 227 * 1024) return fail(HDG_EINVAL, "usolve: the element matrix exceeds shared memory (p > 11)");
-  CK(cudaFuncSetAttribute(usolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  size_t smem = sizeof(double) * ((size_t)nb * ld + nb);
+  const bool packed = smem > 227 * 1024;                     // p = 12: upper triangle of H only
+  if (packed) smem = sizeof(double) * ((size_t)nb * (nb + 1) - (size_t)nb * (nb - 1) / 2 + nb);
+  if (smem > 227 * 1024) return fail(HDG_EINVAL, "usolve: the element matrix exceeds shared memory (p > 15)");
+  auto kern = packed ? usolve_kernel<true> : usolve_kernel<false>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, usolve_kernel, 256, smem);
-  usolve_kernel<<<grid_for_elements(E, occ < 1 ? 1 : occ), 256, smem, S(stream)>>>(nb, E, kx, ky, stab, lap0, lap1,
-                                                                                    rhs, status);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+  kern<<<grid_for_elements(E, occ < 1 ? 1 : occ), 256, smem, S(stream)>>>(nb, E, kx, ky, stab, lap0, lap1, rhs, status);
   CKL();
   return 0;
 }

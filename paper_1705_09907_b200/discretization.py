@@ -369,8 +369,9 @@ class PiecewiseCondenser:
 
     def blocks(self, K):
         """S for every element; K: (E,) isotropic or a (Kxx, Kyy) pair of (E,) arrays.  One CTA per
-        element eliminates [H | B] in shared memory (hdgb200.h: hdg_condense_piecewise); orders
-        whose augmented matrix exceeds shared memory (p = 12) use the batched library solve."""
+        element eliminates [H | B] in shared memory (hdgb200.h: hdg_condense_piecewise; from p = 12
+        the kernel keeps only H's upper triangle); orders whose packed matrix still exceeds shared
+        memory (p > 12) use the batched library solve."""
         import torch
         from . import _device as dev
         from ._lib import check, lib
@@ -378,7 +379,7 @@ class PiecewiseCondenser:
         kx, ky = self._kpair(K)
         E, m, nb = kx.numel(), 4 * self.n1, self.nb
         out = torch.empty((E, m, m), dtype=torch.float64, device="cuda")
-        if 8 * (nb * ((nb + m) | 1) + nb) > 227 * 1024:
+        if 8 * (nb * (nb + m) - nb * (nb - 1) // 2 + nb) > 227 * 1024:
             return self._blocks_library(kx, ky, out)
         status = torch.zeros(1, dtype=torch.int32, device="cuda")
         check(lib.hdg_condense_piecewise(nb, m, E, kx.data_ptr(), ky.data_ptr(), t["stab"].data_ptr(),

@@ -72,10 +72,12 @@ def test_galerkin_kernels(P, p):
     assert rel(D.galerkin_h(cu(Sch[:1]), Q[:1]).cpu().numpy(), D.galerkin_h(Sch[:1], Q[:1])) < 1e-13
 
 
-@pytest.mark.parametrize("p,aniso", [(1, False), (3, True), (4, False), (8, True), (11, False)])
+@pytest.mark.parametrize("p,aniso", [(1, False), (3, True), (4, False), (8, True), (11, False), (12, False),
+                                     (12, True)])
 def test_condense_and_usolve_vs_dense_algebra(P, p, aniso):
     """hdg_condense_piecewise / hdg_piecewise_usolve against numpy solves of the same flux-first
-    elimination, and (p <= 4) against the oracle's full local LU condensation."""
+    elimination, and (p <= 4) against the oracle's full local LU condensation.  p = 12 runs the
+    packed (upper triangle of H) variant of both kernels."""
     from paper_1705_09907_b200.discretization import PiecewiseCondenser
     rng = np.random.default_rng(10 + p)
     E = 40
