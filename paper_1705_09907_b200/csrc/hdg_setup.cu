@@ -44,7 +44,7 @@ __device__ __forceinline__ bool eliminate(double* A, int nb, int ncol, int ld, d
 
 // S_e = kx A00 + ky A01 + Ms - B^T H^-1 B,  B = Tu - kx G0 - ky G1   (C = -B^T: Fq = Tq^T, Fu = -Tu^T)
 template <bool PK>
-__global__ void __launch_bounds__(256) condense_kernel(int nb, int m, long long E, const double* __restrict__ kx,
+__global__ void __launch_bounds__(PK ? 1024 : 256) condense_kernel(int nb, int m, long long E, const double* __restrict__ kx,
                                                        const double* __restrict__ ky, const double* __restrict__ stab,
                                                        const double* __restrict__ lap0, const double* __restrict__ lap1,
                                                        const double* __restrict__ tu, const double* __restrict__ g0,
@@ -316,8 +316,9 @@ int hdg_condense_piecewise(int nb, int m, int64_t E, const double* kx, const dou
   auto kern = packed ? condense_kernel<true> : condense_kernel<false>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
-  kern<<<grid_for_elements(E, occ < 1 ? 1 : occ), 256, smem, S(stream)>>>(
+  const int threads = packed ? 1024 : 256;                   // one resident CTA per SM when packed: 32 warps
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+  kern<<<grid_for_elements(E, occ < 1 ? 1 : occ), threads, smem, S(stream)>>>(
       nb, m, E, kx, ky, stab, lap0, lap1, tu, g0, g1, a00, a01, ms, S_out, status);
   CKL();
   return 0;
