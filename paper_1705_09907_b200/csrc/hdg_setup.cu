@@ -44,7 +44,7 @@ __device__ __forceinline__ bool eliminate(double* A, int nb, int ncol, int ld, d
 
 // S_e = kx A00 + ky A01 + Ms - B^T H^-1 B,  B = Tu - kx G0 - ky G1   (C = -B^T: Fq = Tq^T, Fu = -Tu^T)
 template <bool PK>
-__global__ void __launch_bounds__(PK ? 1024 : 256) condense_kernel(int nb, int m, long long E, const double* __restrict__ kx,
+__global__ void __launch_bounds__(1024) condense_kernel(int nb, int m, long long E, const double* __restrict__ kx,
                                                        const double* __restrict__ ky, const double* __restrict__ stab,
                                                        const double* __restrict__ lap0, const double* __restrict__ lap1,
                                                        const double* __restrict__ tu, const double* __restrict__ g0,
@@ -316,7 +316,9 @@ int hdg_condense_piecewise(int nb, int m, int64_t E, const double* kx, const dou
   auto kern = packed ? condense_kernel<true> : condense_kernel<false>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 1;
-  const int threads = packed ? 1024 : 256;                   // one resident CTA per SM when packed: 32 warps
+  // one resident CTA per SM (p >= 10) gets 32 warps; with two or more, 8 warps each measured fastest
+  // (profiles/condense_threads_r02.txt: p = 8 24.6 / 36.9 / 32.6 ms at 256 / 512 / 1024; p = 11 192 / 124 / 111)
+  const int threads = (227 * 1024) / smem >= 2 ? 256 : 1024;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   kern<<<grid_for_elements(E, occ < 1 ? 1 : occ), threads, smem, S(stream)>>>(
       nb, m, E, kx, ky, stab, lap0, lap1, tu, g0, g1, a00, a01, ms, S_out, status);

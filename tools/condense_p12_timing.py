@@ -12,7 +12,8 @@ from paper_1705_09907_b200.discretization import PiecewiseCondenser
 
 
 def main():
-    p, E = 12, 1 << 15
+    p = int(sys.argv[1]) if len(sys.argv) > 1 else 12
+    E = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 15
     pc = PiecewiseCondenser(p, 1.0 / 64, 1.0 / 64, 1.0)
     rng = np.random.default_rng(2)
     k = np.exp(rng.uniform(np.log(1e-2), np.log(1e2), E))
